@@ -1,0 +1,167 @@
+"""ctypes binding of libwd_b200.so (include/walldist_b200.h).
+
+The shared library is the only compute path: there is no CPU fallback.  If
+the library is missing or no CUDA device is visible, every compute entry
+point raises :class:`NativeUnavailableError` (the package itself still
+imports, so configuration objects can be built and validated anywhere).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import errors
+
+LIB_NAME = "libwd_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+# status codes / enums (walldist_b200.h)
+WD_OK = 0
+WD_ERR_INVALID = 1
+WD_ERR_LINE_TOO_SHORT = 2
+WD_ERR_ZERO_PIVOT = 3
+WD_ERR_SINGULAR_METRIC = 4
+WD_ERR_NEGATIVE_RADICAND = 5
+WD_ERR_DIVERGED = 6
+WD_ERR_CUDA = 7
+WD_ERR_DIM_TOO_SMALL = 8
+
+SCHEME_IDS = {"UW": 0, "E2": 1, "E4": 2, "E6": 3, "C4": 4, "C6": 5}
+KIND_IDS = {"eikonal": 0, "hj": 1, "hj_lad": 2, "hj_curvature": 3, "poisson": 4}
+FACE_IDS = {None: 0, "wall": 1, "farfield": 2, "periodic": 3}
+
+STATE_RUNNING, STATE_CONVERGED, STATE_DIVERGED, STATE_MAXITERS = 0, 1, 2, 3
+
+
+class NativeUnavailableError(RuntimeError):
+    """libwd_b200.so is not built / loadable, or no CUDA device is present."""
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [
+        ("ndim", ctypes.c_int),
+        ("dims", ctypes.c_int * 3),
+        ("face", ctypes.c_int * 6),
+        ("uniform", ctypes.c_int),
+        ("inv_spacing", ctypes.c_double * 3),
+        ("metrics_dev", ctypes.c_void_p),
+        ("solid_mask_dev", ctypes.c_void_p),
+        ("ref_length", ctypes.c_double),
+    ]
+
+
+class SolverDesc(ctypes.Structure):
+    _fields_ = [
+        ("scheme", ctypes.c_int),
+        ("kind", ctypes.c_int),
+        ("epsilon", ctypes.c_double),
+        ("lad_c", ctypes.c_double),
+        ("eps0", ctypes.c_double),
+        ("use_filter", ctypes.c_int),
+        ("alpha_f", ctypes.c_double),
+        ("cfl", ctypes.c_double),
+        ("tol", ctypes.c_double),
+        ("max_iters", ctypes.c_int),
+    ]
+
+
+class Status(ctypes.Structure):
+    _fields_ = [
+        ("state", ctypes.c_int),
+        ("iters", ctypes.c_int),
+        ("max_iters", ctypes.c_int),
+        ("diverged_iter", ctypes.c_int),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_IP = ctypes.POINTER(ctypes.c_int)
+_DP = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); every symbol declared in walldist_b200.h
+SIGNATURES = {
+    "wd_version": (_I, []),
+    "wd_last_error": (ctypes.c_char_p, []),
+    "wd_device_count": (_I, []),
+    "wd_create": (_I, [ctypes.POINTER(GridDesc), ctypes.POINTER(SolverDesc), _P,
+                       ctypes.POINTER(_P)]),
+    "wd_destroy": (_I, [_P]),
+    "wd_bind": (_I, [_P, _P, _P]),
+    "wd_steps": (_I, [_P, _I]),
+    "wd_read_status": (_I, [_P, ctypes.POINTER(Status)]),
+    "wd_status_async": (_I, [_P, _P]),
+    "wd_finish": (_I, [_P]),
+    "wd_get_stream": (_P, [_P]),
+    "wd_rk4_step": (_I, [_P, _P, _P, _P, _IP]),
+    "wd_tendency": (_I, [_P, _P, _P]),
+    "wd_local_timestep": (_I, [_P, _P, _P]),
+    "wd_apply_bc": (_I, [_P, _P]),
+    "wd_poisson_post": (_I, [_P, _P, _P]),
+    "wd_derivative": (_I, [_P, _P, _I, _IP, _I, _I, _I, _D, _P]),
+    "wd_fourth_derivative": (_I, [_P, _P, _I, _IP, _I, _I, _P]),
+    "wd_filter": (_I, [_P, _P, _P, _I, _IP, _I, _D, _I, _P]),
+    "wd_solve_tridiagonal": (_I, [_DP, _DP, _DP, _P, _I, _I, _P]),
+    "wd_compute_metrics": (_I, [_P, _P, _P, _I, _IP, _I, _IP, _DP, _P]),
+    "wd_linf_delta": (_I, [_P, _P, _P, ctypes.c_longlong, _DP, _P]),
+    "wd_fused_active": (_I, [_P]),
+}
+
+_lib = None
+_load_error = None
+
+
+def load(require_device: bool = False):
+    """Load the library (once).  Raises NativeUnavailableError."""
+    global _lib, _load_error
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            _load_error = (f"{LIB_NAME} is not built at {LIB_PATH}; run "
+                           "`python -c 'import __graft_entry__ as g; g.build()'`")
+            raise NativeUnavailableError(_load_error)
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_device and _lib.wd_device_count() < 1:
+        raise NativeUnavailableError("no CUDA device visible to libwd_b200.so "
+                                     "(the B200 path has no CPU fallback)")
+    return _lib
+
+
+def lib():
+    return load(require_device=True)
+
+
+_ERROR_MAP = {
+    WD_ERR_INVALID: ValueError,
+    WD_ERR_LINE_TOO_SHORT: errors.LineTooShortError,
+    WD_ERR_ZERO_PIVOT: errors.ZeroPivotError,
+    WD_ERR_SINGULAR_METRIC: errors.SingularMetricError,
+    WD_ERR_NEGATIVE_RADICAND: errors.NegativeRadicandError,
+    WD_ERR_DIVERGED: errors.DivergenceError,
+    WD_ERR_DIM_TOO_SMALL: errors.DimensionTooSmallError,
+}
+
+
+def check(rc: int):
+    """Map a WD_ERR_* code to the reference exception class."""
+    if rc == WD_OK:
+        return
+    msg = _lib.wd_last_error().decode() if _lib is not None else "native error"
+    exc = _ERROR_MAP.get(rc)
+    if exc is None:
+        raise RuntimeError(f"libwd_b200 CUDA failure: {msg}")
+    raise exc(msg)
+
+
+def int_array(vals):
+    arr = (ctypes.c_int * len(vals))(*[int(v) for v in vals])
+    return arr
+
+
+def double_array(vals):
+    return (ctypes.c_double * len(vals))(*[float(v) for v in vals])

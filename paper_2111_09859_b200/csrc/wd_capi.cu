@@ -1,0 +1,1067 @@
+// C ABI of libwd_b200.so: solver context, factor precomputation, pseudo-step
+// enqueue (CUDA graphs), operator-level entry points.  See
+// include/walldist_b200.h for the contract and the reference lines each
+// entry point replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "wd_kernels.cuh"
+#include "wd_fused.cuh"
+
+using namespace wd;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(expr)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return fail(WD_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kThreads = 256;
+constexpr int kLineThreads = 64;
+
+int nblocks(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)std::min<long long>(b, 148LL * 32);
+}
+
+int min_line(int scheme) {
+  switch (scheme) {
+    case WD_UW: return 3;
+    case WD_E2: return 3;
+    case WD_E4: return 5;
+    default: return 7;  // E6, C4, C6
+  }
+}
+
+const char* scheme_name(int s) {
+  static const char* names[] = {"UW", "E2", "E4", "E6", "C4", "C6"};
+  return (s >= 0 && s <= 5) ? names[s] : "?";
+}
+
+// ------------------------------------------------------------------ factors
+// Host restatement of LAPACK dgtsv's elimination (oracle/wd.py:gtsv_factor);
+// field-independent, so computed once per matrix.
+struct HostFactor {
+  int n = 0;
+  int cyclic = 0;
+  std::vector<double> fact, d, du, du2, swap, z;
+  double vn = 0.0, denom = 1.0;
+};
+
+int gtsv_factor(int n, const double* lower, const double* diag, const double* upper,
+                HostFactor& F) {
+  F.n = n;
+  F.d.assign(diag, diag + n);
+  std::vector<double> dl(std::max(n - 1, 0)), du(std::max(n - 1, 0));
+  for (int i = 0; i < n - 1; ++i) {
+    dl[i] = lower[i + 1];
+    du[i] = upper[i];
+  }
+  F.fact.assign(std::max(n, 1), 0.0);
+  F.swap.assign(std::max(n, 1), 0.0);
+  auto& d = F.d;
+  for (int i = 0; i < n - 1; ++i) {
+    double f;
+    if (std::fabs(d[i]) >= std::fabs(dl[i])) {
+      if (d[i] == 0.0) return fail(WD_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(i + 1));
+      f = dl[i] / d[i];
+      d[i + 1] = d[i + 1] - f * du[i];
+      dl[i] = 0.0;
+    } else {
+      f = d[i] / dl[i];
+      d[i] = dl[i];
+      double t = d[i + 1];
+      d[i + 1] = du[i] - f * t;
+      if (i < n - 2) {
+        dl[i] = du[i + 1];
+        du[i + 1] = -f * dl[i];
+      }
+      du[i] = t;
+      F.swap[i] = 1.0;
+    }
+    F.fact[i] = f;
+  }
+  if (n > 0 && d[n - 1] == 0.0)
+    return fail(WD_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(n));
+  F.du.assign(std::max(n, 1), 0.0);
+  F.du2.assign(std::max(n, 1), 0.0);
+  for (int i = 0; i < n - 1; ++i) F.du[i] = du[i];
+  for (int i = 0; i < n - 2; ++i) F.du2[i] = dl[i];
+  F.z.assign(std::max(n, 1), 0.0);
+  return WD_OK;
+}
+
+void gtsv_apply_host(const HostFactor& F, std::vector<double>& x) {
+  const int n = F.n;
+  if (n == 1) {
+    x[0] = x[0] / F.d[0];
+    return;
+  }
+  for (int i = 0; i < n - 1; ++i) {
+    const double f = F.fact[i];
+    if (F.swap[i] != 0.0) {
+      double t = x[i];
+      double b1 = x[i + 1];
+      x[i] = b1;
+      x[i + 1] = t - f * b1;
+    } else {
+      x[i + 1] = x[i + 1] - f * x[i];
+    }
+  }
+  x[n - 1] = x[n - 1] / F.d[n - 1];
+  x[n - 2] = (x[n - 2] - F.du[n - 2] * x[n - 1]) / F.d[n - 2];
+  for (int i = n - 3; i >= 0; --i) x[i] = ((x[i] - F.du[i] * x[i + 1]) - F.du2[i] * x[i + 2]) / F.d[i];
+}
+
+// EXTENSION: cyclic constant-coefficient tridiagonal by Sherman-Morrison
+// (oracle/wd.py:cyclic_factor).
+int cyclic_factor(double alpha, int n, HostFactor& F) {
+  const double gamma = -1.0;
+  std::vector<double> lower(n, alpha), upper(n, alpha), diag(n, 1.0);
+  lower[0] = 0.0;
+  upper[n - 1] = 0.0;
+  diag[0] = 1.0 - gamma;
+  diag[n - 1] = 1.0 - alpha * alpha / gamma;
+  int rc = gtsv_factor(n, lower.data(), diag.data(), upper.data(), F);
+  if (rc) return rc;
+  std::vector<double> u(n, 0.0);
+  u[0] = gamma;
+  u[n - 1] = alpha;
+  gtsv_apply_host(F, u);
+  F.z = u;
+  F.vn = alpha / gamma;
+  F.denom = 1.0 + (u[0] + F.vn * u[n - 1]);
+  if (F.denom == 0.0) return fail(WD_ERR_ZERO_PIVOT, "singular cyclic system");
+  F.cyclic = 1;
+  return WD_OK;
+}
+
+int compact_factor(int scheme, int n, int periodic, HostFactor& F) {
+  const double alpha = scheme == WD_C4 ? 0.25 : 1.0 / 3.0;
+  if (periodic) return cyclic_factor(alpha, n, F);
+  std::vector<double> lower(n, alpha), diag(n, 1.0), upper(n, alpha);
+  lower[0] = 0.0;
+  upper[0] = 3.0;
+  upper[n - 1] = 0.0;
+  lower[n - 1] = 3.0;
+  if (scheme == WD_C6) {
+    lower[1] = upper[1] = 0.25;
+    lower[n - 2] = upper[n - 2] = 0.25;
+  }
+  return gtsv_factor(n, lower.data(), diag.data(), upper.data(), F);
+}
+
+int filter_factor(double af, int n, int periodic, HostFactor& F) {
+  if (periodic) return cyclic_factor(af, n, F);
+  std::vector<double> lower(n, af), diag(n, 1.0), upper(n, af);
+  upper[0] = 0.0;
+  lower[n - 1] = 0.0;
+  return gtsv_factor(n, lower.data(), diag.data(), upper.data(), F);
+}
+
+// operators.py:269-295 coefficient expressions, folded as _filter_rhs_row
+// (operators.py:298-302): hc[h][0] = a_0, hc[h][k] = 0.5 * a_k.
+FilterCoef filter_coefs(double af) {
+  FilterCoef c;
+  std::memset(&c, 0, sizeof(c));
+  double a[6][6] = {};
+  a[1][0] = 0.5 + af;
+  a[1][1] = 0.5 + af;
+  a[2][0] = (5.0 + 6.0 * af) / 8.0;
+  a[2][1] = (1.0 + 2.0 * af) / 2.0;
+  a[2][2] = (-1.0 + 2.0 * af) / 8.0;
+  a[3][0] = (11.0 + 10.0 * af) / 16.0;
+  a[3][1] = (15.0 + 34.0 * af) / 32.0;
+  a[3][2] = (-3.0 + 6.0 * af) / 16.0;
+  a[3][3] = (1.0 - 2.0 * af) / 32.0;
+  a[4][0] = (93.0 + 70.0 * af) / 128.0;
+  a[4][1] = (7.0 + 18.0 * af) / 16.0;
+  a[4][2] = (-7.0 + 14.0 * af) / 32.0;
+  a[4][3] = (1.0 - 2.0 * af) / 16.0;
+  a[4][4] = (-1.0 + 2.0 * af) / 128.0;
+  a[5][0] = (193.0 + 126.0 * af) / 256.0;
+  a[5][1] = (105.0 + 302.0 * af) / 256.0;
+  a[5][2] = (-15.0 + 30.0 * af) / 64.0;
+  a[5][3] = (45.0 - 90.0 * af) / 512.0;
+  a[5][4] = (-5.0 + 10.0 * af) / 256.0;
+  a[5][5] = (1.0 - 2.0 * af) / 512.0;
+  for (int h = 1; h <= 5; ++h) {
+    c.hc[h * 6] = a[h][0];
+    for (int k = 1; k <= h; ++k) c.hc[h * 6 + k] = 0.5 * a[h][k];
+  }
+  return c;
+}
+
+// Device image of a HostFactor: 7 arrays of n doubles.
+size_t factor_doubles(int n) { return (size_t)7 * std::max(n, 1); }
+
+TriDev factor_view(const HostFactor& F, double* dev) {
+  const size_t n = std::max(F.n, 1);
+  TriDev T;
+  T.n = F.n;
+  T.cyclic = F.cyclic;
+  T.fact = dev;
+  T.d = dev + n;
+  T.du = dev + 2 * n;
+  T.du2 = dev + 3 * n;
+  T.swap = dev + 4 * n;
+  T.z = dev + 5 * n;
+  T.vn = F.vn;
+  T.denom = F.denom;
+  return T;
+}
+
+void factor_pack(const HostFactor& F, std::vector<double>& out) {
+  const size_t n = std::max(F.n, 1);
+  out.assign(factor_doubles(F.n), 0.0);
+  auto put = [&](int slot, const std::vector<double>& v) {
+    std::copy(v.begin(), v.begin() + std::min(v.size(), n), out.begin() + slot * n);
+  };
+  put(0, F.fact);
+  put(1, F.d);
+  put(2, F.du);
+  put(3, F.du2);
+  put(4, F.swap);
+  put(5, F.z);
+}
+
+Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) {
+  Geom g;
+  std::memset(&g, 0, sizeof(g));
+  g.nd = ndim;
+  for (int a = 0; a < kMaxDim; ++a) g.n[a] = a < ndim ? dims[a] : 1;
+  g.s[2] = 1;
+  g.s[1] = g.n[2];
+  g.s[0] = (long long)g.n[1] * g.n[2];
+  g.N = (long long)g.n[0] * g.n[1] * g.n[2];
+  for (int f = 0; f < 2 * kMaxDim; ++f) g.face[f] = face ? face[f] : WD_FACE_NONE;
+  for (int a = 0; a < kMaxDim; ++a)
+    g.per[a] = a < ndim && face && face[2 * a] == WD_FACE_PERIODIC ? 1 : 0;
+  g.mask = mask;
+  return g;
+}
+
+}  // namespace
+
+// ====================================================================== ctx
+
+struct wd_ctx {
+  wd_grid_desc gd;
+  wd_solver_desc sd;
+  Geom g;
+  Metric M;
+  cudaStream_t stream = nullptr;
+  // factors
+  HostFactor hcomp[3], hfilt[3];
+  TriDev comp[3], filt[3];
+  double* factor_dev = nullptr;
+  FilterCoef fcoef;
+  // per-node metric sums (curvilinear) or scalars (uniform)
+  double* sums_dev = nullptr;  // sumS | cflms | sqrtS[d]
+  double sumS_c = 0, cflms_c = 0, sqrtS_c[3] = {0, 0, 0};
+  // workspace
+  double* ws = nullptr;
+  double *p, *k, *acc, *dt, *lap, *tmp, *tmp2, *gam, *phiY;
+  double *dphi[3], *U[3], *Uh[3], *nrm[3], *B[3], *F[3], *Ue[3];
+  Status* st = nullptr;
+  Status* st_scratch = nullptr;
+  double* hist_scratch = nullptr;
+  int* flag_dev = nullptr;
+  // binding
+  double* phi = nullptr;
+  double* hist = nullptr;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  long long enq = 0;  // host-side count of enqueued steps (buffer parity)
+  FusedPlan fused;    // specialised kernels (wd_fused.cuh), if applicable
+};
+
+namespace {
+
+double lref(const wd_ctx* c) { return c->gd.ref_length; }
+
+Epi epi_plain() { return Epi{0, nullptr, nullptr, 0.0}; }
+
+// coefficient M[l, m] as an epilogue source
+Epi epi_metric(const wd_ctx* c, int l, int m, bool first, double* acc) {
+  Epi e;
+  e.mode = first ? 1 : 2;
+  e.acc = acc;
+  if (c->M.m) {
+    e.cfield = c->M.m + (long long)(l * c->g.nd + m) * c->g.N;
+    e.cscal = 0.0;
+  } else {
+    e.cfield = nullptr;
+    e.cscal = l == m ? c->M.c[l] : 0.0;
+  }
+  return e;
+}
+
+// D_axis(in) with `scheme` (central) -> out via epilogue.  scratch is
+// needed for compact schemes when the epilogue is not plain.
+void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int axis, int scheme,
+                  Epi e, const Status* st) {
+  const Geom& g = c->g;
+  if (scheme == WD_C4 || scheme == WD_C6) {
+    const long long L = g.N / g.n[axis];
+    double* scr = (e.mode == 0) ? out : scratch;
+    k_deriv_compact<<<nblocks(L, kLineThreads), kLineThreads, 0, c->stream>>>(
+        in, scr, out, g, axis, scheme, g.per[axis], 0.0, c->comp[axis], e, st);
+  } else {
+    k_deriv_explicit<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(
+        in, out, g, axis, scheme, g.per[axis], 0.0, e, st);
+  }
+}
+
+// lap / kappa = sum_m sum_l M[l,m] D_l(V_m)  (formulations.py:135-143)
+void launch_divergence(wd_ctx* c, double* const V[3], int csch, double* out, const Status* st) {
+  const int nd = c->g.nd;
+  bool first = true;
+  for (int m = 0; m < nd; ++m)
+    for (int l = 0; l < nd; ++l) {
+      if (c->M.m == nullptr && l != m) continue;  // exact zero terms (uniform)
+      launch_deriv(c, V[m], out, c->tmp, l, csch, epi_metric(c, l, m, first, out), st);
+      first = false;
+    }
+}
+
+void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* const Uh[3],
+                     const Status* st) {
+  Vec3 dv;
+  MVec3 Uv, Uhv;
+  for (int a = 0; a < 3; ++a) {
+    dv.p[a] = d[a];
+    Uv.p[a] = U[a];
+    Uhv.p[a] = Uh ? Uh[a] : nullptr;
+  }
+  k_assemble<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv, c->g.N,
+                                                                     c->g.nd, st);
+}
+
+// directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
+void launch_dphi(wd_ctx* c, const double* p, const Status* st) {
+  for (int l = 0; l < c->g.nd; ++l) {
+    if (c->sd.scheme == WD_UW)
+      k_uw_bf<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(p, c->B[l], c->F[l],
+                                                                      c->dphi[l], c->g, l,
+                                                                      c->g.per[l], st);
+    else
+      launch_deriv(c, p, c->dphi[l], c->tmp, l, c->sd.scheme, epi_plain(), st);
+  }
+}
+
+void launch_gamma_lad(wd_ctx* c, const double* p, const Status* st) {
+  const Geom& g = c->g;
+  for (int l = 0; l < g.nd; ++l) {
+    Epi e;
+    e.mode = l == 0 ? 1 : 2;
+    e.acc = c->tmp2;
+    e.cfield = c->sums_dev ? c->sums_dev + (2 + l) * g.N : nullptr;
+    e.cscal = c->sqrtS_c[l];
+    k_d4<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, g, l, g.per[l], e, st);
+  }
+  k_gamma_lad<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, c->gam, g.N,
+                                                                   c->sd.epsilon, c->sd.lad_c, st);
+}
+
+// tendency(p) -> k   (formulations.py:232-252)
+void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st) {
+  const int kind = c->sd.kind, scheme = c->sd.scheme, nd = c->g.nd;
+  const int csch = scheme == WD_UW ? WD_E2 : scheme;
+  ResidualArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.kind = kind;
+  a.scheme = scheme;
+  a.nd = nd;
+  a.eps = c->sd.epsilon;
+  a.p = p;
+  a.lap = c->lap;
+  a.gam = c->gam;
+  a.kappa = c->tmp2;
+  for (int l = 0; l < 3; ++l) {
+    a.U.p[l] = c->U[l];
+    a.Uh.p[l] = c->Uh[l];
+    a.dphi.p[l] = c->dphi[l];
+    a.B.p[l] = c->B[l];
+    a.F.p[l] = c->F[l];
+  }
+  if (kind == WD_POISSON) {
+    for (int l = 0; l < nd; ++l) launch_deriv(c, p, c->dphi[l], c->tmp, l, csch, epi_plain(), st);
+    launch_assemble(c, c->dphi, c->U, nullptr, st);
+    launch_divergence(c, c->U, csch, c->lap, st);
+  } else {
+    launch_dphi(c, p, st);
+    launch_assemble(c, c->dphi, c->U, c->Uh, st);
+    if (kind != WD_EIKONAL) {
+      double* const* Ul = c->U;
+      if (scheme == WD_UW) {
+        for (int l = 0; l < nd; ++l)
+          launch_deriv(c, p, c->nrm[l], c->tmp, l, WD_E2, epi_plain(), st);
+        launch_assemble(c, c->nrm, c->Ue, nullptr, st);
+        Ul = c->Ue;
+        for (int l = 0; l < 3; ++l) a.U.p[l] = c->Ue[l];
+      }
+      launch_divergence(c, Ul, csch, c->lap, st);
+      if (kind == WD_HJ_LAD) launch_gamma_lad(c, p, st);
+      if (kind == WD_HJ_CURVATURE) {
+        Vec3 uv;
+        MVec3 nv;
+        for (int l = 0; l < 3; ++l) {
+          uv.p[l] = Ul[l];
+          nv.p[l] = c->nrm[l];
+        }
+        k_normal<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(uv, nv, c->g.N, nd,
+                                                                         c->sd.eps0, st);
+        launch_divergence(c, c->nrm, csch, c->tmp2, st);
+      }
+    }
+  }
+  k_tendency<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(a, k, c->g.N, st);
+}
+
+// local_timestep(p) -> dt   (solver.py:160-180)
+void enqueue_timestep(wd_ctx* c, const double* p, double* dt, const Status* st) {
+  DtArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.kind = c->sd.kind;
+  a.nd = c->g.nd;
+  a.eps = c->sd.epsilon;
+  a.cfl = c->sd.cfl;
+  a.p = p;
+  a.gam = c->gam;
+  for (int l = 0; l < 3; ++l) a.Uh.p[l] = c->Uh[l];
+  a.sumS = c->sums_dev;
+  a.sumS_c = c->sumS_c;
+  a.cflms = c->sums_dev ? c->sums_dev + c->g.N : nullptr;
+  a.cflms_c = c->cflms_c;
+  if (c->sd.kind != WD_POISSON) {
+    launch_dphi(c, p, st);
+    launch_assemble(c, c->dphi, c->U, c->Uh, st);
+    if (c->sd.kind == WD_HJ_LAD) launch_gamma_lad(c, p, st);
+  }
+  k_timestep<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(a, dt, c->g.N, st);
+}
+
+// filter all axes + BC: x (BC'd RK4 output, clobbered) -> out
+// (solver.py:208-212)
+void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
+  const Geom& g = c->g;
+  double* cur = x;
+  double* bufs[2] = {c->tmp2, x};
+  for (int a = 0; a < g.nd; ++a) {
+    double* nxt = bufs[a & 1];
+    const long long L = g.N / g.n[a];
+    k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, c->stream>>>(
+        cur, nxt, g, a, g.per[a], c->fcoef, c->filt[a], nullptr, 1, st);
+    cur = nxt;
+  }
+  k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
+}
+
+// one RK4 step A -> B given dt already in c->dt (solver.py:183-212)
+void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st) {
+  const Geom& g = c->g;
+  const int nb = nblocks(g.N, kThreads);
+  enqueue_tendency(c, A, c->acc, st);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(1, A, c->dt, c->acc, c->acc, c->p, g, st);
+  enqueue_tendency(c, c->p, c->k, st);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(2, A, c->dt, c->k, c->acc, c->p, g, st);
+  enqueue_tendency(c, c->p, c->k, st);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(3, A, c->dt, c->k, c->acc, c->p, g, st);
+  enqueue_tendency(c, c->p, c->k, st);
+  if (c->sd.use_filter) {
+    k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, A, c->dt, c->k, c->acc, c->p, g, st);
+    enqueue_filter_bc(c, c->p, B, st);
+  } else {
+    k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, A, c->dt, c->k, c->acc, B, g, st);
+  }
+}
+
+void enqueue_step(wd_ctx* c, const double* A, double* B) {
+  if (c->fused.active) {
+    fused_step(c->fused, A, B, c->st, c->hist, c->stream);
+    return;
+  }
+  enqueue_timestep(c, A, c->dt, c->st);
+  enqueue_rk4(c, A, B, c->st);
+  k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
+                                                                   c->g.N);
+  k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
+}
+
+int validate(const wd_grid_desc* gd, const wd_solver_desc* sd) {
+  if (gd->ndim != 2 && gd->ndim != 3) return fail(WD_ERR_INVALID, "ndim must be 2 or 3");
+  if (sd->scheme < WD_UW || sd->scheme > WD_C6) return fail(WD_ERR_INVALID, "unknown scheme");
+  if (sd->kind < WD_EIKONAL || sd->kind > WD_POISSON)
+    return fail(WD_ERR_INVALID, "unknown formulation");
+  if (!(sd->cfl > 0.0)) return fail(WD_ERR_INVALID, "cfl must be positive");
+  if (!(sd->tol > 0.0)) return fail(WD_ERR_INVALID, "tol must be positive");
+  if (sd->epsilon < 0.0) return fail(WD_ERR_INVALID, "epsilon must be non-negative");
+  if (sd->lad_c < 0.0) return fail(WD_ERR_INVALID, "lad_c must be non-negative");
+  if (!(sd->eps0 > 0.0)) return fail(WD_ERR_INVALID, "eps0 must be positive");
+  if (sd->use_filter && !(sd->alpha_f >= 0.40 && sd->alpha_f <= 0.5))
+    return fail(WD_ERR_INVALID, "alpha_f must lie in [0.40, 0.5]");
+  if (!(gd->ref_length > 0.0)) return fail(WD_ERR_INVALID, "ref_length must be positive");
+  for (int a = 0; a < gd->ndim; ++a) {
+    const int lo = gd->face[2 * a], hi = gd->face[2 * a + 1];
+    if ((lo == WD_FACE_PERIODIC) != (hi == WD_FACE_PERIODIC))
+      return fail(WD_ERR_INVALID, "periodic faces must come in lo/hi pairs");
+    const int n = gd->dims[a];
+    const bool per = lo == WD_FACE_PERIODIC;
+    if (n < 1) return fail(WD_ERR_INVALID, "bad dims");
+    const int need = per ? 5 : min_line(sd->scheme);
+    if (n < need)
+      return fail(WD_ERR_LINE_TOO_SHORT, std::string(scheme_name(sd->scheme)) +
+                                             " derivative needs at least " +
+                                             std::to_string(need) + " points, got " +
+                                             std::to_string(n));
+    if ((sd->kind == WD_HJ_LAD) && n < 5)
+      return fail(WD_ERR_LINE_TOO_SHORT, "fourth derivative needs at least 5 points");
+    if (sd->scheme == WD_UW && sd->kind != WD_EIKONAL && n < 3)
+      return fail(WD_ERR_LINE_TOO_SHORT, "E2 derivative needs at least 3 points");
+    if (per && sd->use_filter && sd->scheme != WD_UW && sd->alpha_f >= 0.5)
+      return fail(WD_ERR_INVALID, "periodic filter needs alpha_f < 0.5");
+  }
+  if (!gd->uniform && gd->metrics_dev == nullptr)
+    return fail(WD_ERR_INVALID, "metrics required for a non-uniform grid");
+  return WD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wd_version(void) { return 100; }
+
+const char* wd_last_error(void) { return g_last_error.c_str(); }
+
+int wd_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd_ctx** out) {
+  if (!gd || !sd || !out) return fail(WD_ERR_INVALID, "null argument");
+  int rc = validate(gd, sd);
+  if (rc) return rc;
+  wd_ctx* c = new wd_ctx();
+  c->gd = *gd;
+  c->sd = *sd;
+  c->sd.use_filter = sd->use_filter && sd->scheme != WD_UW;
+  c->g = make_geom(gd->ndim, gd->dims, gd->face, gd->solid_mask_dev);
+  const Geom& g = c->g;
+  c->M.m = gd->uniform ? nullptr : gd->metrics_dev;
+  c->M.N = g.N;
+  c->M.nd = g.nd;
+  for (int a = 0; a < 3; ++a) c->M.c[a] = gd->uniform ? gd->inv_spacing[a] : 0.0;
+  (void)stream;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(WD_ERR_CUDA, "stream create failed");
+  }
+  // factors
+  std::vector<double> packed, all;
+  size_t off_comp[3] = {0, 0, 0}, off_filt[3] = {0, 0, 0};
+  for (int a = 0; a < g.nd; ++a) {
+    if (sd->scheme == WD_C4 || sd->scheme == WD_C6) {
+      rc = compact_factor(sd->scheme, g.n[a], g.per[a], c->hcomp[a]);
+      if (rc) {
+        wd_destroy(c);
+        return rc;
+      }
+      factor_pack(c->hcomp[a], packed);
+      off_comp[a] = all.size();
+      all.insert(all.end(), packed.begin(), packed.end());
+    }
+    if (c->sd.use_filter && g.n[a] >= 3) {
+      rc = filter_factor(sd->alpha_f, g.n[a], g.per[a], c->hfilt[a]);
+      if (rc) {
+        wd_destroy(c);
+        return rc;
+      }
+      factor_pack(c->hfilt[a], packed);
+      off_filt[a] = all.size();
+      all.insert(all.end(), packed.begin(), packed.end());
+    }
+  }
+  if (c->sd.use_filter) c->fcoef = filter_coefs(sd->alpha_f);
+  if (!all.empty()) {
+    if (cudaMalloc(&c->factor_dev, all.size() * sizeof(double)) != cudaSuccess ||
+        cudaMemcpy(c->factor_dev, all.data(), all.size() * sizeof(double),
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+      wd_destroy(c);
+      return fail(WD_ERR_CUDA, "factor upload failed");
+    }
+    for (int a = 0; a < g.nd; ++a) {
+      if (c->hcomp[a].n) c->comp[a] = factor_view(c->hcomp[a], c->factor_dev + off_comp[a]);
+      if (c->hfilt[a].n) c->filt[a] = factor_view(c->hfilt[a], c->factor_dev + off_filt[a]);
+    }
+  }
+  // workspace
+  const int nfields = 10 + 7 * 3;
+  if (cudaMalloc(&c->ws, (size_t)nfields * g.N * sizeof(double)) != cudaSuccess) {
+    wd_destroy(c);
+    return fail(WD_ERR_CUDA, "workspace allocation failed (" +
+                                 std::to_string((double)nfields * g.N * 8 / 1e9) + " GB)");
+  }
+  double* w = c->ws;
+  auto take = [&]() {
+    double* r = w;
+    w += g.N;
+    return r;
+  };
+  c->p = take();
+  c->k = take();
+  c->acc = take();
+  c->dt = take();
+  c->lap = take();
+  c->tmp = take();
+  c->tmp2 = take();
+  c->gam = take();
+  c->phiY = take();
+  take();
+  for (int a = 0; a < 3; ++a) {
+    c->dphi[a] = take();
+    c->U[a] = take();
+    c->Uh[a] = take();
+    c->nrm[a] = take();
+    c->B[a] = take();
+    c->F[a] = take();
+    c->Ue[a] = take();
+  }
+  if (cudaMalloc(&c->st, 2 * sizeof(Status)) != cudaSuccess ||
+      cudaMalloc(&c->hist_scratch, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->flag_dev, sizeof(int)) != cudaSuccess) {
+    wd_destroy(c);
+    return fail(WD_ERR_CUDA, "status allocation failed");
+  }
+  c->st_scratch = c->st + 1;
+  // metric sums
+  if (gd->uniform) {
+    double tot = 0.0, ms = 0.0;
+    for (int l = 0; l < g.nd; ++l) {
+      const double S = gd->inv_spacing[l] * gd->inv_spacing[l];
+      tot = l == 0 ? S : tot + S;
+      const double sq = std::sqrt(S);
+      const double sp = 1.0 / sq;
+      ms = l == 0 ? sp : std::min(ms, sp);
+      c->sqrtS_c[l] = sq;
+    }
+    c->sumS_c = tot;
+    c->cflms_c = sd->cfl * ms;
+  } else {
+    if (cudaMalloc(&c->sums_dev, (size_t)(2 + g.nd) * g.N * sizeof(double)) != cudaSuccess) {
+      wd_destroy(c);
+      return fail(WD_ERR_CUDA, "metric-sum allocation failed");
+    }
+    k_metric_sums<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(
+        c->M, c->sums_dev, c->sums_dev + g.N, c->sums_dev + 2 * g.N, sd->cfl, g.N, g.nd);
+  }
+  {
+    FusedInputs fi;
+    fi.gd = &c->gd;
+    fi.sd = &c->sd;
+    fi.g = c->g;
+    fi.M = c->M;
+    fi.fcoef = c->fcoef;
+    for (int a = 0; a < 3; ++a) fi.filt[a] = c->filt[a];
+    fi.sumS_c = c->sumS_c;
+    fi.cflms_c = c->cflms_c;
+    fi.lref = c->gd.ref_length;
+    fi.bufs[0] = c->dt;
+    fi.bufs[1] = c->acc;
+    fi.bufs[2] = c->p;
+    fi.bufs[3] = c->k;
+    fi.bufs[4] = c->tmp;
+    fi.bufs[5] = c->tmp2;
+    fused_plan(c->fused, fi);
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    wd_destroy(c);
+    return fail(WD_ERR_CUDA, "context setup failed");
+  }
+  *out = c;
+  return WD_OK;
+}
+
+int wd_destroy(wd_ctx* c) {
+  if (!c) return WD_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  fused_release(c->fused);
+  cudaFree(c->factor_dev);
+  cudaFree(c->sums_dev);
+  cudaFree(c->ws);
+  cudaFree(c->st);
+  cudaFree(c->hist_scratch);
+  cudaFree(c->flag_dev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return WD_OK;
+}
+
+int wd_bind(wd_ctx* c, double* phi, double* hist) {
+  if (!c || !phi || !hist) return fail(WD_ERR_INVALID, "null argument");
+  CK(cudaDeviceSynchronize());
+  if (phi != c->phi || hist != c->hist) {
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  c->phi = phi;
+  c->hist = hist;
+  c->enq = 0;
+  Status s;
+  std::memset(&s, 0, sizeof(s));
+  s.state = c->sd.max_iters > 0 ? WD_STATE_RUNNING : WD_STATE_MAXITERS;
+  s.max_iters = c->sd.max_iters;
+  CK(cudaMemcpyAsync(c->st, &s, sizeof(s), cudaMemcpyHostToDevice, c->stream));
+  k_bc<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(phi, c->tmp, c->g, nullptr);
+  CK(cudaMemcpyAsync(phi, c->tmp, c->g.N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+int wd_steps(wd_ctx* c, int k) {
+  if (!c || !c->phi) return fail(WD_ERR_INVALID, "context not bound");
+  if (k <= 0) return WD_OK;
+  const int parity = (int)(c->enq & 1);
+  auto key = std::make_pair(k, parity);
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int s = 0; s < k; ++s) {
+      const bool even = ((parity + s) & 1) == 0;
+      enqueue_step(c, even ? c->phi : c->phiY, even ? c->phiY : c->phi);
+    }
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    cudaGraphExec_t exec;
+    cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(WD_ERR_CUDA, std::string("graph: ") + cudaGetErrorString(e));
+    it = c->graphs.emplace(key, exec).first;
+  }
+  CK(cudaGraphLaunch(it->second, c->stream));
+  c->enq += k;
+  return WD_OK;
+}
+
+int wd_read_status(wd_ctx* c, wd_status* out) {
+  if (!c || !out) return fail(WD_ERR_INVALID, "null argument");
+  Status s;
+  CK(cudaMemcpyAsync(&s, c->st, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out->state = s.state;
+  out->iters = s.iters;
+  out->max_iters = s.max_iters;
+  out->diverged_iter = s.diverged_iter;
+  return WD_OK;
+}
+
+int wd_status_async(wd_ctx* c, wd_status* out) {
+  if (!c || !out) return fail(WD_ERR_INVALID, "null argument");
+  // wd_status is the leading 4 ints of Status
+  CK(cudaMemcpyAsync(out, c->st, sizeof(wd_status), cudaMemcpyDeviceToHost, c->stream));
+  return WD_OK;
+}
+
+int wd_finish(wd_ctx* c) {
+  wd_status s;
+  int rc = wd_read_status(c, &s);
+  if (rc) return rc;
+  // step t (1-based) writes phiY when t is odd; frozen steps write nothing
+  if (s.state != WD_STATE_DIVERGED && (s.iters & 1))
+    CK(cudaMemcpyAsync(c->phi, c->phiY, c->g.N * sizeof(double), cudaMemcpyDeviceToDevice,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+void* wd_get_stream(wd_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int wd_fused_active(wd_ctx* c) { return c && c->fused.active ? 1 : 0; }
+
+int wd_tendency(wd_ctx* c, const double* phi, double* k) {
+  if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  enqueue_tendency(c, phi, k, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+int wd_local_timestep(wd_ctx* c, const double* phi, double* dt) {
+  if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  enqueue_timestep(c, phi, dt, nullptr);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+int wd_apply_bc(wd_ctx* c, double* phi) {
+  if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  k_bc<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(phi, c->tmp, c->g, nullptr);
+  CK(cudaMemcpyAsync(phi, c->tmp, c->g.N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+int wd_rk4_step(wd_ctx* c, const double* phi, const double* dt, double* out, int* diverged) {
+  if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyAsync(c->dt, dt, c->g.N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  enqueue_rk4(c, phi, out, nullptr);
+  Status s;
+  std::memset(&s, 0, sizeof(s));
+  s.max_iters = 1 << 30;
+  CK(cudaMemcpyAsync(c->st_scratch, &s, sizeof(s), cudaMemcpyHostToDevice, c->stream));
+  k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(out, phi, c->g.mask,
+                                                                   c->st_scratch, c->g.N);
+  k_finalize<<<1, 1, 0, c->stream>>>(c->st_scratch, c->hist_scratch, lref(c), 0.0,
+                                     1e6 * lref(c));
+  CK(cudaMemcpyAsync(&s, c->st_scratch, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (diverged) *diverged = s.state == WD_STATE_DIVERGED;
+  return WD_OK;
+}
+
+int wd_poisson_post(wd_ctx* c, const double* pp, double* phi) {
+  if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  const Geom& g = c->g;
+  const int csch = c->sd.scheme == WD_UW ? WD_E2 : c->sd.scheme;
+  const int nb = nblocks(g.N, kThreads);
+  k_poisson_clip<<<nb, kThreads, 0, c->stream>>>(pp, c->p, g.N);
+  for (int l = 0; l < g.nd; ++l) launch_deriv(c, c->p, c->dphi[l], c->tmp, l, csch, epi_plain(), nullptr);
+  launch_assemble(c, c->dphi, c->U, nullptr, nullptr);
+  CK(cudaMemsetAsync(c->flag_dev, 0, sizeof(int), c->stream));
+  Vec3 uv;
+  for (int l = 0; l < 3; ++l) uv.p[l] = c->U[l];
+  k_poisson_map<<<nb, kThreads, 0, c->stream>>>(c->p, uv, c->tmp, g.N, g.nd, c->flag_dev);
+  int neg = 0;
+  CK(cudaMemcpyAsync(&neg, c->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  k_bc<<<nb, kThreads, 0, c->stream>>>(c->tmp, phi, g, nullptr);
+  CK(cudaStreamSynchronize(c->stream));
+  if (neg) return fail(WD_ERR_NEGATIVE_RADICAND, "negative radicand in the Poisson map");
+  return WD_OK;
+}
+
+int wd_derivative(const double* in, double* out, int ndim, const int* dims, int axis, int scheme,
+                  int periodic, double offset, void* stream) {
+  if (!in || !out || !dims || ndim < 1 || ndim > 3 || axis < 0 || axis >= ndim)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  if (scheme == WD_UW || scheme < 0 || scheme > WD_C6)
+    return fail(WD_ERR_INVALID, "use upwind_front_derivative for the UW scheme");
+  const int n = dims[axis];
+  const int need = periodic ? 5 : min_line(scheme);
+  if (n < need)
+    return fail(WD_ERR_LINE_TOO_SHORT, std::string(scheme_name(scheme)) +
+                                           " derivative needs at least " + std::to_string(need) +
+                                           " points, got " + std::to_string(n));
+  int face[6] = {0, 0, 0, 0, 0, 0};
+  if (periodic) face[2 * axis] = face[2 * axis + 1] = WD_FACE_PERIODIC;
+  Geom g = make_geom(ndim, dims, face, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (scheme == WD_C4 || scheme == WD_C6) {
+    HostFactor F;
+    int rc = compact_factor(scheme, n, periodic, F);
+    if (rc) return rc;
+    std::vector<double> packed;
+    factor_pack(F, packed);
+    double* dev = nullptr;
+    CK(cudaMallocAsync(&dev, packed.size() * sizeof(double), s));
+    CK(cudaMemcpyAsync(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       s));
+    const long long L = g.N / n;
+    k_deriv_compact<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(
+        in, out, out, g, axis, scheme, periodic, offset, factor_view(F, dev), epi_plain(),
+        nullptr);
+    CK(cudaFreeAsync(dev, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    k_deriv_explicit<<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, out, g, axis, scheme,
+                                                                   periodic, offset, epi_plain(),
+                                                                   nullptr);
+  }
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_fourth_derivative(const double* in, double* out, int ndim, const int* dims, int axis,
+                         int periodic, void* stream) {
+  if (!in || !out || !dims || ndim < 1 || ndim > 3 || axis < 0 || axis >= ndim)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  if (dims[axis] < 5)
+    return fail(WD_ERR_LINE_TOO_SHORT, "fourth derivative needs at least 5 points, got " +
+                                           std::to_string(dims[axis]));
+  int face[6] = {0, 0, 0, 0, 0, 0};
+  if (periodic) face[2 * axis] = face[2 * axis + 1] = WD_FACE_PERIODIC;
+  Geom g = make_geom(ndim, dims, face, nullptr);
+  k_d4<<<nblocks(g.N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(in, out, g, axis, periodic,
+                                                                       epi_plain(), nullptr);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_filter(const double* in, double* out, const unsigned char* pinned, int ndim,
+              const int* dims, int axis, double alpha_f, int periodic, void* stream) {
+  if (!in || !out || in == out || !dims || ndim < 1 || ndim > 3 || axis < 0 || axis >= ndim)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  if (!(alpha_f >= 0.40 && alpha_f <= 0.5))
+    return fail(WD_ERR_INVALID, "alpha_f must lie in [0.40, 0.5]");
+  const int n = dims[axis];
+  if (periodic && alpha_f >= 0.5) return fail(WD_ERR_INVALID, "periodic filter needs alpha_f < 0.5");
+  if (periodic && n < 5) return fail(WD_ERR_LINE_TOO_SHORT, "periodic filter needs 5 points");
+  int face[6] = {0, 0, 0, 0, 0, 0};
+  if (periodic) face[2 * axis] = face[2 * axis + 1] = WD_FACE_PERIODIC;
+  Geom g = make_geom(ndim, dims, face, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  HostFactor F;
+  TriDev T;
+  std::memset(&T, 0, sizeof(T));
+  double* dev = nullptr;
+  if (n >= 3 || periodic) {
+    int rc = filter_factor(alpha_f, n, periodic, F);
+    if (rc) return rc;
+    std::vector<double> packed;
+    factor_pack(F, packed);
+    CK(cudaMallocAsync(&dev, packed.size() * sizeof(double), s));
+    CK(cudaMemcpyAsync(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       s));
+    T = factor_view(F, dev);
+  }
+  const long long L = g.N / n;
+  k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(in, out, g, axis, periodic,
+                                                               filter_coefs(alpha_f), T, pinned, 0,
+                                                               nullptr);
+  CK(cudaGetLastError());
+  if (dev) CK(cudaFreeAsync(dev, s));
+  CK(cudaStreamSynchronize(s));
+  return WD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_tri_lines(double* x, Geom g, int axis, TriDev T) {
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  const long long L = g.N / n;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
+       q += (long long)gridDim.x * blockDim.x)
+    tri_solve_line(x + line_base(g, axis, q), sa, T);
+}
+}  // namespace
+
+extern "C" {
+
+int wd_solve_tridiagonal(const double* lower, const double* diag, const double* upper,
+                         double* rhs, int n, int nrhs, void* stream) {
+  if (!lower || !diag || !upper || !rhs || n < 1 || nrhs < 1)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  HostFactor F;
+  if (n == 1) {
+    if (diag[0] == 0.0) return fail(WD_ERR_ZERO_PIVOT, "1x1 tridiagonal system with zero diagonal");
+    F.n = 1;
+    F.d.assign(1, diag[0]);
+    F.fact.assign(1, 0.0);
+    F.du.assign(1, 0.0);
+    F.du2.assign(1, 0.0);
+    F.swap.assign(1, 0.0);
+    F.z.assign(1, 0.0);
+  } else {
+    int rc = gtsv_factor(n, lower, diag, upper, F);
+    if (rc) return rc;
+  }
+  int dims[2] = {n, nrhs};
+  Geom g = make_geom(2, dims, nullptr, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<double> packed;
+  factor_pack(F, packed);
+  double* dev = nullptr;
+  CK(cudaMallocAsync(&dev, packed.size() * sizeof(double), s));
+  CK(cudaMemcpyAsync(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  k_tri_lines<<<nblocks(nrhs, kLineThreads), kLineThreads, 0, s>>>(rhs, g, 0, factor_view(F, dev));
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(dev, s));
+  CK(cudaStreamSynchronize(s));
+  return WD_OK;
+}
+
+int wd_compute_metrics(const double* coords, double* metrics, double* jac, int ndim,
+                       const int* dims, int scheme, const int* periodic, const double* periods,
+                       void* stream) {
+  if (!coords || !metrics || !jac || !dims || (ndim != 2 && ndim != 3))
+    return fail(WD_ERR_INVALID, "bad arguments");
+  const int csch = scheme == WD_UW ? WD_E2 : scheme;
+  int face[6] = {0, 0, 0, 0, 0, 0};
+  for (int a = 0; a < ndim; ++a)
+    if (periodic && periodic[a]) face[2 * a] = face[2 * a + 1] = WD_FACE_PERIODIC;
+  Geom g = make_geom(ndim, dims, face, nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* fwd = nullptr;
+  CK(cudaMallocAsync(&fwd, (size_t)ndim * ndim * g.N * sizeof(double), s));
+  int rc = WD_OK;
+  for (int m = 0; m < ndim && rc == WD_OK; ++m)
+    for (int l = 0; l < ndim && rc == WD_OK; ++l) {
+      const double off = periods ? periods[l * ndim + m] : 0.0;
+      rc = wd_derivative(coords + (long long)m * g.N, fwd + (long long)(m * ndim + l) * g.N, ndim,
+                         dims, l, csch, g.per[l], off, stream);
+    }
+  int* flag = nullptr;
+  if (rc == WD_OK) {
+    CK(cudaMallocAsync(&flag, sizeof(int), s));
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    k_metric_invert<<<nblocks(g.N, kThreads), kThreads, 0, s>>>(fwd, metrics, jac, g.N, ndim,
+                                                                  flag);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h) rc = fail(WD_ERR_SINGULAR_METRIC, "metric matrix is singular at a node");
+    cudaFreeAsync(flag, s);
+  }
+  cudaFreeAsync(fwd, s);
+  CK(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int wd_linf_delta(const double* a, const double* b, const unsigned char* mask, long long n,
+                  double* out, void* stream) {
+  if (!a || !b || !out) return fail(WD_ERR_INVALID, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* dev = nullptr;
+  CK(cudaMallocAsync(&dev, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(dev, 0, sizeof(unsigned long long), s));
+  k_linf<<<nblocks(n, kThreads), kThreads, 0, s>>>(a, b, mask, dev, n);
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(dev, s));
+  CK(cudaStreamSynchronize(s));
+  double v;
+  std::memcpy(&v, &h, sizeof(v));
+  *out = v;
+  return WD_OK;
+}
+
+}  // extern "C"

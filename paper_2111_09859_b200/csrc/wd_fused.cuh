@@ -1,0 +1,34 @@
+// Specialised (fused) pseudo-step kernels.  A FusedPlan is built at
+// context creation when the configuration matches a specialised path; the
+// generic kernels of wd_kernels.cuh handle everything else.
+#pragma once
+
+#include "wd_kernels.cuh"
+
+namespace wd {
+
+struct FusedInputs {
+  const wd_grid_desc* gd;
+  const wd_solver_desc* sd;
+  Geom g;
+  Metric M;
+  FilterCoef fcoef;
+  TriDev filt[3];
+  double sumS_c, cflms_c, lref;
+  double* bufs[6];  // dt, acc, p, k, tmp, tmp2 (N each)
+};
+
+struct FusedPlan {
+  int active = 0;
+  int kind = 0;          // which specialised path
+  FusedInputs in;
+};
+
+// Decide whether a specialised path applies; fills fp (fp.active = 1).
+void fused_plan(FusedPlan& fp, const FusedInputs& in);
+// One pseudo-step A -> B incl. change reduction and stop test.
+void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,
+                cudaStream_t s);
+void fused_release(FusedPlan& fp);
+
+}  // namespace wd

@@ -1,0 +1,587 @@
+// Generic line / pointwise kernels of the wall-distance hot path.
+//
+// These are the "reference-structured" kernels: one launch per operator
+// pass, any dimensionality, curvilinear metrics, every scheme and
+// formulation.  They define the arithmetic (bit-identical to the reference)
+// and are the fallback-free path for everything the fused kernels
+// (wd_fused3d.cu) do not specialise.  Reference lines are cited per kernel.
+#pragma once
+
+#include "wd_common.cuh"
+
+namespace wd {
+
+// Device-resident tridiagonal factor (dgtsv elimination order, see
+// oracle/wd.py:gtsv_factor and LAPACK dgtsv.f).  Packed arrays of n each.
+struct TriDev {
+  int n;
+  int cyclic;
+  const double* fact;
+  const double* d;
+  const double* du;
+  const double* du2;
+  const double* swap;  // 0.0 / 1.0
+  const double* z;     // cyclic correction vector
+  double vn, denom;
+};
+
+// Epilogue of a derivative pass: out = D | c*D | acc + c*D, c = per-node
+// field or scalar.  Used to fuse the metric contractions of
+// formulations.py:87-98 / 135-143 and the LAD sensor (164-176).
+struct Epi {
+  int mode;              // 0: D, 1: c*D, 2: acc + c*D
+  const double* acc;     // may alias out
+  const double* cfield;  // per-node coefficient or nullptr
+  double cscal;
+  __device__ __forceinline__ double apply(double D, long long idx) const {
+    if (mode == 0) return D;
+    double c = cfield ? cfield[idx] : cscal;
+    double t = c * D;
+    if (mode == 1) return t;
+    return acc[idx] + t;
+  }
+};
+
+__device__ __forceinline__ long long line_base(const Geom& g, int axis, long long q) {
+  long long base = 0;
+  for (int a = kMaxDim - 1; a >= 0; --a) {
+    if (a == axis) continue;
+    long long c = q % g.n[a];
+    q /= g.n[a];
+    base += c * g.s[a];
+  }
+  return base;
+}
+
+__device__ __forceinline__ void tri_solve_line(double* __restrict__ x, long long st,
+                                               const TriDev& T) {
+  const int n = T.n;
+  if (n == 1) {
+    x[0] = x[0] / T.d[0];
+    return;
+  }
+  for (int i = 0; i < n - 1; ++i) {
+    const double f = T.fact[i];
+    double* xi = x + (long long)i * st;
+    double* xj = xi + st;
+    if (T.swap[i] != 0.0) {
+      double t = *xi;
+      double b1 = *xj;
+      *xi = b1;
+      *xj = t - f * b1;
+    } else {
+      *xj = *xj - f * *xi;
+    }
+  }
+  x[(long long)(n - 1) * st] = x[(long long)(n - 1) * st] / T.d[n - 1];
+  x[(long long)(n - 2) * st] =
+      (x[(long long)(n - 2) * st] - T.du[n - 2] * x[(long long)(n - 1) * st]) / T.d[n - 2];
+  for (int i = n - 3; i >= 0; --i) {
+    double* xi = x + (long long)i * st;
+    *xi = ((*xi - T.du[i] * xi[st]) - T.du2[i] * xi[2 * st]) / T.d[i];
+  }
+  if (T.cyclic) {
+    const double s = x[0] + T.vn * x[(long long)(n - 1) * st];
+    const double f = s / T.denom;
+    for (int i = 0; i < n; ++i) {
+      double* xi = x + (long long)i * st;
+      *xi = *xi - f * T.z[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernels
+
+// Explicit first derivative along `axis` (operators.py:109-128) + epilogue.
+static __global__ void k_deriv_explicit(const double* __restrict__ in, double* out, Geom g, int axis,
+                                 int scheme, int per, double off, Epi epi, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)((idx / sa) % n);
+    Line w{in + (idx - (long long)i * sa), sa, n, per, off};
+    out[idx] = epi.apply(deriv_explicit_at(w, i, n, scheme, per), idx);
+  }
+}
+
+// Compact first derivative: RHS + dgtsv-order solve per line
+// (operators.py:130-148, 53-78).  One thread per grid line; `scratch`
+// holds the raw solution (may equal out when epi.mode == 0).
+static __global__ void k_deriv_compact(const double* __restrict__ in, double* scratch, double* out,
+                                Geom g, int axis, int scheme, int per, double off, TriDev T,
+                                Epi epi, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  const long long L = g.N / n;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long base = line_base(g, axis, q);
+    Line w{in + base, sa, n, per, off};
+    double* x = scratch + base;
+    for (int i = 0; i < n; ++i) x[(long long)i * sa] = compact_rhs_at(w, i, n, scheme, per);
+    tri_solve_line(x, sa, T);
+    if (epi.mode != 0 || out != scratch)
+      for (int i = 0; i < n; ++i) {
+        const long long idx = base + (long long)i * sa;
+        out[idx] = epi.apply(scratch[idx], idx);
+      }
+  }
+}
+
+// 4th derivative (operators.py:236-250) + epilogue.
+static __global__ void k_d4(const double* __restrict__ in, double* out, Geom g, int axis, int per,
+                     Epi epi, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)((idx / sa) % n);
+    Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
+    out[idx] = epi.apply(d4_at(w, i, n, per), idx);
+  }
+}
+
+// Implicit filter along `axis` (operators.py:305-352).  hc[h*6+k] holds
+// the folded row coefficients: k = 0 -> a_0, k >= 1 -> 0.5*a_k of the
+// half-order-h filter (operators.py:269-302).  pin: explicit pinned array
+// (wd_filter) or, when use_geom_pin, walls + solid mask of g
+// (BoundarySpec.pinned_mask solver.py:59-70).
+struct FilterCoef {
+  double hc[6 * 6];
+};
+
+static __global__ void k_filter(const double* __restrict__ in, double* out, Geom g, int axis, int per,
+                         FilterCoef fc, TriDev T, const uint8_t* pin, int use_geom_pin,
+                         const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  const long long L = g.N / n;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long base = line_base(g, axis, q);
+    Line w{in + base, sa, n, per, 0.0};
+    double* x = out + base;
+    if (n < 3 && !per) {
+      for (int i = 0; i < n; ++i) x[(long long)i * sa] = w(i);
+      continue;
+    }
+    for (int i = 0; i < n; ++i) {
+      double r;
+      int h;
+      if (per) {
+        h = 5;
+      } else if (i == 0 || i == n - 1) {
+        h = 0;
+      } else {
+        h = min(min(i, n - 1 - i), 5);
+      }
+      if (h == 0) {
+        r = w(i);
+      } else {
+        const double* c = fc.hc + h * 6;
+        r = c[0] * w(i);
+        for (int k = 1; k <= h; ++k) r = r + c[k] * (w(i + k) + w(i - k));
+      }
+      x[(long long)i * sa] = r;
+    }
+    tri_solve_line(x, sa, T);
+    for (int i = 0; i < n; ++i) {
+      const long long idx = base + (long long)i * sa;
+      bool p;
+      if (use_geom_pin) {
+        int c[kMaxDim];
+        node_coords(g, idx, c);
+        p = is_pinned(g, idx, c);
+      } else {
+        p = pin != nullptr && pin[idx] != 0;
+      }
+      if (p) out[idx] = in[idx];
+    }
+  }
+}
+
+__device__ __forceinline__ double sign1(double x) { return x >= 0.0 ? 1.0 : -1.0; }
+
+// UW one-sided differences + front-selected derivative
+// (operators.py:151-193).
+static __global__ void k_uw_bf(const double* __restrict__ in, double* Bo, double* Fo, double* dphi,
+                        Geom g, int axis, int per, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const long long sa = g.s[axis];
+  const int n = g.n[axis];
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)((idx / sa) % n);
+    Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
+    double B, F;
+    if (per) {
+      B = w(i) - w(i - 1);
+      F = w(i + 1) - w(i);
+    } else {
+      B = i > 0 ? w(i) - w(i - 1) : w(1) - w(0);
+      F = i < n - 1 ? w(i + 1) - w(i) : w(n - 1) - w(n - 2);
+    }
+    const double s_fb = sign1(F + B);
+    const double nim1 = 0.25 * (1.0 + s_fb) * (1.0 + sign1(B));
+    const double nip1 = 0.25 * (1.0 - s_fb) * (1.0 - sign1(F));
+    Bo[idx] = B;
+    Fo[idx] = F;
+    dphi[idx] = nim1 * B + nip1 * F;
+  }
+}
+
+struct Vec3 {
+  const double* p[kMaxDim];
+};
+struct MVec3 {
+  double* p[kMaxDim];
+};
+
+// U_m = sum_l M[l,m] dphi_l ; Uhat_l = sum_m M[l,m] U_m
+// (formulations.py:87-98, Python sum order).
+static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd,
+                           const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double d[kMaxDim], u[kMaxDim];
+    for (int l = 0; l < nd; ++l) d[l] = dphi.p[l][idx];
+    for (int m = 0; m < nd; ++m) {
+      double s = M.get(0, m, idx) * d[0];
+      for (int l = 1; l < nd; ++l) s = s + M.get(l, m, idx) * d[l];
+      u[m] = s;
+      U.p[m][idx] = s;
+    }
+    if (Uh.p[0] != nullptr)
+      for (int l = 0; l < nd; ++l) {
+        double s = M.get(l, 0, idx) * u[0];
+        for (int m = 1; m < nd; ++m) s = s + M.get(l, m, idx) * u[m];
+        Uh.p[l][idx] = s;
+      }
+  }
+}
+
+// Curvature normal n_m = U_m / (|U| + eps0) (formulations.py:212-214).
+static __global__ void k_normal(Vec3 U, MVec3 nrm, long long N, int nd, double eps0,
+                         const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double u[kMaxDim];
+    double s = 0.0;
+    for (int m = 0; m < nd; ++m) {
+      u[m] = U.p[m][idx];
+      s = m == 0 ? u[0] * u[0] : s + u[m] * u[m];
+    }
+    const double gm = sqrt(s);
+    for (int m = 0; m < nd; ++m) nrm.p[m][idx] = u[m] / (gm + eps0);
+  }
+}
+
+// LAD diffusivity min(eps phi, C |sensor|) (formulations.py:175-176).
+static __global__ void k_gamma_lad(const double* __restrict__ p, const double* __restrict__ sensor,
+                            double* gam, long long N, double eps, double c, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x)
+    gam[idx] = np_min(eps * p[idx], c * fabs(sensor[idx]));
+}
+
+struct ResidualArgs {
+  int kind, scheme, nd;
+  double eps;
+  const double* p;
+  const double* lap;
+  const double* gam;    // LAD gamma or nullptr
+  const double* kappa;  // curvature
+  Vec3 U, Uh, dphi, B, F;
+};
+
+// Tendency (formulations.py:153-252).  UW advection: flux_from_bf
+// (operators.py:216-219); central: Uhat . dphi.
+static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (a.kind == WD_POISSON) {
+      const double r = -1.0 - a.lap[idx];
+      k[idx] = -r;
+      continue;
+    }
+    double adv = 0.0;
+    for (int l = 0; l < a.nd; ++l) {
+      const double uh = a.Uh.p[l][idx];
+      double t;
+      if (a.scheme == WD_UW) {
+        const double au = fabs(uh);
+        t = 0.5 * ((uh + au) * a.B.p[l][idx] + (uh - au) * a.F.p[l][idx]);
+      } else {
+        t = uh * a.dphi.p[l][idx];
+      }
+      adv = l == 0 ? t : adv + t;
+    }
+    if (a.kind == WD_EIKONAL) {
+      k[idx] = 1.0 - adv;
+    } else if (a.kind == WD_HJ || a.kind == WD_HJ_LAD) {
+      const double gam = a.kind == WD_HJ ? a.eps * a.p[idx] : a.gam[idx];
+      k[idx] = 1.0 + gam * a.lap[idx] - adv;
+    } else {  // WD_HJ_CURVATURE
+      double s = 0.0;
+      for (int m = 0; m < a.nd; ++m) {
+        const double u = a.U.p[m][idx];
+        s = m == 0 ? u * u : s + u * u;
+      }
+      const double gm = sqrt(s);
+      const double om = 1.0 - gm;
+      const double nu = 0.001 * (om * om);
+      const double gam = a.eps * a.p[idx] + nu;
+      const double corr = a.lap[idx] - np_max(0.0, gm * a.kappa[idx]);
+      k[idx] = 1.0 + gam * corr - adv;
+    }
+  }
+}
+
+struct DtArgs {
+  int kind, nd;
+  double eps, cfl;
+  const double* p;
+  const double* gam;     // LAD gamma
+  Vec3 Uh;
+  const double* sumS;    // field or nullptr (then sumS_c)
+  double sumS_c;
+  const double* cflms;   // cfl * min_spacing field or nullptr
+  double cflms_c;
+};
+
+// local_timestep (solver.py:160-180).
+static __global__ void k_timestep(DtArgs a, double* dt, long long N, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const double sS = a.sumS ? a.sumS[idx] : a.sumS_c;
+    if (a.kind == WD_POISSON) {
+      dt[idx] = a.cfl / (2.0 * sS);
+      continue;
+    }
+    double den = fabs(a.Uh.p[0][idx]);
+    for (int l = 1; l < a.nd; ++l) den = den + fabs(a.Uh.p[l][idx]);
+    if (a.kind == WD_HJ || a.kind == WD_HJ_CURVATURE)
+      den = den + 2.0 * (a.eps * a.p[idx]) * sS;
+    else if (a.kind == WD_HJ_LAD)
+      den = den + 2.0 * a.gam[idx] * sS;
+    const double d = a.cfl / (den + 1e-30);
+    dt[idx] = np_min(d, a.cflms ? a.cflms[idx] : a.cflms_c);
+  }
+}
+
+// RK4 stage update with the boundary conditions fused as a source
+// redirect (solver.py:198-206 + 87-110).
+//   stage 1..3: out = BC(phi + c(dt) k), c = 0.5*dt | 0.5*dt | dt
+//   stage 2, 3 also: acc = acc + 2 k   (acc holds k1 after stage 1)
+//   stage 4:  out = BC(phi + (dt/6)(acc + k))
+static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
+                           const double* __restrict__ dt, const double* __restrict__ k,
+                           double* acc, double* out, Geom g, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int c[kMaxDim];
+    node_coords(g, idx, c);
+    const long long s = bc_source(g, idx, c);
+    double v;
+    if (stage == 4) {
+      v = phi[s] + (dt[s] / 6.0) * (acc[s] + k[s]);
+    } else {
+      const double cdt = stage == 3 ? dt[s] : 0.5 * dt[s];
+      v = phi[s] + cdt * k[s];
+    }
+    out[idx] = is_pinned(g, idx, c) ? 0.0 : v;
+  }
+  if (stage == 2 || stage == 3) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+         idx += (long long)gridDim.x * blockDim.x)
+      acc[idx] = acc[idx] + 2.0 * k[idx];
+  }
+}
+
+// Out-of-place boundary conditions (solver.py:87-110).
+static __global__ void k_bc(const double* __restrict__ in, double* out, Geom g, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int c[kMaxDim];
+    node_coords(g, idx, c);
+    out[idx] = is_pinned(g, idx, c) ? 0.0 : in[bc_source(g, idx, c)];
+  }
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// max |new - old| over active nodes, max |new|, non-finite flag
+// (solver.py:214-217, 253-256).  max is order-free -> deterministic.
+static __global__ void k_change(const double* __restrict__ nw, const double* __restrict__ old,
+                         const uint8_t* mask, Status* st, long long N) {
+  if (st->state != WD_STATE_RUNNING) return;
+  double md = 0.0, ma = 0.0;
+  int bad = 0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const double v = nw[idx];
+    if (!isfinite(v)) bad = 1;
+    ma = fmax(ma, fabs(v));
+    if (mask == nullptr || mask[idx] == 0) md = fmax(md, fabs(v - old[idx]));
+  }
+  md = warp_max(md);
+  ma = warp_max(ma);
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ double smd[32], sma[32];
+  __shared__ int sbad[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    smd[wid] = md;
+    sma[wid] = ma;
+    sbad[wid] = bad;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw_ = blockDim.x >> 5;
+    md = lane < nw_ ? smd[lane] : 0.0;
+    ma = lane < nw_ ? sma[lane] : 0.0;
+    bad = lane < nw_ ? sbad[lane] : 0;
+    md = warp_max(md);
+    ma = warp_max(ma);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      atomicMax(&st->max_delta_bits, (unsigned long long)__double_as_longlong(md));
+      atomicMax(&st->max_abs_bits, (unsigned long long)__double_as_longlong(ma));
+      if (bad) atomicOr(&st->nonfinite, 1);
+    }
+  }
+}
+
+// Stop test + history (solver.py:253-272).
+static __global__ void k_finalize(Status* st, double* hist, double lref, double tol, double limit) {
+  if (st->state == WD_STATE_RUNNING) {
+    const double ma = __longlong_as_double((long long)st->max_abs_bits);
+    if (st->nonfinite || ma > limit) {
+      st->state = WD_STATE_DIVERGED;
+      st->diverged_iter = st->iters + 1;
+    } else {
+      const double change = __longlong_as_double((long long)st->max_delta_bits) / lref;
+      hist[st->iters] = change;
+      st->iters += 1;
+      if (change <= tol)
+        st->state = WD_STATE_CONVERGED;
+      else if (st->iters >= st->max_iters)
+        st->state = WD_STATE_MAXITERS;
+    }
+  }
+  st->max_delta_bits = 0ull;
+  st->max_abs_bits = 0ull;
+  st->nonfinite = 0;
+}
+
+// Poisson post-map (formulations.py:255-270): clip, radicand, sqrt.
+static __global__ void k_poisson_clip(const double* __restrict__ pp, double* out, long long N) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const double v = pp[idx];
+    out[idx] = (v < 0.0 && v > -1e-12) ? 0.0 : v;
+  }
+}
+
+static __global__ void k_poisson_map(const double* __restrict__ pp, Vec3 U, double* out, long long N,
+                              int nd, int* negative) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double gs = 0.0;
+    for (int m = 0; m < nd; ++m) {
+      const double u = U.p[m][idx];
+      gs = m == 0 ? u * u : gs + u * u;
+    }
+    double rad = gs + 2.0 * pp[idx];
+    if (rad < -1e-12) atomicOr(negative, 1);
+    rad = np_max(rad, 0.0);
+    out[idx] = -sqrt(gs) + sqrt(rad);
+  }
+}
+
+// Per-node metric sums (grid.py:60-73): sumS = sum_l S_l, cfl*min spacing,
+// sqrt(S_l) for the LAD sensor.
+static __global__ void k_metric_sums(Metric M, double* sumS, double* cflms, double* sqrtS, double cfl,
+                              long long N, int nd) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double tot = 0.0, ms = 0.0;
+    for (int l = 0; l < nd; ++l) {
+      double S = M.get(l, 0, idx) * M.get(l, 0, idx);
+      for (int m = 1; m < nd; ++m) S = S + M.get(l, m, idx) * M.get(l, m, idx);
+      tot = l == 0 ? S : tot + S;
+      const double sq = sqrt(S);
+      const double sp = 1.0 / sq;
+      ms = l == 0 ? sp : np_min(ms, sp);
+      sqrtS[(long long)l * N + idx] = sq;
+    }
+    sumS[idx] = tot;
+    cflms[idx] = cfl * ms;
+  }
+}
+
+// 2-D / 3-D metric inversion (grid.py:196-216).  fwd[m*d+l] = dx_m/dxi_l.
+static __global__ void k_metric_invert(const double* __restrict__ fwd, double* met, double* jac,
+                                long long N, int nd, int* singular) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+#define A(m, l) fwd[(long long)((m) * nd + (l)) * N + idx]
+#define O(l, m) met[(long long)((l) * nd + (m)) * N + idx]
+    if (nd == 2) {
+      const double det = A(0, 0) * A(1, 1) - A(0, 1) * A(1, 0);
+      if (fabs(det) < 1e-14 || det != det) atomicOr(singular, 1);
+      const double inv = 1.0 / det;
+      O(0, 0) = A(1, 1) * inv;
+      O(0, 1) = -A(0, 1) * inv;
+      O(1, 0) = -A(1, 0) * inv;
+      O(1, 1) = A(0, 0) * inv;
+      jac[idx] = inv;
+    } else {
+      const double c00 = A(1, 1) * A(2, 2) - A(1, 2) * A(2, 1);
+      const double c01 = A(1, 2) * A(2, 0) - A(1, 0) * A(2, 2);
+      const double c02 = A(1, 0) * A(2, 1) - A(1, 1) * A(2, 0);
+      const double det = A(0, 0) * c00 + A(0, 1) * c01 + A(0, 2) * c02;
+      if (fabs(det) < 1e-14 || det != det) atomicOr(singular, 1);
+      const double inv = 1.0 / det;
+      O(0, 0) = c00 * inv;
+      O(1, 0) = c01 * inv;
+      O(2, 0) = c02 * inv;
+      O(0, 1) = (A(0, 2) * A(2, 1) - A(0, 1) * A(2, 2)) * inv;
+      O(1, 1) = (A(0, 0) * A(2, 2) - A(0, 2) * A(2, 0)) * inv;
+      O(2, 1) = (A(0, 1) * A(2, 0) - A(0, 0) * A(2, 1)) * inv;
+      O(0, 2) = (A(0, 1) * A(1, 2) - A(0, 2) * A(1, 1)) * inv;
+      O(1, 2) = (A(0, 2) * A(1, 0) - A(0, 0) * A(1, 2)) * inv;
+      O(2, 2) = (A(0, 0) * A(1, 1) - A(0, 1) * A(1, 0)) * inv;
+      jac[idx] = inv;
+    }
+#undef A
+#undef O
+  }
+}
+
+static __global__ void k_linf(const double* __restrict__ a, const double* __restrict__ b,
+                       const uint8_t* mask, unsigned long long* out, long long N) {
+  double md = 0.0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x)
+    if (mask == nullptr || mask[idx] == 0) md = fmax(md, fabs(a[idx] - b[idx]));
+  md = warp_max(md);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(md));
+}
+
+}  // namespace wd
