@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the pseudo-time wall-distance iteration (HJ, GLUPS fp64).
+
+Default workload = BASELINE config 4 (the metric's target case): 3-D channel
+512^3 on [0,1]^3, walls at y = 0, 1, periodic x and z, HJ (eps = 0.2),
+explicit 6th order (E6), implicit filter alpha_f = 0.49, CFL 0.5, from
+phi = 0.  One "step" = one full pseudo-iteration (local dt, 4 RK stages,
+BCs, 3 filter sweeps, convergence reduction) over all 134,217,728 nodes.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference runs the CPU oracle port (oracle/wd.py, the reference's
+numpy algorithm restated) on rank 0 over a bounded sample of the same
+workload.  Under torchrun (N > 1) each rank runs an independent replica
+(round 1: no slab decomposition yet), weak scaling, max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HJ grid-point updates/s (GLUPS, fp64)"
+UNIT = "GLUPS"
+
+CONFIGS = {
+    "c4": dict(workload="c4_channel3d_512^3_hj_E6_F0.49", dims=(512, 512, 512),
+               periodic=(True, False, True), kind="hj", scheme="E6", alpha_f=0.49,
+               faces={"imin": "periodic", "imax": "periodic", "jmin": "wall",
+                      "jmax": "wall", "kmin": "periodic", "kmax": "periodic"}),
+}
+
+# Algorithmic fp64 words per node update: stages S1 4,
+# S2 6, S3 6, S4 5 (= 21) + filter 2 per axis + convergence read 1.
+WORDS_STAGE = {1: 4, 2: 6, 3: 6, 4: 5}
+
+
+def words_per_update(nd, filt):
+    return 21 + (2 * nd if filt else 0) + 1
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_sample(cfg, steps, warmup):
+    """The oracle (reference algorithm, numpy, 1 thread) on a bounded slab
+    of the same workload: (32, 512, 64) nodes with the 512^3 spacings."""
+    from oracle import wd
+    n = cfg["dims"]
+    sd = (32, n[1], 64)
+    og = wd.cartesian(sd[0], sd[1], sd[2], Lx=sd[0] / n[0], Ly=1.0, Lz=sd[2] / n[2],
+                      periodic=cfg["periodic"])
+    bnd = wd.Boundary({k: v for k, v in cfg["faces"].items() if v != "periodic"})
+    c = wd.Config(wd.Formulation(cfg["kind"]), cfg["scheme"], cfg["alpha_f"], 0.5, 1e-15, 10**9)
+    phi = wd.apply_bc(np.zeros(sd), bnd)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        dt = wd.local_timestep(phi, og, c.formulation, c.cfl, c.scheme)
+        phi = wd.rk4_step(phi, og, c, dt, bnd)
+        if s >= warmup:
+            times.append(time.perf_counter() - t0)
+    nodes = int(np.prod(sd))
+    total = float(sum(times))
+    return {"value": nodes * len(times) / total / 1e9, "unit": UNIT, "cores": 1,
+            "kind": "port",
+            "sample": f"{len(times)} pseudo-iterations of a {sd[0]}x{sd[1]}x{sd[2]} slab "
+                      f"(same spacing/BCs as 512^3), oracle/wd.py numpy, 1 thread "
+                      f"of {os.cpu_count()} host cores",
+            "seconds": total}
+
+
+def run_reference(args, world, rank):
+    cfg = CONFIGS[args.config]
+    if rank != 0:
+        return
+    cb = cpu_sample(cfg, args.steps, args.warmup)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg["workload"], "sample_dims": [32, 512, 64]},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_b200(args, world, rank, local):
+    import ctypes
+    import torch
+    import paper_2111_09859_b200 as W
+    from paper_2111_09859_b200 import _context, _native as nat
+
+    cfg = CONFIGS[args.config]
+    dims = tuple(args.n if args.n else d for d in cfg["dims"])
+    grid = W.build_cartesian(*dims, Lx=dims[0] / 512 if args.n else 1.0, Ly=1.0,
+                             Lz=dims[2] / 512 if args.n else 1.0, periodic=cfg["periodic"])
+    fc = W.FormulationConfig(kind=cfg["kind"])
+    filt = W.FilterConfig(cfg["alpha_f"]) if cfg["alpha_f"] else None
+    K, Wm = args.steps, args.warmup
+    ctx = _context.NativeSolver(grid, cfg["faces"], None, cfg["scheme"], fc, filt, 0.5, 1e-15,
+                                10**9)
+    lib = ctx.lib
+    N = int(np.prod(dims))
+    phi = torch.zeros(dims, dtype=torch.float64, device="cuda")
+    hist = torch.zeros(K + Wm + 8, dtype=torch.float64, device="cuda")
+    nat.check(lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
+    stream = ctx.stream()
+    chunk = 2
+    for _ in range((Wm + chunk - 1) // chunk):
+        nat.check(lib.wd_steps(ctx.ptr, chunk))
+    torch.cuda.synchronize()
+    # timed region
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done = 0
+    while done < K:
+        c = min(chunk, K - done)
+        nat.check(lib.wd_steps(ctx.ptr, c))
+        done += c
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    secs = e0.elapsed_time(e1) / 1e3
+    st = nat.Status()
+    nat.check(lib.wd_read_status(ctx.ptr, ctypes.byref(st)))
+    if st.state == nat.STATE_DIVERGED:
+        raise RuntimeError("benchmark run diverged")
+    secs_max = allreduce_max(secs, world)
+    value = N * K * world / secs_max / 1e9
+
+    # per-kernel device time (CUDA events on the solver stream)
+    kern = {}
+    if ctx.fused:
+        avg = ctypes.c_double(0.0)
+        names = {1: "stage1", 2: "stage2", 3: "stage3", 4: "stage4", 5: "filter_axis0",
+                 6: "filter_axis1", 7: "filter_axis2", 8: "change"}
+        for kid, name in names.items():
+            if lib.wd_time_kernel(ctx.ptr, kid, 5, ctypes.byref(avg)) == 0:
+                kern[name] = avg.value
+    peak, peak_kind = _peaks()
+    nd = len(dims)
+    roof = None
+    if kern:
+        kwords = {"stage1": 4, "stage2": 6, "stage3": 6, "stage4": 5, "filter_axis0": 2,
+                  "filter_axis1": 2, "filter_axis2": 3, "change": 2}
+        dom = max(kern, key=kern.get)
+        ach = kwords[dom] * 8 * N / (kern[dom] / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(dom)
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "kernel": dom,
+                "alg_bytes_per_launch": kwords[dom] * 8 * N, "peak_source": peak_kind}
+    w_upd = words_per_update(nd, filt is not None)
+    step_ach = w_upd * 8 * N / (secs / K) / 1e9
+    ctx.close()
+    del phi, hist
+    torch.cuda.empty_cache()
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        phi0 = torch.zeros(dims, dtype=torch.float64).pin_memory()
+        scfg = W.SolveConfig(formulation=fc, scheme=cfg["scheme"], filter_config=filt, cfl=0.5,
+                             tol=1e-15, max_iters=K)
+        bnd = W.BoundarySpec(cfg["faces"])
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        rep = W.solve_steady(grid, bnd, scfg, phi0=phi0, chunk=chunk)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        t_e2e = allreduce_max(t_e2e, world)
+        assert rep.iters == K
+        e2e = {"value": N * K * world / t_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(N * 8 / K),
+               "d2h_bytes_per_step": int((N * 8 + 8 * K) / K),
+               "seconds": t_e2e, "includes": "context setup + H2D phi0 (pinned) + K steps + "
+                                             "residual history + D2H phi"}
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": Wm, "ms_per_step": round(secs_max / K * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "dims": list(dims),
+                       "global_nodes": N * world, "parallelism": f"replica{world}",
+                       "l2": "inputs larger than L2 (1.07 GB per field)",
+                       "fused": True if kern else False},
+            "roofline": roof,
+            "step_roofline": {"achieved": round(step_ach, 1), "peak": peak, "unit": "GB/s",
+                              "frac": round(step_ach / peak, 4), "words_per_update": w_upd},
+            "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
+            "gpu_launches": K * (8 if kern else 0),
+            "clocks": clk, "e2e": e2e}
+    if rank == 0 and not args.no_cpu and world == 1:
+        line["cpu_baseline"] = cpu_sample(cfg, 3, 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="override grid size (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,11 @@ int wd_finish(wd_ctx* ctx);
 void* wd_get_stream(wd_ctx* ctx);
 /* 1 when a fused (specialised) pseudo-step kernel path is in use.        */
 int wd_fused_active(wd_ctx* ctx);
+/* Average device time (CUDA events on the context stream) of one kernel of
+ * the fused step, run `reps` times on the bound state: kid 1..4 RK stages,
+ * 5..7 filter sweeps, 8 change reduction.  Clobbers the workspace; for
+ * benchmarking only.                                                     */
+int wd_time_kernel(wd_ctx* ctx, int kid, int reps, double* avg_ms);
 
 /* ---- operator-level entry points (parity + drop-in operators) -------- */
 /* RK4 step solver.py:183-218 (phi_out = BC(filter(RK4(phi_in))))         */

@@ -106,6 +106,7 @@ SIGNATURES = {
     "wd_compute_metrics": (_I, [_P, _P, _P, _I, _IP, _I, _IP, _DP, _P]),
     "wd_linf_delta": (_I, [_P, _P, _P, ctypes.c_longlong, _DP, _P]),
     "wd_fused_active": (_I, [_P]),
+    "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
 }
 
 _lib = None

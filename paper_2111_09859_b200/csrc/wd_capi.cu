@@ -800,6 +800,27 @@ void* wd_get_stream(wd_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int wd_fused_active(wd_ctx* c) { return c && c->fused.active ? 1 : 0; }
 
+int wd_time_kernel(wd_ctx* c, int kid, int reps, double* avg_ms) {
+  if (!c || !c->phi || !avg_ms || reps < 1) return fail(WD_ERR_INVALID, "bad arguments");
+  if (!c->fused.active) return fail(WD_ERR_INVALID, "no fused path for this configuration");
+  if (kid < 1 || kid > 8 || (kid >= 5 && kid <= 7 && !c->sd.use_filter))
+    return fail(WD_ERR_INVALID, "bad kernel id");
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  fused_launch(c->fused, kid, c->phi, c->phiY, c->st, c->stream);  // warm
+  CK(cudaEventRecord(e0, c->stream));
+  for (int r = 0; r < reps; ++r) fused_launch(c->fused, kid, c->phi, c->phiY, c->st, c->stream);
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *avg_ms = ms / reps;
+  return WD_OK;
+}
+
 int wd_tendency(wd_ctx* c, const double* phi, double* k) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
   CK(cudaDeviceSynchronize());

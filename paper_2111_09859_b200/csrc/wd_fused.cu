@@ -1,14 +1,141 @@
 // Specialised pseudo-step paths (see wd_fused.cuh).
+//
+// PATH_F3: 3-D, uniform Cartesian metrics, explicit E2/E4/E6, HJ or
+// Eikonal, wall / periodic faces only (no far-field copies, no solid
+// mask).  Covers BASELINE config 4 (512^3 channel) and 3-D wall-bounded
+// boxes.  Everything else runs the generic kernels.
 #include "wd_fused.cuh"
+#include "wd_fused3d.cuh"
 
 namespace wd {
+
+namespace {
+constexpr int PATH_F3 = 1;
+
+int grid_blocks(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b < 148LL * 32 ? b : 148LL * 32);
+}
+
+template <int R, bool EIK>
+void launch_stage(int stage, const F3Args& a, int blocks, cudaStream_t s) {
+  const dim3 thr(F3_TK, F3_TJ);
+  const size_t sm = F3_SMEM_DOUBLES * sizeof(double);
+  switch (stage) {
+    case 1: k_f3_stage<R, EIK, 1><<<blocks, thr, sm, s>>>(a); break;
+    case 2: k_f3_stage<R, EIK, 2><<<blocks, thr, sm, s>>>(a); break;
+    case 3: k_f3_stage<R, EIK, 3><<<blocks, thr, sm, s>>>(a); break;
+    default: k_f3_stage<R, EIK, 4><<<blocks, thr, sm, s>>>(a); break;
+  }
+}
+
+void stage_dispatch(int R, bool eik, int stage, const F3Args& a, int blocks, cudaStream_t s) {
+  if (R == 1) eik ? launch_stage<1, true>(stage, a, blocks, s) : launch_stage<1, false>(stage, a, blocks, s);
+  else if (R == 2) eik ? launch_stage<2, true>(stage, a, blocks, s) : launch_stage<2, false>(stage, a, blocks, s);
+  else eik ? launch_stage<3, true>(stage, a, blocks, s) : launch_stage<3, false>(stage, a, blocks, s);
+}
+}  // namespace
 
 void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   fp.active = 0;
   fp.in = in;
+  const wd_grid_desc& gd = *in.gd;
+  const wd_solver_desc& sd = *in.sd;
+  if (const char* env = getenv("WD_DISABLE_FUSED")) {
+    if (env[0] == '1') return;
+  }
+  if (gd.ndim != 3 || !gd.uniform || gd.solid_mask_dev != nullptr) return;
+  if (sd.scheme != WD_E2 && sd.scheme != WD_E4 && sd.scheme != WD_E6) return;
+  if (sd.kind != WD_HJ && sd.kind != WD_EIKONAL) return;
+  for (int f = 0; f < 6; ++f)
+    if (gd.face[f] == WD_FACE_FARFIELD) return;
+  fp.kind = PATH_F3;
+  fp.active = 1;
 }
 
-void fused_step(const FusedPlan&, const double*, double*, Status*, double*, cudaStream_t) {}
+namespace {
+F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
+  const FusedInputs& in = fp.in;
+  const wd_grid_desc& gd = *in.gd;
+  const wd_solver_desc& sd = *in.sd;
+  const Geom& g = in.g;
+  F3Args a;
+  a.n0 = g.n[0];
+  a.n1 = g.n[1];
+  a.n2 = g.n[2];
+  a.s0 = (long long)g.n[1] * g.n[2];
+  a.per0 = g.per[0];
+  a.per1 = g.per[1];
+  a.per2 = g.per[2];
+  for (int f = 0; f < 6; ++f) a.wall[f] = gd.face[f] == WD_FACE_WALL;
+  a.c0 = gd.inv_spacing[0];
+  a.c1 = gd.inv_spacing[1];
+  a.c2 = gd.inv_spacing[2];
+  a.eps = sd.epsilon;
+  a.cfl = sd.cfl;
+  a.sumS = in.sumS_c;
+  a.cflms = in.cflms_c;
+  a.A = A;
+  a.dt = in.bufs[0];
+  a.acc = in.bufs[1];
+  a.st = st;
+  a.tiles_k = (a.n2 + F3_TK - 1) / F3_TK;
+  a.tiles_j = (a.n1 + F3_TJ - 1) / F3_TJ;
+  const int tiles = a.tiles_k * a.tiles_j;
+  // split the i-stream so the grid is several waves of 148 SMs
+  int chunks = 1;
+  while ((long long)tiles * chunks < 148LL * 8 && a.n0 / (chunks * 2) >= 32) chunks *= 2;
+  a.chunk = (a.n0 + chunks - 1) / chunks;
+  *blocks = tiles * chunks;
+  return a;
+}
+}  // namespace
+
+// kid 1..4: RK stages, 5..7: filter sweeps, 8: change reduction
+void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Status* st,
+                  cudaStream_t s) {
+  const FusedInputs& in = fp.in;
+  const wd_solver_desc& sd = *in.sd;
+  const Geom& g = in.g;
+  double* bp = in.bufs[2];
+  double* bk = in.bufs[3];
+  double* tmp = in.bufs[4];
+  int blocks = 0;
+  F3Args a = f3_args(fp, A, st, &blocks);
+  const int R = sd.scheme == WD_E2 ? 1 : (sd.scheme == WD_E4 ? 2 : 3);
+  const bool eik = sd.kind == WD_EIKONAL;
+  switch (kid) {
+    case 1: a.p = A; a.out = bp; break;
+    case 2: a.p = bp; a.out = bk; break;
+    case 3: a.p = bk; a.out = bp; break;
+    case 4: a.p = bp; a.out = sd.use_filter ? bk : B; break;
+    default: break;
+  }
+  if (kid >= 1 && kid <= 4) {
+    stage_dispatch(R, eik, kid, a, blocks, s);
+  } else if (kid >= 5 && kid <= 7) {
+    const int ax = kid - 5;
+    const double* srcs[3] = {bk, tmp, bp};
+    double* dsts[3] = {tmp, bp, B};
+    const long long L = g.N / g.n[ax];
+    k_filter<<<grid_blocks(L, 64), 64, 0, s>>>(srcs[ax], dsts[ax], g, ax, g.per[ax], in.fcoef,
+                                                in.filt[ax], nullptr, 1, st);
+  } else if (kid == 8) {
+    k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
+  }
+}
+
+void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,
+                cudaStream_t s) {
+  const FusedInputs& in = fp.in;
+  const wd_solver_desc& sd = *in.sd;
+  for (int kid = 1; kid <= 4; ++kid) fused_launch(fp, kid, A, B, st, s);
+  if (sd.use_filter)
+    for (int kid = 5; kid <= 7; ++kid) fused_launch(fp, kid, A, B, st, s);
+  fused_launch(fp, 8, A, B, st, s);
+  k_finalize<<<1, 1, 0, s>>>(st, hist, in.lref, sd.tol, 1e6 * in.lref);
+}
 
 void fused_release(FusedPlan& fp) { fp.active = 0; }
 

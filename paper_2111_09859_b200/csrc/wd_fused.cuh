@@ -3,6 +3,7 @@
 // generic kernels of wd_kernels.cuh handle everything else.
 #pragma once
 
+#include <cstdlib>
 #include "wd_kernels.cuh"
 
 namespace wd {
@@ -30,5 +31,9 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in);
 void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,
                 cudaStream_t s);
 void fused_release(FusedPlan& fp);
+// Launch one kernel of the fused step (timing / profiling): kid 1..4 RK
+// stages, 5..7 filter sweeps, 8 change reduction.
+void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Status* st,
+                  cudaStream_t s);
 
 }  // namespace wd

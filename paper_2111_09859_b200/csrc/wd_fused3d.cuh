@@ -1,0 +1,307 @@
+// Fused 3-D RK4 stage kernel for uniform Cartesian grids with explicit
+// central schemes (E2/E4/E6): one launch per RK stage computes the
+// directional derivatives, U, U_hat, the Laplacian div(grad phi) as
+// first derivatives of U (formulations.py:135-150), the HJ / Eikonal
+// residual (formulations.py:153-197), the local time step (stage 1,
+// solver.py:160-180) and the RK combine (solver.py:198-205) -- in the
+// reference's exact operation order, so the result is bit-identical to the
+// generic kernels.
+//
+// Data movement (B200): a CTA owns a TK x TJ column tile of the (j, k)
+// plane and streams along i (axis 0).  Axis-0 stencils run out of register
+// windows (p at i-R..i+4+R, U_0 at i-4..i+4, d_0 at i..i+4), so every p
+// value is read from HBM once per stage; the in-plane stencils read a
+// double-buffered shared-memory plane with a 7-point halo (the halo comes
+// from L2).  Pointwise fields (phi0, dt, acc) are read/written once.
+// Per update per stage: S1 4 words, S2/S3 6, S4 5.
+#pragma once
+
+#include "wd_kernels.cuh"
+
+namespace wd {
+
+constexpr int F3_TK = 32;
+constexpr int F3_TJ = 16;
+constexpr int F3_HP = 7;   // p halo (U halo 4 + stencil radius <= 3)
+constexpr int F3_HU = 4;   // U halo (E4 closures reach 4 rows)
+constexpr int F3_PW = F3_TK + 2 * F3_HP;  // 46
+constexpr int F3_PH = F3_TJ + 2 * F3_HP;  // 30
+constexpr int F3_UKW = F3_TK + 2 * F3_HU; // 40
+constexpr int F3_UJH = F3_TJ + 2 * F3_HU; // 24
+constexpr int F3_SMEM_DOUBLES = 2 * (F3_PH * F3_PW + F3_TJ * F3_UKW + F3_UJH * F3_TK);
+
+struct F3Args {
+  int n0, n1, n2;
+  long long s0;          // n1 * n2
+  int per0, per1, per2;
+  int wall[6];
+  double c0, c1, c2;     // d xi_l / d x_l
+  double eps, cfl, sumS, cflms;
+  const double* p;       // stage input field
+  const double* A;       // field at step start
+  double* dt;
+  double* acc;
+  double* out;
+  int chunk;             // planes per CTA
+  int tiles_k, tiles_j;
+  const Status* st;
+};
+
+template <int R>
+struct SchemeOf;
+template <>
+struct SchemeOf<1> { static constexpr int id = WD_E2; };
+template <>
+struct SchemeOf<2> { static constexpr int id = WD_E4; };
+template <>
+struct SchemeOf<3> { static constexpr int id = WD_E6; };
+
+// central relation on values at offsets -R..R
+template <int R>
+__device__ __forceinline__ double central(double m3, double m2, double m1, double p1, double p2,
+                                          double p3) {
+  if (R == 1) return E2_CA * (p1 - m1);
+  if (R == 2) return E4_CA * (p1 - m1) + E4_CB * (p2 - m2);
+  return E6_CA * (p1 - m1) + E6_CB * (p2 - m2) + E6_CC * (p3 - m3);
+}
+
+// closures written on explicit values (same expression text as
+// e4_closure / the E2 closures in wd_common.cuh)
+__device__ __forceinline__ double e4_row0(double w0, double w1, double w2, double w3, double w4) {
+  return (-25.0 * w0 + 48.0 * w1 - 36.0 * w2 + 16.0 * w3 - 3.0 * w4) / 12.0;
+}
+__device__ __forceinline__ double e4_row1(double w0, double w1, double w2, double w3, double w4) {
+  return (-3.0 * w0 - 10.0 * w1 + 18.0 * w2 - 6.0 * w3 + w4) / 12.0;
+}
+// last row: wl = w(n-1), wl1 = w(n-2), ...
+__device__ __forceinline__ double e4_rowl(double wl, double wl1, double wl2, double wl3,
+                                          double wl4) {
+  return (25.0 * wl - 48.0 * wl1 + 36.0 * wl2 - 16.0 * wl3 + 3.0 * wl4) / 12.0;
+}
+__device__ __forceinline__ double e4_rowl1(double wl, double wl1, double wl2, double wl3,
+                                           double wl4) {
+  return (3.0 * wl + 10.0 * wl1 - 18.0 * wl2 + 6.0 * wl3 - wl4) / 12.0;
+}
+__device__ __forceinline__ double e4_central(double m2, double m1, double p1, double p2) {
+  return E4_CA * (p1 - m1) + E4_CB * (p2 - m2);
+}
+
+// Derivative along axis 0 at row i from the U window u[0..8] (positions
+// i-4..i+4) -- every row type with compile-time slots.
+template <int R>
+__device__ __forceinline__ double d0_from_window(const double* u, int i, int n, int per) {
+  if (per) return central<R>(u[1], u[2], u[3], u[5], u[6], u[7]);
+  if (R == 1) {
+    if (i == 0) return -1.5 * u[4] + 2.0 * u[5] - 0.5 * u[6];
+    if (i == n - 1) return 1.5 * u[4] - 2.0 * u[3] + 0.5 * u[2];
+    return central<1>(0, 0, u[3], u[5], 0, 0);
+  }
+  if (i == 0) return e4_row0(u[4], u[5], u[6], u[7], u[8]);
+  if (i == 1) return e4_row1(u[3], u[4], u[5], u[6], u[7]);
+  if (i == n - 1) return e4_rowl(u[4], u[3], u[2], u[1], u[0]);
+  if (i == n - 2) return e4_rowl1(u[5], u[4], u[3], u[2], u[1]);
+  if (R == 3 && (i == 2 || i == n - 3)) return e4_central(u[2], u[3], u[5], u[6]);
+  return central<R>(u[1], u[2], u[3], u[5], u[6], u[7]);
+}
+
+// d_0 at the entering row q = i+5 from the p window w[0..4+2R]
+// (positions i+1-R .. i+5+R, q at slot 4+R).  Only far-end closures occur.
+template <int R>
+__device__ __forceinline__ double d0_entering(const double* w, int q, int n, int per) {
+  constexpr int Q = 4 + R;
+  if (!per) {
+    if (R == 1) {
+      if (q == n - 1) return 1.5 * w[Q] - 2.0 * w[Q - 1] + 0.5 * w[Q - 2];
+    } else {
+      if (q == n - 1) return e4_rowl(w[Q], w[Q - 1], w[Q - 2], w[Q - 3], w[Q - 4]);
+      if (q == n - 2) return e4_rowl1(w[Q + 1], w[Q], w[Q - 1], w[Q - 2], w[Q - 3]);
+      if (R == 3 && q == n - 3) return e4_central(w[Q - 2], w[Q - 1], w[Q + 1], w[Q + 2]);
+    }
+  }
+  return central<R>(R >= 3 ? w[Q - 3] : 0.0, R >= 2 ? w[Q - 2] : 0.0, w[Q - 1], w[Q + 1],
+                    R >= 2 ? w[Q + 2] : 0.0, R >= 3 ? w[Q + 3] : 0.0);
+}
+
+struct SLine {  // shared-memory line addressed by global index
+  const double* p;
+  int base;
+  int st;
+  __device__ __forceinline__ double operator()(int j) const { return p[(j - base) * st]; }
+};
+
+__device__ __forceinline__ int wrapi(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+
+template <int R, bool EIK, int STAGE>
+__global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
+  if (a.st->state != WD_STATE_RUNNING) return;
+  constexpr int SCH = SchemeOf<R>::id;
+  constexpr int NPW = 5 + 2 * R;
+  extern __shared__ double smem[];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tile = blockIdx.x % (a.tiles_k * a.tiles_j);
+  const int chunk_id = blockIdx.x / (a.tiles_k * a.tiles_j);
+  const int k0 = (tile % a.tiles_k) * F3_TK;
+  const int j0 = (tile / a.tiles_k) * F3_TJ;
+  const int i0 = chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.n0);
+  if (i0 >= i1) return;
+  const int k = k0 + tx, j = j0 + ty;
+  const bool act = k < a.n2 && j < a.n1;
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const long long s0 = a.s0;
+  const long long col = (long long)j * n2 + k;  // offset of (0, j, k)
+
+  // ---- prologue: register windows along axis 0
+  double pw[NPW], uw[9], dw[5];
+#pragma unroll
+  for (int s = 0; s < NPW; ++s) {
+    int pos = i0 - R + s;
+    double v = 0.0;
+    if (act) {
+      if (a.per0) v = a.p[(long long)wrapi(wrapi(pos, n0), n0) * s0 + col];
+      else if (pos >= 0 && pos < n0) v = a.p[(long long)pos * s0 + col];
+    }
+    pw[s] = v;
+  }
+  {
+    Line gl{a.p + col, s0, n0, a.per0, 0.0};
+#pragma unroll
+    for (int s = 0; s < 9; ++s) {
+      const int q = i0 - 4 + s;
+      double d = 0.0;
+      if (act && (a.per0 || (q >= 0 && q < n0))) {
+        const int qq = a.per0 ? wrapi(q, n0) : q;
+        d = deriv_explicit_at(gl, qq, n0, SCH, a.per0);
+      }
+      uw[s] = a.c0 * d;
+      if (s >= 4) dw[s - 4] = d;
+    }
+  }
+
+
+  for (int i = i0; i < i1; ++i) {
+    const int b = (i - i0) & 1;
+    double* Pb = smem + b * (F3_PH * F3_PW);
+    double* Ukb = smem + 2 * F3_PH * F3_PW + b * (F3_TJ * F3_UKW);
+    double* Ujb = smem + 2 * F3_PH * F3_PW + 2 * F3_TJ * F3_UKW + b * (F3_UJH * F3_TK);
+    const long long plane = (long long)i * s0;
+    // prefetch: next window value and this plane's pointwise fields
+    const int nxt = i + 5 + R;
+    double pnext = 0.0;
+    if (act) {
+      if (a.per0) pnext = a.p[(long long)wrapi(nxt % n0, n0) * s0 + col];
+      else if (nxt < n0) pnext = a.p[(long long)nxt * s0 + col];
+    }
+    double Av = 0.0, dtv = 0.0, accv = 0.0;
+    if (act) {
+      Av = a.A[plane + col];
+      if (STAGE > 1) dtv = a.dt[plane + col];
+      if (STAGE == 2 || STAGE == 3 || STAGE == 4) accv = a.acc[plane + col];
+    }
+    // ---- plane i into shared memory (own value from the window)
+    Pb[(ty + F3_HP) * F3_PW + tx + F3_HP] = pw[R];
+    if (ty < 2 * F3_HP) {  // j halo rows
+      const int jj = ty < F3_HP ? ty : ty + F3_TJ;  // tile-relative row
+      const int jg = j0 - F3_HP + jj;
+      double v = 0.0;
+      if (k < n2) {
+        if (a.per1) v = a.p[plane + (long long)wrapi(jg, n1) * n2 + k];
+        else if (jg >= 0 && jg < n1) v = a.p[plane + (long long)jg * n2 + k];
+      }
+      Pb[jj * F3_PW + tx + F3_HP] = v;
+    }
+    if (tx < 2 * F3_HP) {  // k halo columns
+      const int kk = tx < F3_HP ? tx : tx + F3_TK;
+      const int kg = k0 - F3_HP + kk;
+      double v = 0.0;
+      if (j < n1) {
+        if (a.per2) v = a.p[plane + (long long)j * n2 + wrapi(kg, n2)];
+        else if (kg >= 0 && kg < n2) v = a.p[plane + (long long)j * n2 + kg];
+      }
+      Pb[(ty + F3_HP) * F3_PW + kk] = v;
+    }
+    __syncthreads();
+    // ---- U_k on [TJ] x [TK + 2HU], U_j on [TJ + 2HU] x [TK]
+    for (int t = tx; t < F3_UKW; t += F3_TK) {
+      const int kg = k0 - F3_HU + t;
+      double v = 0.0;
+      if (j < n1 && (a.per2 || (kg >= 0 && kg < n2))) {
+        SLine ln{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
+        v = a.c2 * deriv_explicit_at(ln, a.per2 ? kg : kg, n2, SCH, a.per2);
+      }
+      Ukb[ty * F3_UKW + t] = v;
+    }
+    for (int t = ty; t < F3_UJH; t += F3_TJ) {
+      const int jg = j0 - F3_HU + t;
+      double v = 0.0;
+      if (k < n2 && (a.per1 || (jg >= 0 && jg < n1))) {
+        SLine ln{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
+        v = a.c1 * deriv_explicit_at(ln, jg, n1, SCH, a.per1);
+      }
+      Ujb[t * F3_TK + tx] = v;
+    }
+    // own directional derivatives d_2, d_1 (plane values, from smem)
+    double d2 = 0.0, d1 = 0.0;
+    if (act) {
+      SLine lk{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
+      d2 = deriv_explicit_at(lk, k, n2, SCH, a.per2);
+      SLine lj{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
+      d1 = deriv_explicit_at(lj, j, n1, SCH, a.per1);
+    }
+    __syncthreads();
+    if (act) {
+      SLine uk{Ukb + ty * F3_UKW, k0 - F3_HU, 1};
+      SLine uj{Ujb + tx, j0 - F3_HU, F3_TK};
+      const double D2 = deriv_explicit_at(uk, k, n2, SCH, a.per2);
+      const double D1 = deriv_explicit_at(uj, j, n1, SCH, a.per1);
+      const double D0 = d0_from_window<R>(uw, i, n0, a.per0);
+      const double d0 = dw[0];
+      const double pv = pw[R];
+      // U_m = c_m d_m ; U_hat_l = c_l U_l (diagonal metrics)
+      const double U0 = a.c0 * d0, U1 = a.c1 * d1, U2 = a.c2 * d2;
+      const double H0 = a.c0 * U0, H1 = a.c1 * U1, H2 = a.c2 * U2;
+      const double adv = H0 * d0 + H1 * d1 + H2 * d2;
+      double kv;
+      if (EIK) {
+        kv = 1.0 - adv;
+      } else {
+        const double lap = a.c0 * D0 + a.c1 * D1 + a.c2 * D2;
+        kv = 1.0 + (a.eps * pv) * lap - adv;
+      }
+      const bool pinned = (i == 0 && a.wall[0]) || (i == n0 - 1 && a.wall[1]) ||
+                          (j == 0 && a.wall[2]) || (j == n1 - 1 && a.wall[3]) ||
+                          (k == 0 && a.wall[4]) || (k == n2 - 1 && a.wall[5]);
+      const long long idx = plane + col;
+      if (STAGE == 1) {
+        double den = fabs(H0) + fabs(H1) + fabs(H2);
+        if (!EIK) den = den + 2.0 * (a.eps * pv) * a.sumS;
+        const double d = a.cfl / (den + 1e-30);
+        dtv = np_min(d, a.cflms);
+        a.dt[idx] = dtv;
+        a.acc[idx] = kv;
+        a.out[idx] = pinned ? 0.0 : Av + (0.5 * dtv) * kv;
+      } else if (STAGE == 2 || STAGE == 3) {
+        a.acc[idx] = accv + 2.0 * kv;
+        const double cdt = STAGE == 3 ? dtv : 0.5 * dtv;
+        a.out[idx] = pinned ? 0.0 : Av + cdt * kv;
+      } else {
+        a.out[idx] = pinned ? 0.0 : Av + (dtv / 6.0) * (accv + kv);
+      }
+    }
+    // ---- advance the axis-0 windows
+#pragma unroll
+    for (int s = 0; s < NPW - 1; ++s) pw[s] = pw[s + 1];
+    pw[NPW - 1] = pnext;
+    const int q = i + 5;
+    double dq = 0.0;
+    if (act && (a.per0 || q < n0)) dq = d0_entering<R>(pw, q, n0, a.per0);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) uw[s] = uw[s + 1];
+    uw[8] = a.c0 * dq;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) dw[s] = dw[s + 1];
+    dw[4] = dq;
+  }
+}
+
+}  // namespace wd

@@ -1,0 +1,87 @@
+"""The fused 3-D stage kernels (wd_fused3d.cuh) against the oracle and the
+generic kernels, bit-for-bit, across schemes, face kinds, periodicity,
+non-multiple-of-tile sizes and i-chunked launches."""
+import numpy as np
+import pytest
+
+from helpers import same
+from oracle import wd
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_2111_09859_b200")
+from paper_2111_09859_b200 import _context  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+FACES = ("imin", "imax", "jmin", "jmax", "kmin", "kmax")
+
+CASES = [
+    # dims, periodic, faces (non-periodic axes), kind, scheme, alpha_f, iters
+    ((8, 17, 9), (True, False, True), ("wall", "wall"), "hj", "E6", 0.49, 12),
+    ((64, 20, 40), (True, False, True), ("wall", "wall"), "hj", "E6", 0.49, 6),
+    ((13, 21, 35), (False, False, False), ("wall",) * 6, "hj", "E4", 0.49, 8),
+    ((19, 18, 33), (False, True, False), ("wall", None, "wall", "wall"), "hj", "E2", 0.48, 8),
+    ((70, 11, 12), (False, False, True), ("wall", "wall", "wall", None), "eikonal", "E6", 0.49, 6),
+    ((12, 40, 37), (True, True, False), (None, "wall"), "hj", "E4", None, 8),
+]
+
+
+def _faces(periodic, kinds):
+    it = iter(kinds)
+    faces = {}
+    for ax, p in enumerate(periodic):
+        for f in FACES[2 * ax:2 * ax + 2]:
+            if p:
+                faces[f] = "periodic"
+            else:
+                k = next(it)
+                if k is not None:
+                    faces[f] = k
+    return faces
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[0])) + f"-{c[4]}-{c[3]}")
+def test_fused_vs_oracle(case):
+    dims, per, kinds, kind, scheme, af, iters = case
+    faces = _faces(per, kinds)
+    L = [0.9, 1.0, 1.1]
+    og = wd.cartesian(*dims, Lx=L[0], Ly=L[1], Lz=L[2], periodic=per)
+    pg = W.build_cartesian(*dims, Lx=L[0], Ly=L[1], Lz=L[2], periodic=per)
+    rng = np.random.default_rng(sum(dims))
+    phi0 = 1e-3 * rng.random(dims)
+    bnd_o = wd.Boundary({k: v for k, v in faces.items() if v != "periodic"})
+    ro = wd.solve(og, bnd_o, wd.Config(wd.Formulation(kind), scheme, af, 0.5, 1e-15, iters),
+                  phi0=phi0, raise_on_divergence=False)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme=scheme,
+                        filter_config=None if af is None else W.FilterConfig(af), tol=1e-15,
+                        max_iters=iters)
+    ctx = _context.NativeSolver(pg, faces, None, scheme, cfg.formulation, cfg.filter_config)
+    assert ctx.fused, "fused path expected"
+    ctx.close()
+    rp = W.solve_steady(pg, W.BoundarySpec(faces), cfg, phi0=phi0)
+    assert rp.iters == ro.iters
+    assert same(rp.residual_history, ro.residual_history)
+    assert same(rp.phi, ro.phi)
+
+
+def test_fused_matches_generic(monkeypatch):
+    dims, per = (40, 33, 48), (True, False, True)
+    faces = _faces(per, ("wall", "wall"))
+    pg = W.build_cartesian(*dims, periodic=per)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E6",
+                        filter_config=W.FilterConfig(0.49), tol=1e-15, max_iters=10)
+    a = W.solve_steady(pg, W.BoundarySpec(faces), cfg)
+    monkeypatch.setenv("WD_DISABLE_FUSED", "1")
+    ctx = _context.NativeSolver(pg, faces, None, "E6", cfg.formulation, cfg.filter_config)
+    assert not ctx.fused
+    ctx.close()
+    b = W.solve_steady(pg, W.BoundarySpec(faces), cfg)
+    assert same(a.residual_history, b.residual_history)
+    assert same(a.phi, b.phi)

@@ -237,8 +237,9 @@ def test_solve_uniform_cartesian_c1_prefix():
     assert rep.iters == int(z["iters"]) == 18440
     assert same(rep.residual_history, z["residual_history"])
     assert same(rep.phi, z["phi"])
-    exact = g.y
-    assert maxdiff(rep.phi, exact) / 1.0 < 5e-2
+    # HJ (eps = 0.2) is accurate near the wall (sec. 5.1)
+    near = g.y <= 0.3
+    assert maxdiff(rep.phi[near], g.y[near]) < 1e-2
 
 
 def test_divergence_plate():
@@ -275,11 +276,26 @@ def test_periodic_channel3d_e6_vs_oracle():
 
 def test_annulus_curvature_c6_vs_oracle():
     faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield"}
-    og = wd.annulus(24, 13, scheme="C6")
-    pg = G.build_annulus(24, 13, scheme="C6")
-    ro, rp = _ext_solve(og, pg, faces, "hj_curvature", "C6", 0.48, 15)
+    og = wd.annulus(33, 17, scheme="C6")
+    pg = G.build_annulus(33, 17, scheme="C6")
+    ro, rp = _ext_solve(og, pg, faces, "hj_curvature", "C6", 0.48, 40)
     assert same(rp.residual_history, ro.residual_history)
     assert same(rp.phi, ro.phi)
+
+
+def test_annulus_divergence_iteration_matches_oracle():
+    """Too coarse an annulus diverges; the iteration must match the oracle."""
+    from paper_2111_09859_b200.errors import DivergenceError
+    faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield"}
+    og = wd.annulus(24, 13, scheme="C6")
+    ro = wd.solve(og, wd.Boundary(faces), wd.Config(wd.Formulation("hj_curvature"), "C6", 0.48,
+                                                   0.5, 1e-14, 40), raise_on_divergence=False)
+    assert ro.diverged_at == 10
+    pg = G.build_annulus(24, 13, scheme="C6")
+    cfg = slv.SolveConfig(formulation=forms.FormulationConfig(kind="hj_curvature"), scheme="C6",
+                          filter_config=ops.FilterConfig(0.48), tol=1e-14, max_iters=40)
+    with pytest.raises(DivergenceError, match="iteration 10"):
+        slv.solve_steady(pg, slv.BoundarySpec(faces), cfg)
 
 
 def test_cylinder_poisson_c6_vs_oracle():
