@@ -225,6 +225,7 @@ TriDev factor_view(const HostFactor& F, double* dev) {
   T.du2 = dev + 3 * n;
   T.swap = dev + 4 * n;
   T.z = dev + 5 * n;
+  T.rinv = dev + 6 * n;
   T.vn = F.vn;
   T.denom = F.denom;
   return T;
@@ -242,6 +243,9 @@ void factor_pack(const HostFactor& F, std::vector<double>& out) {
   put(3, F.du2);
   put(4, F.swap);
   put(5, F.z);
+  std::vector<double> rinv(n, 0.0);
+  for (size_t i = 0; i < (size_t)F.n && i < F.d.size(); ++i) rinv[i] = 1.0 / F.d[i];
+  put(6, rinv);
 }
 
 Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) {
@@ -683,7 +687,11 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
     fi.g = c->g;
     fi.M = c->M;
     fi.fcoef = c->fcoef;
-    for (int a = 0; a < 3; ++a) fi.filt[a] = c->filt[a];
+    for (int a = 0; a < 3; ++a) {
+      fi.filt[a] = c->filt[a];
+      fi.filt_swaps[a] = 0;
+      for (double sw : c->hfilt[a].swap) fi.filt_swaps[a] |= sw != 0.0;
+    }
     fi.sumS_c = c->sumS_c;
     fi.cflms_c = c->cflms_c;
     fi.lref = c->gd.ref_length;

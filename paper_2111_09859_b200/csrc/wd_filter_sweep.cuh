@@ -1,0 +1,307 @@
+// Fused implicit-filter sweep along one axis (operators.py:305-352) for the
+// specialised 3-D path, in LAPACK dgtsv elimination order (no row
+// interchanges occur for the filter matrix).
+//
+// Layout / data movement: one warp owns 32 grid lines (lane = line) and
+// walks them row by row.  Axes 0/1: the 32 lines are 32 consecutive k, so
+// every row access is one coalesced 256-byte segment.  Axis 2 (contiguous
+// lines): rows are staged through a padded 32x33 shared-memory transpose.
+// The forward-elimination values are parked in a lane-contiguous scratch
+// region private to the warp (sized so all resident warps' scratch stays
+// L2-resident), then read back in reverse for the back substitution.  HBM
+// traffic is therefore one read + one write per node (+ one read of phi for
+// the fused convergence reduction on the last axis).
+//
+// Division: x_i = (y_i - du_i x_{i+1}) / d_i is evaluated as a correctly
+// rounded quotient from the precomputed reciprocal (Markstein: q0 = s*r,
+// e = fma(-q0, d, s), q = fma(e, r, q0)), which equals IEEE s / d; the
+// parity tests check bit equality with the reference.
+#pragma once
+
+#include "wd_kernels.cuh"
+
+namespace wd {
+
+struct SweepArgs {
+  const double* in;
+  double* out;
+  double* scratch;     // >= total_warps * n * 32 doubles
+  int n;               // line length
+  int axis;            // 0, 1, 2
+  int n0, n1, n2;
+  long long s0;        // n1 * n2
+  int per;
+  // factor (dgtsv order, no interchanges) + cyclic correction
+  const double* fact;  // n
+  const double* du;    // n
+  const double* d;     // n
+  const double* rinv;  // n, RN(1/d)
+  const double* z;     // n (cyclic)
+  double vn, denom;
+  FilterCoef fc;
+  // fused convergence reduction (last axis)
+  const double* A;     // nullptr -> no reduction
+  Status* st;
+};
+
+__device__ __forceinline__ double div_rn(double s, double d, double r) {
+  const double q0 = s * r;
+  const double e = fma(-q0, d, s);
+  return fma(e, r, q0);
+}
+
+// filter RHS for row r from the window (slot 5 = row r): order of
+// _filter_rhs_row (operators.py:298-302).
+__device__ __forceinline__ double filt_rhs(const double* w, int h, const FilterCoef& fc) {
+  if (h == 0) return w[5];
+  const double* c = fc.hc + h * 6;
+  double v = c[0] * w[5];
+#pragma unroll
+  for (int k = 1; k <= 5; ++k)
+    if (k <= h) v = v + c[k] * (w[5 + k] + w[5 - k]);
+  return v;
+}
+
+template <bool CONTIG>
+__global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
+  if (a.st->state != WD_STATE_RUNNING) return;
+  __shared__ double tile[4][32][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int n = a.n;
+  double(*T)[33] = tile[wib];
+  double* scr = a.scratch + (long long)gw * n * 32;
+  // line groups of 32
+  long long groups, lines_per_row_blk;
+  long long rstride;
+  if (a.axis == 2) {
+    lines_per_row_blk = (a.n1 + 31) / 32;
+    groups = (long long)a.n0 * lines_per_row_blk;
+    rstride = 1;
+  } else {
+    lines_per_row_blk = (a.n2 + 31) / 32;
+    groups = (long long)(a.axis == 0 ? a.n1 : a.n0) * lines_per_row_blk;
+    rstride = a.axis == 0 ? a.s0 : a.n2;
+  }
+  double md = 0.0, ma = 0.0;
+  int bad = 0;
+  for (long long g = gw; g < groups; g += nwarps) {
+    const long long outer = g / lines_per_row_blk;
+    const int blk = (int)(g % lines_per_row_blk);
+    // base offset of this lane's line and lane validity
+    long long base;
+    bool valid;
+    long long gbase = 0;  // CONTIG: offset of line 0 of the group (row 0)
+    if (a.axis == 2) {
+      const int j = blk * 32 + lane;
+      valid = j < a.n1;
+      base = outer * a.s0 + (long long)j * a.n2;
+      gbase = outer * a.s0 + (long long)(blk * 32) * a.n2;
+    } else {
+      const int k = blk * 32 + lane;
+      valid = k < a.n2;
+      base = (a.axis == 0 ? outer * a.n2 : outer * a.s0) + k;
+    }
+    const int nl = a.axis == 2 ? min(32, a.n1 - blk * 32) : min(32, a.n2 - blk * 32);
+    auto ld = [&](int row) -> double {  // scalar load, row may wrap
+      if (!valid) return 0.0;
+      int r = row;
+      if (a.per) {
+        r = r % n;
+        if (r < 0) r += n;
+      } else if (r < 0 || r >= n) {
+        return 0.0;
+      }
+      return a.in[base + (long long)r * rstride];
+    };
+    // ---------------- forward elimination
+    double w[11];
+#pragma unroll
+    for (int s = 0; s < 11; ++s) w[s] = 0.0;
+    // window holds rows t-10..t; preload rows -5..-1 into slots 6..10
+#pragma unroll
+    for (int s = 6; s < 11; ++s) w[s] = ld(s - 11);
+    double y = 0.0;
+    const int nch = (n + 31) / 32;
+    for (int c = 0; c < nch; ++c) {
+      const int r0 = c * 32;
+      double v[32];
+      if (CONTIG) {
+        // coalesced: lane reads column (r0 + lane) of each of the nl lines
+        double tv[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+          const int r = r0 + lane;
+          tv[m] = (m < nl && r < n) ? a.in[gbase + (long long)m * a.n2 + r] : 0.0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 32; ++m) T[m][lane] = tv[m];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 32; ++s) v[s] = T[lane][s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+          const int r = r0 + s;
+          v[s] = (valid && r < n) ? a.in[base + (long long)r * rstride] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        const int t = r0 + s;  // newest row
+        if (t >= n) break;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) w[q] = w[q + 1];
+        w[10] = v[s];
+        const int r = t - 5;
+        if (r >= 0) {
+          const int h = a.per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
+          const double rhs = filt_rhs(w, h, a.fc);
+          y = r == 0 ? rhs : rhs - a.fact[r - 1] * y;
+          scr[(long long)r * 32 + lane] = y;
+        }
+      }
+    }
+    // rows n..n+4 (periodic wrap or zero) finish the last 5 right-hand sides
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int t = n + s;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) w[q] = w[q + 1];
+      w[10] = ld(t);
+      const int r = t - 5;
+      if (r >= 0 && r < n) {
+        const int h = a.per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
+        const double rhs = filt_rhs(w, h, a.fc);
+        y = r == 0 ? rhs : rhs - a.fact[r - 1] * y;
+        scr[(long long)r * 32 + lane] = y;
+      }
+    }
+    __syncwarp();
+    // ---------------- back substitution (+ cyclic correction)
+    double x1 = 0.0;
+    double xlast = 0.0;
+    const bool cyc = a.per;
+    for (int c = nch - 1; c >= 0; --c) {
+      const int r0 = c * 32;
+      double o[32];
+#pragma unroll
+      for (int s = 31; s >= 0; --s) {
+        const int r = r0 + s;
+        double x = 0.0;
+        if (r < n) {
+          const double yr = scr[(long long)r * 32 + lane];
+          if (r == n - 1) {
+            x = yr / a.d[r];
+            xlast = x;
+          } else {
+            x = div_rn(yr - a.du[r] * x1, a.d[r], a.rinv[r]);
+          }
+          x1 = x;
+          if (cyc) scr[(long long)r * 32 + lane] = x;
+        }
+        o[s] = x;
+      }
+      if (!cyc) {
+        // final values: write out (+ convergence reduction)
+        if (CONTIG) {
+          __syncwarp();
+#pragma unroll
+          for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
+          __syncwarp();
+          for (int m = 0; m < nl; ++m) {
+            const int r = r0 + lane;
+            if (r < n) {
+              const long long idx = gbase + (long long)m * a.n2 + r;
+              const double xv = T[m][lane];
+              a.out[idx] = xv;
+              if (a.A) {
+                if (!isfinite(xv)) bad = 1;
+                ma = fmax(ma, fabs(xv));
+                md = fmax(md, fabs(xv - a.A[idx]));
+              }
+            }
+          }
+        } else if (valid) {
+#pragma unroll
+          for (int s = 0; s < 32; ++s) {
+            const int r = r0 + s;
+            if (r < n) {
+              const long long idx = base + (long long)r * rstride;
+              a.out[idx] = o[s];
+              if (a.A) {
+                const double xv = o[s];
+                if (!isfinite(xv)) bad = 1;
+                ma = fmax(ma, fabs(xv));
+                md = fmax(md, fabs(xv - a.A[idx]));
+              }
+            }
+          }
+        }
+      }
+    }
+    if (cyc) {
+      // x = y - f z,  f = (y_0 + vn y_{n-1}) / denom  (oracle/wd.py:cyclic_apply)
+      const double f = (x1 + a.vn * xlast) / a.denom;
+      __syncwarp();
+      for (int c = 0; c < nch; ++c) {
+        const int r0 = c * 32;
+        double o[32];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+          const int r = r0 + s;
+          o[s] = r < n ? scr[(long long)r * 32 + lane] - f * a.z[r] : 0.0;
+        }
+        if (CONTIG) {
+          __syncwarp();
+#pragma unroll
+          for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
+          __syncwarp();
+          for (int m = 0; m < nl; ++m) {
+            const int r = r0 + lane;
+            if (r < n) {
+              const long long idx = gbase + (long long)m * a.n2 + r;
+              const double xv = T[m][lane];
+              a.out[idx] = xv;
+              if (a.A) {
+                if (!isfinite(xv)) bad = 1;
+                ma = fmax(ma, fabs(xv));
+                md = fmax(md, fabs(xv - a.A[idx]));
+              }
+            }
+          }
+        } else if (valid) {
+#pragma unroll
+          for (int s = 0; s < 32; ++s) {
+            const int r = r0 + s;
+            if (r < n) {
+              const long long idx = base + (long long)r * rstride;
+              a.out[idx] = o[s];
+              if (a.A) {
+                const double xv = o[s];
+                if (!isfinite(xv)) bad = 1;
+                ma = fmax(ma, fabs(xv));
+                md = fmax(md, fabs(xv - a.A[idx]));
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (a.A) {
+    md = warp_max(md);
+    ma = warp_max(ma);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      atomicMax(&a.st->max_delta_bits, (unsigned long long)__double_as_longlong(md));
+      atomicMax(&a.st->max_abs_bits, (unsigned long long)__double_as_longlong(ma));
+      if (bad) atomicOr(&a.st->nonfinite, 1);
+    }
+  }
+}
+
+}  // namespace wd

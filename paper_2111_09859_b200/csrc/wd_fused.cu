@@ -6,6 +6,7 @@
 // boxes.  Everything else runs the generic kernels.
 #include "wd_fused.cuh"
 #include "wd_fused3d.cuh"
+#include "wd_filter_sweep.cuh"
 
 namespace wd {
 
@@ -50,6 +51,27 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   if (sd.kind != WD_HJ && sd.kind != WD_EIKONAL) return;
   for (int f = 0; f < 6; ++f)
     if (gd.face[f] == WD_FACE_FARFIELD) return;
+  if (sd.use_filter) {
+    for (int a = 0; a < 3; ++a)
+      if (in.filt_swaps[a]) return;
+    // one scratch slab of n * 32 doubles per resident warp
+    int nmax = 0;
+    long long groups_min = 1LL << 62;
+    for (int a = 0; a < 3; ++a) {
+      nmax = in.g.n[a] > nmax ? in.g.n[a] : nmax;
+      const long long L = in.g.N / in.g.n[a];
+      const long long gr = (L + 31) / 32;
+      groups_min = gr < groups_min ? gr : groups_min;
+    }
+    int ctas = 148;
+    if (const char* env = getenv("WD_SWEEP_CTAS")) ctas = atoi(env) > 0 ? atoi(env) : ctas;
+    const size_t bytes = (size_t)ctas * 4 * nmax * 32 * sizeof(double);
+    if (cudaMalloc(&fp.scratch, bytes) != cudaSuccess) {
+      fp.scratch = nullptr;
+      return;
+    }
+    fp.sweep_ctas = ctas;
+  }
   fp.kind = PATH_F3;
   fp.active = 1;
 }
@@ -118,9 +140,36 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     const int ax = kid - 5;
     const double* srcs[3] = {bk, tmp, bp};
     double* dsts[3] = {tmp, bp, B};
+    SweepArgs w;
+    w.in = srcs[ax];
+    w.out = dsts[ax];
+    w.scratch = fp.scratch;
+    w.n = g.n[ax];
+    w.axis = ax;
+    w.n0 = g.n[0];
+    w.n1 = g.n[1];
+    w.n2 = g.n[2];
+    w.s0 = (long long)g.n[1] * g.n[2];
+    w.per = g.per[ax];
+    const TriDev& T = in.filt[ax];
+    w.fact = T.fact;
+    w.du = T.du;
+    w.d = T.d;
+    w.rinv = T.rinv;
+    w.z = T.z;
+    w.vn = T.vn;
+    w.denom = T.denom;
+    w.fc = in.fcoef;
+    w.A = ax == 2 ? A : nullptr;
+    w.st = st;
     const long long L = g.N / g.n[ax];
-    k_filter<<<grid_blocks(L, 64), 64, 0, s>>>(srcs[ax], dsts[ax], g, ax, g.per[ax], in.fcoef,
-                                                in.filt[ax], nullptr, 1, st);
+    const long long groups = (L + 31) / 32;
+    long long ctas = (groups + 3) / 4;
+    if (ctas > fp.sweep_ctas) ctas = fp.sweep_ctas;
+    if (ax == 2)
+      k_filter_sweep<true><<<(int)ctas, 128, 0, s>>>(w);
+    else
+      k_filter_sweep<false><<<(int)ctas, 128, 0, s>>>(w);
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }
@@ -132,11 +181,16 @@ void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, dou
   const wd_solver_desc& sd = *in.sd;
   for (int kid = 1; kid <= 4; ++kid) fused_launch(fp, kid, A, B, st, s);
   if (sd.use_filter)
-    for (int kid = 5; kid <= 7; ++kid) fused_launch(fp, kid, A, B, st, s);
-  fused_launch(fp, 8, A, B, st, s);
+    for (int kid = 5; kid <= 7; ++kid) fused_launch(fp, kid, A, B, st, s);  // 7 reduces
+  else
+    fused_launch(fp, 8, A, B, st, s);
   k_finalize<<<1, 1, 0, s>>>(st, hist, in.lref, sd.tol, 1e6 * in.lref);
 }
 
-void fused_release(FusedPlan& fp) { fp.active = 0; }
+void fused_release(FusedPlan& fp) {
+  if (fp.scratch) cudaFree(fp.scratch);
+  fp.scratch = nullptr;
+  fp.active = 0;
+}
 
 }  // namespace wd

@@ -15,6 +15,7 @@ struct FusedInputs {
   Metric M;
   FilterCoef fcoef;
   TriDev filt[3];
+  int filt_swaps[3];
   double sumS_c, cflms_c, lref;
   double* bufs[6];  // dt, acc, p, k, tmp, tmp2 (N each)
 };
@@ -23,6 +24,8 @@ struct FusedPlan {
   int active = 0;
   int kind = 0;          // which specialised path
   FusedInputs in;
+  double* scratch = nullptr;  // filter-sweep forward values (L2-resident)
+  int sweep_ctas = 0;
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).

@@ -129,7 +129,56 @@ struct SLine {  // shared-memory line addressed by global index
   __device__ __forceinline__ double operator()(int j) const { return p[(j - base) * st]; }
 };
 
-__device__ __forceinline__ int wrapi(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+__device__ __forceinline__ int wrapm(int x, int n) {
+  x %= n;
+  return x < 0 ? x + n : x;
+}
+
+// Values one thread loads for plane i (software-pipelined one plane ahead).
+struct F3Plane {
+  double own;    // own P slot when the thread is outside the domain (periodic wrap)
+  double jh;     // j-halo row value (ty < 2*HP)
+  double kh;     // k-halo column value (tx < 2*HP)
+  double A, dt, acc;
+  double pnext;  // axis-0 window entry p(i + 5 + R)
+};
+
+template <int R, int STAGE>
+__device__ __forceinline__ void f3_load_plane(const F3Args& a, int i, int j0, int k0, int tx,
+                                              int ty, bool act, F3Plane& v) {
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const int k = k0 + tx, j = j0 + ty;
+  const long long plane = (long long)i * a.s0;
+  v.own = 0.0;
+  if (!act && (k < n2 || a.per2) && (j < n1 || a.per1)) {
+    const int jw = j < n1 ? j : wrapm(j, n1), kw = k < n2 ? k : wrapm(k, n2);
+    v.own = a.p[plane + (long long)jw * n2 + kw];
+  }
+  v.jh = 0.0;
+  if (ty < 2 * F3_HP && k < n2) {
+    const int jj = ty < F3_HP ? ty : ty + F3_TJ;
+    const int jg = j0 - F3_HP + jj;
+    if (a.per1) v.jh = a.p[plane + (long long)wrapm(jg, n1) * n2 + k];
+    else if (jg >= 0 && jg < n1) v.jh = a.p[plane + (long long)jg * n2 + k];
+  }
+  v.kh = 0.0;
+  if (tx < 2 * F3_HP && j < n1) {
+    const int kk = tx < F3_HP ? tx : tx + F3_TK;
+    const int kg = k0 - F3_HP + kk;
+    if (a.per2) v.kh = a.p[plane + (long long)j * n2 + wrapm(kg, n2)];
+    else if (kg >= 0 && kg < n2) v.kh = a.p[plane + (long long)j * n2 + kg];
+  }
+  v.A = v.dt = v.acc = v.pnext = 0.0;
+  if (act) {
+    const long long idx = plane + (long long)j * n2 + k;
+    v.A = __ldcs(a.A + idx);
+    if (STAGE > 1) v.dt = __ldcs(a.dt + idx);
+    if (STAGE > 1) v.acc = __ldcs(a.acc + idx);
+    const int nxt = i + 5 + R;
+    if (a.per0) v.pnext = a.p[(long long)wrapm(nxt, n0) * a.s0 + (long long)j * n2 + k];
+    else if (nxt < n0) v.pnext = a.p[(long long)nxt * a.s0 + (long long)j * n2 + k];
+  }
+}
 
 template <int R, bool EIK, int STAGE>
 __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
@@ -158,7 +207,7 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
     int pos = i0 - R + s;
     double v = 0.0;
     if (act) {
-      if (a.per0) v = a.p[(long long)wrapi(wrapi(pos, n0), n0) * s0 + col];
+      if (a.per0) v = a.p[(long long)wrapm(pos, n0) * s0 + col];
       else if (pos >= 0 && pos < n0) v = a.p[(long long)pos * s0 + col];
     }
     pw[s] = v;
@@ -170,14 +219,15 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
       const int q = i0 - 4 + s;
       double d = 0.0;
       if (act && (a.per0 || (q >= 0 && q < n0))) {
-        const int qq = a.per0 ? wrapi(q, n0) : q;
+        const int qq = a.per0 ? wrapm(q, n0) : q;
         d = deriv_explicit_at(gl, qq, n0, SCH, a.per0);
       }
       uw[s] = a.c0 * d;
       if (s >= 4) dw[s - 4] = d;
     }
   }
-
+  F3Plane cur;
+  f3_load_plane<R, STAGE>(a, i0, j0, k0, tx, ty, act, cur);
 
   for (int i = i0; i < i1; ++i) {
     const int b = (i - i0) & 1;
@@ -185,41 +235,13 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
     double* Ukb = smem + 2 * F3_PH * F3_PW + b * (F3_TJ * F3_UKW);
     double* Ujb = smem + 2 * F3_PH * F3_PW + 2 * F3_TJ * F3_UKW + b * (F3_UJH * F3_TK);
     const long long plane = (long long)i * s0;
-    // prefetch: next window value and this plane's pointwise fields
-    const int nxt = i + 5 + R;
-    double pnext = 0.0;
-    if (act) {
-      if (a.per0) pnext = a.p[(long long)wrapi(nxt % n0, n0) * s0 + col];
-      else if (nxt < n0) pnext = a.p[(long long)nxt * s0 + col];
-    }
-    double Av = 0.0, dtv = 0.0, accv = 0.0;
-    if (act) {
-      Av = a.A[plane + col];
-      if (STAGE > 1) dtv = a.dt[plane + col];
-      if (STAGE == 2 || STAGE == 3 || STAGE == 4) accv = a.acc[plane + col];
-    }
     // ---- plane i into shared memory (own value from the window)
-    Pb[(ty + F3_HP) * F3_PW + tx + F3_HP] = pw[R];
-    if (ty < 2 * F3_HP) {  // j halo rows
-      const int jj = ty < F3_HP ? ty : ty + F3_TJ;  // tile-relative row
-      const int jg = j0 - F3_HP + jj;
-      double v = 0.0;
-      if (k < n2) {
-        if (a.per1) v = a.p[plane + (long long)wrapi(jg, n1) * n2 + k];
-        else if (jg >= 0 && jg < n1) v = a.p[plane + (long long)jg * n2 + k];
-      }
-      Pb[jj * F3_PW + tx + F3_HP] = v;
-    }
-    if (tx < 2 * F3_HP) {  // k halo columns
-      const int kk = tx < F3_HP ? tx : tx + F3_TK;
-      const int kg = k0 - F3_HP + kk;
-      double v = 0.0;
-      if (j < n1) {
-        if (a.per2) v = a.p[plane + (long long)j * n2 + wrapi(kg, n2)];
-        else if (kg >= 0 && kg < n2) v = a.p[plane + (long long)j * n2 + kg];
-      }
-      Pb[(ty + F3_HP) * F3_PW + kk] = v;
-    }
+    Pb[(ty + F3_HP) * F3_PW + tx + F3_HP] = act ? pw[R] : cur.own;
+    if (ty < 2 * F3_HP) Pb[(ty < F3_HP ? ty : ty + F3_TJ) * F3_PW + tx + F3_HP] = cur.jh;
+    if (tx < 2 * F3_HP) Pb[(ty + F3_HP) * F3_PW + (tx < F3_HP ? tx : tx + F3_TK)] = cur.kh;
+    const double Av = cur.A, dtin = cur.dt, accv = cur.acc, pnext = cur.pnext;
+    // ---- prefetch plane i + 1 (latency hidden behind this plane's math)
+    if (i + 1 < i1) f3_load_plane<R, STAGE>(a, i + 1, j0, k0, tx, ty, act, cur);
     __syncthreads();
     // ---- U_k on [TJ] x [TK + 2HU], U_j on [TJ + 2HU] x [TK]
     for (int t = tx; t < F3_UKW; t += F3_TK) {
@@ -227,7 +249,7 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
       double v = 0.0;
       if (j < n1 && (a.per2 || (kg >= 0 && kg < n2))) {
         SLine ln{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
-        v = a.c2 * deriv_explicit_at(ln, a.per2 ? kg : kg, n2, SCH, a.per2);
+        v = a.c2 * deriv_explicit_at(ln, kg, n2, SCH, a.per2);
       }
       Ukb[ty * F3_UKW + t] = v;
     }
@@ -276,16 +298,16 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
         double den = fabs(H0) + fabs(H1) + fabs(H2);
         if (!EIK) den = den + 2.0 * (a.eps * pv) * a.sumS;
         const double d = a.cfl / (den + 1e-30);
-        dtv = np_min(d, a.cflms);
-        a.dt[idx] = dtv;
-        a.acc[idx] = kv;
+        const double dtv = np_min(d, a.cflms);
+        __stcs(a.dt + idx, dtv);
+        __stcs(a.acc + idx, kv);
         a.out[idx] = pinned ? 0.0 : Av + (0.5 * dtv) * kv;
       } else if (STAGE == 2 || STAGE == 3) {
-        a.acc[idx] = accv + 2.0 * kv;
-        const double cdt = STAGE == 3 ? dtv : 0.5 * dtv;
+        __stcs(a.acc + idx, accv + 2.0 * kv);
+        const double cdt = STAGE == 3 ? dtin : 0.5 * dtin;
         a.out[idx] = pinned ? 0.0 : Av + cdt * kv;
       } else {
-        a.out[idx] = pinned ? 0.0 : Av + (dtv / 6.0) * (accv + kv);
+        a.out[idx] = pinned ? 0.0 : Av + (dtin / 6.0) * (accv + kv);
       }
     }
     // ---- advance the axis-0 windows

@@ -22,6 +22,7 @@ struct TriDev {
   const double* du2;
   const double* swap;  // 0.0 / 1.0
   const double* z;     // cyclic correction vector
+  const double* rinv;  // RN(1/d) per row (fused sweeps)
   double vn, denom;
 };
 
