@@ -3,24 +3,28 @@
 // interchanges occur for the filter matrix).
 //
 // Layout / data movement: one warp owns 32 grid lines (lane = line) and
-// walks them row by row.  Axes 0/1: the 32 lines are 32 consecutive k, so
-// every row access is one coalesced 256-byte segment.  Axis 2 (contiguous
-// lines): rows are staged through a padded 32x33 shared-memory transpose.
-// The forward-elimination values are parked in a lane-contiguous scratch
-// region private to the warp (sized so all resident warps' scratch stays
-// L2-resident), then read back in reverse for the back substitution.  HBM
-// traffic is therefore one read + one write per node (+ one read of phi for
-// the fused convergence reduction on the last axis).
+// walks them row by row in chunks of 32 rows.  Axes 0/1: the 32 lines are 32
+// consecutive k, so every row access is one coalesced 256-byte segment.
+// Axis 2 (contiguous lines): each chunk is staged through a padded 32x33
+// shared-memory transpose.  The forward-elimination values are parked in a
+// lane-contiguous scratch slab private to the warp (sized so all resident
+// warps' slabs stay L2-resident) and read back in reverse for the back
+// substitution.  Every chunk is loaded into registers one chunk ahead, so
+// the only serial dependency is the recurrence itself.  The factor
+// (dgtsv order) lives in shared memory.  HBM traffic: one read + one write
+// per node (+ one read of phi for the fused convergence reduction on the
+// last axis).
 //
 // Division: x_i = (y_i - du_i x_{i+1}) / d_i is evaluated as a correctly
-// rounded quotient from the precomputed reciprocal (Markstein: q0 = s*r,
-// e = fma(-q0, d, s), q = fma(e, r, q0)), which equals IEEE s / d; the
-// parity tests check bit equality with the reference.
+// rounded quotient from the precomputed reciprocal r_i = RN(1/d_i)
+// (Markstein: q0 = s*r, e = fma(-q0, d, s), q = fma(e, r, q0)), equal to
+// IEEE s / d; the parity tests check bit equality with the reference.
 #pragma once
 
 #include "wd_kernels.cuh"
 
 namespace wd {
+
 
 struct SweepArgs {
   const double* in;
@@ -61,18 +65,61 @@ __device__ __forceinline__ double filt_rhs(const double* w, int h, const FilterC
     if (k <= h) v = v + c[k] * (w[5 + k] + w[5 - k]);
   return v;
 }
+__device__ __forceinline__ double filt_rhs5(const double* w, const FilterCoef& fc) {
+  const double* c = fc.hc + 30;
+  return c[0] * w[5] + c[1] * (w[6] + w[4]) + c[2] * (w[7] + w[3]) + c[3] * (w[8] + w[2]) +
+         c[4] * (w[9] + w[1]) + c[5] * (w[10] + w[0]);
+}
+
+// rows per chunk: 32 for the transposed (contiguous-line) axis, 16 otherwise
+template <bool CONTIG>
+struct SwCh { static constexpr int v = CONTIG ? 32 : 16; };
 
 template <bool CONTIG>
-__global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
+__device__ __forceinline__ void sw_load_chunk(const SweepArgs& a, double (*T)[33], int lane, int c,
+                                              int nl, bool valid, long long base,
+                                              long long gbase, long long rstride, double* v) {
+  constexpr int CH = SwCh<CONTIG>::v;
+  const int n = a.n;
+  const int r0 = c * CH;
+  if (CONTIG) {
+    const int r = r0 + lane;
+#pragma unroll
+    for (int m = 0; m < 32; ++m)
+      v[m] = (m < nl && r < n) ? __ldcs(a.in + gbase + (long long)m * a.n2 + r) : 0.0;
+  } else {
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const int r = r0 + s;
+      v[s] = (valid && r < n) ? __ldcs(a.in + base + (long long)r * rstride) : 0.0;
+    }
+  }
+}
+
+template <bool CONTIG>
+__global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
-  __shared__ double tile[4][32][33];
+  extern __shared__ double sw_smem[];
+  double(*tile)[32][33] = reinterpret_cast<double(*)[32][33]>(sw_smem);
+  const int n = a.n;
+  double* sf0 = sw_smem + 4 * 32 * 33;  // fact | du | d | rinv | z, n each
+  double* sf1 = sf0 + n;
+  double* sf2 = sf1 + n;
+  double* sf3 = sf2 + n;
+  double* sf4 = sf3 + n;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    sf0[t] = a.fact[t];
+    sf1[t] = a.du[t];
+    sf2[t] = a.d[t];
+    sf3[t] = a.rinv[t];
+    sf4[t] = a.per ? a.z[t] : 0.0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const int n = a.n;
   double(*T)[33] = tile[wib];
   double* scr = a.scratch + (long long)gw * n * 32;
-  // line groups of 32
   long long groups, lines_per_row_blk;
   long long rstride;
   if (a.axis == 2) {
@@ -84,15 +131,15 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
     groups = (long long)(a.axis == 0 ? a.n1 : a.n0) * lines_per_row_blk;
     rstride = a.axis == 0 ? a.s0 : a.n2;
   }
+  constexpr int CH = SwCh<CONTIG>::v;
+  const int nch = (n + CH - 1) / CH;
   double md = 0.0, ma = 0.0;
   int bad = 0;
   for (long long g = gw; g < groups; g += nwarps) {
     const long long outer = g / lines_per_row_blk;
     const int blk = (int)(g % lines_per_row_blk);
-    // base offset of this lane's line and lane validity
-    long long base;
+    long long base, gbase = 0;
     bool valid;
-    long long gbase = 0;  // CONTIG: offset of line 0 of the group (row 0)
     if (a.axis == 2) {
       const int j = blk * 32 + lane;
       valid = j < a.n1;
@@ -118,50 +165,51 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
     // ---------------- forward elimination
     double w[11];
 #pragma unroll
-    for (int s = 0; s < 11; ++s) w[s] = 0.0;
-    // window holds rows t-10..t; preload rows -5..-1 into slots 6..10
+    for (int s = 0; s < 6; ++s) w[s] = 0.0;
 #pragma unroll
-    for (int s = 6; s < 11; ++s) w[s] = ld(s - 11);
+    for (int s = 6; s < 11; ++s) w[s] = ld(s - 11);  // rows -5..-1
     double y = 0.0;
-    const int nch = (n + 31) / 32;
+    double nxt[CH];
+    sw_load_chunk<CONTIG>(a, T, lane, 0, nl, valid, base, gbase, rstride, nxt);
     for (int c = 0; c < nch; ++c) {
-      const int r0 = c * 32;
-      double v[32];
+      const int r0 = c * CH;
+      double v[CH];
       if (CONTIG) {
-        // coalesced: lane reads column (r0 + lane) of each of the nl lines
-        double tv[32];
-#pragma unroll
-        for (int m = 0; m < 32; ++m) {
-          const int r = r0 + lane;
-          tv[m] = (m < nl && r < n) ? a.in[gbase + (long long)m * a.n2 + r] : 0.0;
-        }
         __syncwarp();
 #pragma unroll
-        for (int m = 0; m < 32; ++m) T[m][lane] = tv[m];
+        for (int m = 0; m < 32; ++m) T[m][lane] = nxt[m];
         __syncwarp();
 #pragma unroll
         for (int s = 0; s < 32; ++s) v[s] = T[lane][s];
       } else {
 #pragma unroll
-        for (int s = 0; s < 32; ++s) {
-          const int r = r0 + s;
-          v[s] = (valid && r < n) ? a.in[base + (long long)r * rstride] : 0.0;
-        }
+        for (int s = 0; s < CH; ++s) v[s] = nxt[s];
       }
+      if (c + 1 < nch) sw_load_chunk<CONTIG>(a, T, lane, c + 1, nl, valid, base, gbase, rstride, nxt);
+      const bool interior = a.per || (r0 >= 10 && r0 + CH + 5 <= n - 5);
+      double yo[CH];
 #pragma unroll
-      for (int s = 0; s < 32; ++s) {
+      for (int s = 0; s < CH; ++s) {
         const int t = r0 + s;  // newest row
-        if (t >= n) break;
+        if (t >= n) continue;
 #pragma unroll
         for (int q = 0; q < 10; ++q) w[q] = w[q + 1];
         w[10] = v[s];
         const int r = t - 5;
-        if (r >= 0) {
-          const int h = a.per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
-          const double rhs = filt_rhs(w, h, a.fc);
-          y = r == 0 ? rhs : rhs - a.fact[r - 1] * y;
-          scr[(long long)r * 32 + lane] = y;
+        double rhs;
+        if (interior) {
+          rhs = filt_rhs5(w, a.fc);
+        } else {
+          const int h = (r <= 0 || r >= n - 1) ? 0 : min(min(r, n - 1 - r), 5);
+          rhs = filt_rhs(w, h, a.fc);
         }
+        if (r >= 0) y = r == 0 ? rhs : rhs - sf0[r - 1] * y;
+        yo[s] = y;
+      }
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        const int r = r0 + s - 5;
+        if (r >= 0 && r0 + s < n) scr[(long long)r * 32 + lane] = yo[s];
       }
     }
     // rows n..n+4 (periodic wrap or zero) finish the last 5 right-hand sides
@@ -175,68 +223,83 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
       if (r >= 0 && r < n) {
         const int h = a.per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
         const double rhs = filt_rhs(w, h, a.fc);
-        y = r == 0 ? rhs : rhs - a.fact[r - 1] * y;
+        y = r == 0 ? rhs : rhs - sf0[r - 1] * y;
         scr[(long long)r * 32 + lane] = y;
       }
     }
     __syncwarp();
     // ---------------- back substitution (+ cyclic correction)
-    double x1 = 0.0;
-    double xlast = 0.0;
     const bool cyc = a.per;
-    for (int c = nch - 1; c >= 0; --c) {
-      const int r0 = c * 32;
-      double o[32];
+    double x1 = 0.0, xlast = 0.0;
+    double yn[CH];
 #pragma unroll
-      for (int s = 31; s >= 0; --s) {
+    for (int s = 0; s < CH; ++s) {
+      const int r = (nch - 1) * CH + s;
+      yn[s] = r < n ? scr[(long long)r * 32 + lane] : 0.0;
+    }
+    for (int c = nch - 1; c >= 0; --c) {
+      const int r0 = c * CH;
+      double yv[CH];
+#pragma unroll
+      for (int s = 0; s < CH; ++s) yv[s] = yn[s];
+      if (c > 0) {
+#pragma unroll
+        for (int s = 0; s < CH; ++s) yn[s] = scr[(long long)(r0 - CH + s) * 32 + lane];
+      }
+      double o[CH];
+#pragma unroll
+      for (int s = CH - 1; s >= 0; --s) {
         const int r = r0 + s;
         double x = 0.0;
         if (r < n) {
-          const double yr = scr[(long long)r * 32 + lane];
           if (r == n - 1) {
-            x = yr / a.d[r];
+            x = yv[s] / sf2[r];
             xlast = x;
           } else {
-            x = div_rn(yr - a.du[r] * x1, a.d[r], a.rinv[r]);
+            x = div_rn(yv[s] - sf1[r] * x1, sf2[r], sf3[r]);
           }
           x1 = x;
-          if (cyc) scr[(long long)r * 32 + lane] = x;
         }
         o[s] = x;
       }
-      if (!cyc) {
-        // final values: write out (+ convergence reduction)
-        if (CONTIG) {
-          __syncwarp();
+      if (cyc) {
 #pragma unroll
-          for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
-          __syncwarp();
-          for (int m = 0; m < nl; ++m) {
-            const int r = r0 + lane;
-            if (r < n) {
-              const long long idx = gbase + (long long)m * a.n2 + r;
-              const double xv = T[m][lane];
-              a.out[idx] = xv;
-              if (a.A) {
-                if (!isfinite(xv)) bad = 1;
-                ma = fmax(ma, fabs(xv));
-                md = fmax(md, fabs(xv - a.A[idx]));
-              }
+        for (int s = 0; s < CH; ++s)
+          if (r0 + s < n) scr[(long long)(r0 + s) * 32 + lane] = o[s];
+        continue;
+      }
+      // final values: write out (+ convergence reduction)
+      if (CONTIG) {
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
+        __syncwarp();
+        const int r = r0 + lane;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+          if (m < nl && r < n) {
+            const long long idx = gbase + (long long)m * a.n2 + r;
+            const double xv = T[m][lane];
+            __stcs(a.out + idx, xv);
+            if (a.A) {
+              if (!isfinite(xv)) bad = 1;
+              ma = fmax(ma, fabs(xv));
+              md = fmax(md, fabs(xv - __ldcs(a.A + idx)));
             }
           }
-        } else if (valid) {
+        }
+      } else if (valid) {
 #pragma unroll
-          for (int s = 0; s < 32; ++s) {
-            const int r = r0 + s;
-            if (r < n) {
-              const long long idx = base + (long long)r * rstride;
-              a.out[idx] = o[s];
-              if (a.A) {
-                const double xv = o[s];
-                if (!isfinite(xv)) bad = 1;
-                ma = fmax(ma, fabs(xv));
-                md = fmax(md, fabs(xv - a.A[idx]));
-              }
+        for (int s = 0; s < CH; ++s) {
+          const int r = r0 + s;
+          if (r < n) {
+            const long long idx = base + (long long)r * rstride;
+            __stcs(a.out + idx, o[s]);
+            if (a.A) {
+              const double xv = o[s];
+              if (!isfinite(xv)) bad = 1;
+              ma = fmax(ma, fabs(xv));
+              md = fmax(md, fabs(xv - __ldcs(a.A + idx)));
             }
           }
         }
@@ -247,43 +310,49 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
       const double f = (x1 + a.vn * xlast) / a.denom;
       __syncwarp();
       for (int c = 0; c < nch; ++c) {
-        const int r0 = c * 32;
-        double o[32];
+        const int r0 = c * CH;
+        double o[CH];
 #pragma unroll
-        for (int s = 0; s < 32; ++s) {
+        for (int s = 0; s < CH; ++s) {
           const int r = r0 + s;
-          o[s] = r < n ? scr[(long long)r * 32 + lane] - f * a.z[r] : 0.0;
+          o[s] = r < n ? scr[(long long)r * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          const int r = r0 + s;
+          o[s] = r < n ? o[s] - f * sf4[r] : 0.0;
         }
         if (CONTIG) {
           __syncwarp();
 #pragma unroll
           for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
           __syncwarp();
-          for (int m = 0; m < nl; ++m) {
-            const int r = r0 + lane;
-            if (r < n) {
+          const int r = r0 + lane;
+#pragma unroll
+          for (int m = 0; m < 32; ++m) {
+            if (m < nl && r < n) {
               const long long idx = gbase + (long long)m * a.n2 + r;
               const double xv = T[m][lane];
-              a.out[idx] = xv;
+              __stcs(a.out + idx, xv);
               if (a.A) {
                 if (!isfinite(xv)) bad = 1;
                 ma = fmax(ma, fabs(xv));
-                md = fmax(md, fabs(xv - a.A[idx]));
+                md = fmax(md, fabs(xv - __ldcs(a.A + idx)));
               }
             }
           }
         } else if (valid) {
 #pragma unroll
-          for (int s = 0; s < 32; ++s) {
+          for (int s = 0; s < CH; ++s) {
             const int r = r0 + s;
             if (r < n) {
               const long long idx = base + (long long)r * rstride;
-              a.out[idx] = o[s];
+              __stcs(a.out + idx, o[s]);
               if (a.A) {
                 const double xv = o[s];
                 if (!isfinite(xv)) bad = 1;
                 ma = fmax(ma, fabs(xv));
-                md = fmax(md, fabs(xv - a.A[idx]));
+                md = fmax(md, fabs(xv - __ldcs(a.A + idx)));
               }
             }
           }

@@ -71,6 +71,15 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
       return;
     }
     fp.sweep_ctas = ctas;
+    const int smem = (int)((4 * 32 * 33 + 5 * (size_t)nmax) * sizeof(double));
+    if (cudaFuncSetAttribute(k_filter_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_filter_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess) {
+      cudaFree(fp.scratch);
+      fp.scratch = nullptr;
+      return;
+    }
   }
   fp.kind = PATH_F3;
   fp.active = 1;
@@ -166,10 +175,11 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     const long long groups = (L + 31) / 32;
     long long ctas = (groups + 3) / 4;
     if (ctas > fp.sweep_ctas) ctas = fp.sweep_ctas;
+    const size_t smem = (4 * 32 * 33 + 5 * (size_t)w.n) * sizeof(double);
     if (ax == 2)
-      k_filter_sweep<true><<<(int)ctas, 128, 0, s>>>(w);
+      k_filter_sweep<true><<<(int)ctas, 128, smem, s>>>(w);
     else
-      k_filter_sweep<false><<<(int)ctas, 128, 0, s>>>(w);
+      k_filter_sweep<false><<<(int)ctas, 128, smem, s>>>(w);
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }

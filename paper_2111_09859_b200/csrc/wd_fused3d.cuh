@@ -143,40 +143,50 @@ struct F3Plane {
   double pnext;  // axis-0 window entry p(i + 5 + R)
 };
 
-template <int R, int STAGE>
-__device__ __forceinline__ void f3_load_plane(const F3Args& a, int i, int j0, int k0, int tx,
-                                              int ty, bool act, F3Plane& v) {
-  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+// Per-thread in-plane offsets, fixed for the whole i-stream (-1 = unused).
+struct F3Offs {
+  int own, jh, kh, node;
+};
+
+__device__ __forceinline__ F3Offs f3_offsets(const F3Args& a, int j0, int k0, int tx, int ty,
+                                             bool act) {
+  const int n1 = a.n1, n2 = a.n2;
   const int k = k0 + tx, j = j0 + ty;
-  const long long plane = (long long)i * a.s0;
-  v.own = 0.0;
+  F3Offs o;
+  o.node = act ? j * n2 + k : -1;
+  o.own = -1;
   if (!act && (k < n2 || a.per2) && (j < n1 || a.per1)) {
     const int jw = j < n1 ? j : wrapm(j, n1), kw = k < n2 ? k : wrapm(k, n2);
-    v.own = a.p[plane + (long long)jw * n2 + kw];
+    o.own = jw * n2 + kw;
   }
-  v.jh = 0.0;
+  o.jh = -1;
   if (ty < 2 * F3_HP && k < n2) {
-    const int jj = ty < F3_HP ? ty : ty + F3_TJ;
-    const int jg = j0 - F3_HP + jj;
-    if (a.per1) v.jh = a.p[plane + (long long)wrapm(jg, n1) * n2 + k];
-    else if (jg >= 0 && jg < n1) v.jh = a.p[plane + (long long)jg * n2 + k];
+    const int jg = j0 - F3_HP + (ty < F3_HP ? ty : ty + F3_TJ);
+    if (a.per1) o.jh = wrapm(jg, n1) * n2 + k;
+    else if (jg >= 0 && jg < n1) o.jh = jg * n2 + k;
   }
-  v.kh = 0.0;
+  o.kh = -1;
   if (tx < 2 * F3_HP && j < n1) {
-    const int kk = tx < F3_HP ? tx : tx + F3_TK;
-    const int kg = k0 - F3_HP + kk;
-    if (a.per2) v.kh = a.p[plane + (long long)j * n2 + wrapm(kg, n2)];
-    else if (kg >= 0 && kg < n2) v.kh = a.p[plane + (long long)j * n2 + kg];
+    const int kg = k0 - F3_HP + (tx < F3_HP ? tx : tx + F3_TK);
+    if (a.per2) o.kh = j * n2 + wrapm(kg, n2);
+    else if (kg >= 0 && kg < n2) o.kh = j * n2 + kg;
   }
+  return o;
+}
+
+template <int STAGE>
+__device__ __forceinline__ void f3_load_plane(const F3Args& a, const double* __restrict__ pp,
+                                              long long plane, const double* __restrict__ pn,
+                                              const F3Offs& o, F3Plane& v) {
+  v.own = o.own >= 0 ? pp[o.own] : 0.0;
+  v.jh = o.jh >= 0 ? pp[o.jh] : 0.0;
+  v.kh = o.kh >= 0 ? pp[o.kh] : 0.0;
   v.A = v.dt = v.acc = v.pnext = 0.0;
-  if (act) {
-    const long long idx = plane + (long long)j * n2 + k;
-    v.A = __ldcs(a.A + idx);
-    if (STAGE > 1) v.dt = __ldcs(a.dt + idx);
-    if (STAGE > 1) v.acc = __ldcs(a.acc + idx);
-    const int nxt = i + 5 + R;
-    if (a.per0) v.pnext = a.p[(long long)wrapm(nxt, n0) * a.s0 + (long long)j * n2 + k];
-    else if (nxt < n0) v.pnext = a.p[(long long)nxt * a.s0 + (long long)j * n2 + k];
+  if (o.node >= 0) {
+    v.A = __ldcs(a.A + plane + o.node);
+    if (STAGE > 1) v.dt = __ldcs(a.dt + plane + o.node);
+    if (STAGE > 1) v.acc = __ldcs(a.acc + plane + o.node);
+    if (pn) v.pnext = pn[o.node];
   }
 }
 
@@ -226,8 +236,18 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
       if (s >= 4) dw[s - 4] = d;
     }
   }
+  const F3Offs offs = f3_offsets(a, j0, k0, tx, ty, act);
+  // plane index of the axis-0 window entry i + 5 + R (wrapped incrementally)
+  int inext = a.per0 ? wrapm(i0 + 5 + R, n0) : i0 + 5 + R;
+  auto next_ptr = [&](int ip) -> const double* {
+    return (a.per0 || ip < n0) ? a.p + (long long)ip * s0 : nullptr;
+  };
   F3Plane cur;
-  f3_load_plane<R, STAGE>(a, i0, j0, k0, tx, ty, act, cur);
+  f3_load_plane<STAGE>(a, a.p + (long long)i0 * s0, (long long)i0 * s0, next_ptr(inext), offs,
+                       cur);
+  // CTA-uniform: does the tile (with halo) stay clear of non-periodic ends?
+  const bool kfast = a.per2 ? (k0 + F3_TK <= n2) : (k0 >= F3_HP && k0 + F3_TK + F3_HP <= n2);
+  const bool jfast = a.per1 ? (j0 + F3_TJ <= n1) : (j0 >= F3_HP && j0 + F3_TJ + F3_HP <= n1);
 
   for (int i = i0; i < i1; ++i) {
     const int b = (i - i0) & 1;
@@ -241,42 +261,91 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
     if (tx < 2 * F3_HP) Pb[(ty + F3_HP) * F3_PW + (tx < F3_HP ? tx : tx + F3_TK)] = cur.kh;
     const double Av = cur.A, dtin = cur.dt, accv = cur.acc, pnext = cur.pnext;
     // ---- prefetch plane i + 1 (latency hidden behind this plane's math)
-    if (i + 1 < i1) f3_load_plane<R, STAGE>(a, i + 1, j0, k0, tx, ty, act, cur);
+    inext = inext + 1;
+    if (a.per0 && inext == n0) inext = 0;
+    if (i + 1 < i1)
+      f3_load_plane<STAGE>(a, a.p + plane + s0, plane + s0, next_ptr(inext), offs, cur);
     __syncthreads();
     // ---- U_k on [TJ] x [TK + 2HU], U_j on [TJ + 2HU] x [TK]
-    for (int t = tx; t < F3_UKW; t += F3_TK) {
-      const int kg = k0 - F3_HU + t;
-      double v = 0.0;
-      if (j < n1 && (a.per2 || (kg >= 0 && kg < n2))) {
-        SLine ln{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
-        v = a.c2 * deriv_explicit_at(ln, kg, n2, SCH, a.per2);
-      }
-      Ukb[ty * F3_UKW + t] = v;
-    }
-    for (int t = ty; t < F3_UJH; t += F3_TJ) {
-      const int jg = j0 - F3_HU + t;
-      double v = 0.0;
-      if (k < n2 && (a.per1 || (jg >= 0 && jg < n1))) {
-        SLine ln{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
-        v = a.c1 * deriv_explicit_at(ln, jg, n1, SCH, a.per1);
-      }
-      Ujb[t * F3_TK + tx] = v;
-    }
-    // own directional derivatives d_2, d_1 (plane values, from smem)
     double d2 = 0.0, d1 = 0.0;
-    if (act) {
-      SLine lk{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
-      d2 = deriv_explicit_at(lk, k, n2, SCH, a.per2);
-      SLine lj{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
-      d1 = deriv_explicit_at(lj, j, n1, SCH, a.per1);
+    if (kfast) {  // interior / periodic tile: central stencil, compile-time offsets
+      const double* row = Pb + (ty + F3_HP) * F3_PW + 3;  // row[t] <-> kg = k0 - 4 + t
+      Ukb[ty * F3_UKW + tx] = a.c2 * central<R>(row[tx - 3], row[tx - 2], row[tx - 1],
+                                                row[tx + 1], row[tx + 2], row[tx + 3]);
+      if (tx < 2 * F3_HU) {
+        const int t = tx + F3_TK;
+        Ukb[ty * F3_UKW + t] = a.c2 * central<R>(row[t - 3], row[t - 2], row[t - 1], row[t + 1],
+                                                 row[t + 2], row[t + 3]);
+      }
+      const int c = tx + 4;
+      d2 = central<R>(row[c - 3], row[c - 2], row[c - 1], row[c + 1], row[c + 2], row[c + 3]);
+    } else {
+      for (int t = tx; t < F3_UKW; t += F3_TK) {
+        const int kg = k0 - F3_HU + t;
+        double v = 0.0;
+        if (j < n1 && (a.per2 || (kg >= 0 && kg < n2))) {
+          SLine ln{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
+          v = a.c2 * deriv_explicit_at(ln, kg, n2, SCH, a.per2);
+        }
+        Ukb[ty * F3_UKW + t] = v;
+      }
+      if (act) {
+        SLine lk{Pb + (ty + F3_HP) * F3_PW, k0 - F3_HP, 1};
+        d2 = deriv_explicit_at(lk, k, n2, SCH, a.per2);
+      }
+    }
+    if (jfast) {
+      const double* colp = Pb + tx + F3_HP + 3 * F3_PW;  // colp[t*PW] <-> jg = j0 - 4 + t
+      Ujb[ty * F3_TK + tx] =
+          a.c1 * central<R>(colp[(ty - 3) * F3_PW], colp[(ty - 2) * F3_PW],
+                            colp[(ty - 1) * F3_PW], colp[(ty + 1) * F3_PW],
+                            colp[(ty + 2) * F3_PW], colp[(ty + 3) * F3_PW]);
+      if (ty < 2 * F3_HU) {
+        const int t = ty + F3_TJ;
+        Ujb[t * F3_TK + tx] =
+            a.c1 * central<R>(colp[(t - 3) * F3_PW], colp[(t - 2) * F3_PW],
+                              colp[(t - 1) * F3_PW], colp[(t + 1) * F3_PW],
+                              colp[(t + 2) * F3_PW], colp[(t + 3) * F3_PW]);
+      }
+      const int c = ty + 4;
+      d1 = central<R>(colp[(c - 3) * F3_PW], colp[(c - 2) * F3_PW], colp[(c - 1) * F3_PW],
+                      colp[(c + 1) * F3_PW], colp[(c + 2) * F3_PW], colp[(c + 3) * F3_PW]);
+    } else {
+      for (int t = ty; t < F3_UJH; t += F3_TJ) {
+        const int jg = j0 - F3_HU + t;
+        double v = 0.0;
+        if (k < n2 && (a.per1 || (jg >= 0 && jg < n1))) {
+          SLine ln{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
+          v = a.c1 * deriv_explicit_at(ln, jg, n1, SCH, a.per1);
+        }
+        Ujb[t * F3_TK + tx] = v;
+      }
+      if (act) {
+        SLine lj{Pb + tx + F3_HP, j0 - F3_HP, F3_PW};
+        d1 = deriv_explicit_at(lj, j, n1, SCH, a.per1);
+      }
     }
     __syncthreads();
     if (act) {
-      SLine uk{Ukb + ty * F3_UKW, k0 - F3_HU, 1};
-      SLine uj{Ujb + tx, j0 - F3_HU, F3_TK};
-      const double D2 = deriv_explicit_at(uk, k, n2, SCH, a.per2);
-      const double D1 = deriv_explicit_at(uj, j, n1, SCH, a.per1);
-      const double D0 = d0_from_window<R>(uw, i, n0, a.per0);
+      double D2, D1;
+      if (kfast) {
+        const double* u = Ukb + ty * F3_UKW + tx + F3_HU;
+        D2 = central<R>(u[-3], u[-2], u[-1], u[1], u[2], u[3]);
+      } else {
+        SLine uk{Ukb + ty * F3_UKW, k0 - F3_HU, 1};
+        D2 = deriv_explicit_at(uk, k, n2, SCH, a.per2);
+      }
+      if (jfast) {
+        const double* u = Ujb + (ty + F3_HU) * F3_TK + tx;
+        D1 = central<R>(u[-3 * F3_TK], u[-2 * F3_TK], u[-F3_TK], u[F3_TK], u[2 * F3_TK],
+                        u[3 * F3_TK]);
+      } else {
+        SLine uj{Ujb + tx, j0 - F3_HU, F3_TK};
+        D1 = deriv_explicit_at(uj, j, n1, SCH, a.per1);
+      }
+      const double D0 = (a.per0 || (i >= 4 && i <= n0 - 5))
+                            ? central<R>(uw[1], uw[2], uw[3], uw[5], uw[6], uw[7])
+                            : d0_from_window<R>(uw, i, n0, a.per0);
       const double d0 = dw[0];
       const double pv = pw[R];
       // U_m = c_m d_m ; U_hat_l = c_l U_l (diagonal metrics)
@@ -316,7 +385,13 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
     pw[NPW - 1] = pnext;
     const int q = i + 5;
     double dq = 0.0;
-    if (act && (a.per0 || q < n0)) dq = d0_entering<R>(pw, q, n0, a.per0);
+    if (act && (a.per0 || q < n0)) {
+      constexpr int Q = 4 + R;
+      dq = (a.per0 || q <= n0 - 5)
+               ? central<R>(R >= 3 ? pw[Q - 3] : 0.0, R >= 2 ? pw[Q - 2] : 0.0, pw[Q - 1],
+                            pw[Q + 1], R >= 2 ? pw[Q + 2] : 0.0, R >= 3 ? pw[Q + 3] : 0.0)
+               : d0_entering<R>(pw, q, n0, a.per0);
+    }
 #pragma unroll
     for (int s = 0; s < 8; ++s) uw[s] = uw[s + 1];
     uw[8] = a.c0 * dq;
