@@ -194,7 +194,7 @@ def run_b200(args, world, rank, local):
     filt = W.FilterConfig(cfg["alpha_f"]) if cfg["alpha_f"] else None
     K, Wm = args.steps, args.warmup
     ctx = _context.NativeSolver(grid, cfg["faces"], None, cfg["scheme"], fc, filt, 0.5, 1e-15,
-                                10**9)
+                                10**9, arith=args.arith)
     lib = ctx.lib
     N = int(np.prod(dims))
     phi = torch.zeros(dims, dtype=torch.float64, device="cuda")
@@ -269,7 +269,7 @@ def run_b200(args, world, rank, local):
     if not args.no_e2e:
         phi0 = torch.zeros(dims, dtype=torch.float64).pin_memory()
         scfg = W.SolveConfig(formulation=fc, scheme=cfg["scheme"], filter_config=filt, cfl=0.5,
-                             tol=1e-15, max_iters=K)
+                             tol=1e-15, max_iters=K, arith=args.arith)
         bnd = W.BoundarySpec(cfg["faces"])
         torch.cuda.synchronize()
         barrier(world)
@@ -288,7 +288,7 @@ def run_b200(args, world, rank, local):
             "steps": K, "warmup": Wm, "ms_per_step": round(secs_max / K * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg["workload"], "dims": list(dims),
+            "config": {"workload": cfg["workload"], "dims": list(dims), "arith": args.arith,
                        "global_nodes": N * world, "parallelism": f"replica{world}",
                        "l2": "inputs larger than L2 (1.07 GB per field)",
                        "fused": True if kern else False},
@@ -314,6 +314,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override grid size (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -82,6 +82,9 @@ typedef struct wd_solver_desc {
   double cfl;                /* SolveConfig.cfl                           */
   double tol;                /* SolveConfig.tol                           */
   int max_iters;             /* SolveConfig.max_iters                     */
+  int arith;                 /* EXTENSION: 0 exact (bit-identical to the
+                                reference), 1 fast (FMA + composite
+                                Laplacian stencil; round-off differences) */
 } wd_solver_desc;
 
 typedef struct wd_status {

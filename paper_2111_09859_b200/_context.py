@@ -36,7 +36,7 @@ class NativeSolver:
     """wd_ctx for (grid, faces, mask, scheme, formulation, filter, cfl, tol)."""
 
     def __init__(self, grid, faces=None, solid_mask=None, scheme="E2", formulation=None,
-                 filter_config=None, cfl=0.5, tol=1e-5, max_iters=1):
+                 filter_config=None, cfl=0.5, tol=1e-5, max_iters=1, arith="exact"):
         import torch
         from .formulations import FormulationConfig
         self.torch = torch
@@ -82,6 +82,7 @@ class NativeSolver:
         sd.cfl = float(cfl)
         sd.tol = float(tol)
         sd.max_iters = int(max_iters)
+        sd.arith = {"exact": 0, "fast": 1}[arith]
         self.gd, self.sd = gd, sd
         ptr = ctypes.c_void_p()
         torch.cuda.synchronize()

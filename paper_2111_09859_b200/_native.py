@@ -62,6 +62,7 @@ class SolverDesc(ctypes.Structure):
         ("cfl", ctypes.c_double),
         ("tol", ctypes.c_double),
         ("max_iters", ctypes.c_int),
+        ("arith", ctypes.c_int),
     ]
 
 

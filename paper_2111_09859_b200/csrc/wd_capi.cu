@@ -524,6 +524,7 @@ int validate(const wd_grid_desc* gd, const wd_solver_desc* sd) {
   if (sd->use_filter && !(sd->alpha_f >= 0.40 && sd->alpha_f <= 0.5))
     return fail(WD_ERR_INVALID, "alpha_f must lie in [0.40, 0.5]");
   if (!(gd->ref_length > 0.0)) return fail(WD_ERR_INVALID, "ref_length must be positive");
+  if (sd->arith != 0 && sd->arith != 1) return fail(WD_ERR_INVALID, "arith must be 0 (exact) or 1 (fast)");
   for (int a = 0; a < gd->ndim; ++a) {
     const int lo = gd->face[2 * a], hi = gd->face[2 * a + 1];
     if ((lo == WD_FACE_PERIODIC) != (hi == WD_FACE_PERIODIC))

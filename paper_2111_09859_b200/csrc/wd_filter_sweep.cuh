@@ -73,20 +73,23 @@ __device__ __forceinline__ double filt_rhs5(const double* w, const FilterCoef& f
 
 // rows per chunk: 32 for the transposed (contiguous-line) axis, 16 otherwise
 template <bool CONTIG>
-struct SwCh { static constexpr int v = CONTIG ? 32 : 16; };
+struct SwCh { static constexpr int v = 16; };
 
 template <bool CONTIG>
-__device__ __forceinline__ void sw_load_chunk(const SweepArgs& a, double (*T)[33], int lane, int c,
+__device__ __forceinline__ void sw_load_chunk(const SweepArgs& a, double (*T)[17], int lane, int c,
                                               int nl, bool valid, long long base,
                                               long long gbase, long long rstride, double* v) {
   constexpr int CH = SwCh<CONTIG>::v;
   const int n = a.n;
   const int r0 = c * CH;
   if (CONTIG) {
-    const int r = r0 + lane;
+    // element q of this lane: line 2q + (lane >> 4), row r0 + (lane & 15)
+    const int r = r0 + (lane & 15);
 #pragma unroll
-    for (int m = 0; m < 32; ++m)
-      v[m] = (m < nl && r < n) ? __ldcs(a.in + gbase + (long long)m * a.n2 + r) : 0.0;
+    for (int q = 0; q < 16; ++q) {
+      const int m = 2 * q + (lane >> 4);
+      v[q] = (m < nl && r < n) ? __ldcs(a.in + gbase + (long long)m * a.n2 + r) : 0.0;
+    }
   } else {
 #pragma unroll
     for (int s = 0; s < CH; ++s) {
@@ -97,12 +100,12 @@ __device__ __forceinline__ void sw_load_chunk(const SweepArgs& a, double (*T)[33
 }
 
 template <bool CONTIG>
-__global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(128, 3) k_filter_sweep(SweepArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double sw_smem[];
-  double(*tile)[32][33] = reinterpret_cast<double(*)[32][33]>(sw_smem);
+  double(*tile)[32][17] = reinterpret_cast<double(*)[32][17]>(sw_smem);
   const int n = a.n;
-  double* sf0 = sw_smem + 4 * 32 * 33;  // fact | du | d | rinv | z, n each
+  double* sf0 = sw_smem + 4 * 32 * 17;  // fact | du | d | rinv | z, n each
   double* sf1 = sf0 + n;
   double* sf2 = sf1 + n;
   double* sf3 = sf2 + n;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  double(*T)[33] = tile[wib];
+  double(*T)[17] = tile[wib];
   double* scr = a.scratch + (long long)gw * n * 32;
   long long groups, lines_per_row_blk;
   long long rstride;
@@ -177,10 +180,10 @@ __global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs 
       if (CONTIG) {
         __syncwarp();
 #pragma unroll
-        for (int m = 0; m < 32; ++m) T[m][lane] = nxt[m];
+        for (int q = 0; q < 16; ++q) T[2 * q + (lane >> 4)][lane & 15] = nxt[q];
         __syncwarp();
 #pragma unroll
-        for (int s = 0; s < 32; ++s) v[s] = T[lane][s];
+        for (int s = 0; s < 16; ++s) v[s] = T[lane][s];
       } else {
 #pragma unroll
         for (int s = 0; s < CH; ++s) v[s] = nxt[s];
@@ -272,14 +275,15 @@ __global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs 
       if (CONTIG) {
         __syncwarp();
 #pragma unroll
-        for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
+        for (int s = 0; s < 16; ++s) T[lane][s] = o[s];
         __syncwarp();
-        const int r = r0 + lane;
+        const int r = r0 + (lane & 15);
 #pragma unroll
-        for (int m = 0; m < 32; ++m) {
+        for (int q = 0; q < 16; ++q) {
+          const int m = 2 * q + (lane >> 4);
           if (m < nl && r < n) {
             const long long idx = gbase + (long long)m * a.n2 + r;
-            const double xv = T[m][lane];
+            const double xv = T[m][lane & 15];
             __stcs(a.out + idx, xv);
             if (a.A) {
               if (!isfinite(xv)) bad = 1;
@@ -325,14 +329,15 @@ __global__ void __launch_bounds__(128, CONTIG ? 2 : 3) k_filter_sweep(SweepArgs 
         if (CONTIG) {
           __syncwarp();
 #pragma unroll
-          for (int s = 0; s < 32; ++s) T[lane][s] = o[s];
+          for (int s = 0; s < 16; ++s) T[lane][s] = o[s];
           __syncwarp();
-          const int r = r0 + lane;
+          const int r = r0 + (lane & 15);
 #pragma unroll
-          for (int m = 0; m < 32; ++m) {
+          for (int q = 0; q < 16; ++q) {
+            const int m = 2 * q + (lane >> 4);
             if (m < nl && r < n) {
               const long long idx = gbase + (long long)m * a.n2 + r;
-              const double xv = T[m][lane];
+              const double xv = T[m][lane & 15];
               __stcs(a.out + idx, xv);
               if (a.A) {
                 if (!isfinite(xv)) bad = 1;

@@ -8,6 +8,8 @@
 #include "wd_fused3d.cuh"
 #include "wd_filter_sweep.cuh"
 
+#include <vector>
+
 namespace wd {
 
 namespace {
@@ -20,21 +22,33 @@ int grid_blocks(long long work, int threads) {
 }
 
 template <int R, bool EIK>
-void launch_stage(int stage, const F3Args& a, int blocks, cudaStream_t s) {
+void launch_stage(int stage, const F3Args& a, int blocks, const int* tiles, bool fast,
+                  cudaStream_t s) {
   const dim3 thr(F3_TK, F3_TJ);
   const size_t sm = F3_SMEM_DOUBLES * sizeof(double);
+  const size_t smf = 2 * F3_PH * F3_PW * sizeof(double);
+  if (fast) {
+    switch (stage) {
+      case 1: k_f3_fast<R, EIK, 1><<<blocks, thr, smf, s>>>(a, tiles); break;
+      case 2: k_f3_fast<R, EIK, 2><<<blocks, thr, smf, s>>>(a, tiles); break;
+      case 3: k_f3_fast<R, EIK, 3><<<blocks, thr, smf, s>>>(a, tiles); break;
+      default: k_f3_fast<R, EIK, 4><<<blocks, thr, smf, s>>>(a, tiles); break;
+    }
+    return;
+  }
   switch (stage) {
-    case 1: k_f3_stage<R, EIK, 1><<<blocks, thr, sm, s>>>(a); break;
-    case 2: k_f3_stage<R, EIK, 2><<<blocks, thr, sm, s>>>(a); break;
-    case 3: k_f3_stage<R, EIK, 3><<<blocks, thr, sm, s>>>(a); break;
-    default: k_f3_stage<R, EIK, 4><<<blocks, thr, sm, s>>>(a); break;
+    case 1: k_f3_stage<R, EIK, 1><<<blocks, thr, sm, s>>>(a, tiles); break;
+    case 2: k_f3_stage<R, EIK, 2><<<blocks, thr, sm, s>>>(a, tiles); break;
+    case 3: k_f3_stage<R, EIK, 3><<<blocks, thr, sm, s>>>(a, tiles); break;
+    default: k_f3_stage<R, EIK, 4><<<blocks, thr, sm, s>>>(a, tiles); break;
   }
 }
 
-void stage_dispatch(int R, bool eik, int stage, const F3Args& a, int blocks, cudaStream_t s) {
-  if (R == 1) eik ? launch_stage<1, true>(stage, a, blocks, s) : launch_stage<1, false>(stage, a, blocks, s);
-  else if (R == 2) eik ? launch_stage<2, true>(stage, a, blocks, s) : launch_stage<2, false>(stage, a, blocks, s);
-  else eik ? launch_stage<3, true>(stage, a, blocks, s) : launch_stage<3, false>(stage, a, blocks, s);
+void stage_dispatch(int R, bool eik, int stage, const F3Args& a, int blocks, const int* tiles,
+                    bool fast, cudaStream_t s) {
+  if (R == 1) eik ? launch_stage<1, true>(stage, a, blocks, tiles, fast, s) : launch_stage<1, false>(stage, a, blocks, tiles, fast, s);
+  else if (R == 2) eik ? launch_stage<2, true>(stage, a, blocks, tiles, fast, s) : launch_stage<2, false>(stage, a, blocks, tiles, fast, s);
+  else eik ? launch_stage<3, true>(stage, a, blocks, tiles, fast, s) : launch_stage<3, false>(stage, a, blocks, tiles, fast, s);
 }
 }  // namespace
 
@@ -63,7 +77,7 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
       const long long gr = (L + 31) / 32;
       groups_min = gr < groups_min ? gr : groups_min;
     }
-    int ctas = 148;
+    int ctas = 296;
     if (const char* env = getenv("WD_SWEEP_CTAS")) ctas = atoi(env) > 0 ? atoi(env) : ctas;
     const size_t bytes = (size_t)ctas * 4 * nmax * 32 * sizeof(double);
     if (cudaMalloc(&fp.scratch, bytes) != cudaSuccess) {
@@ -71,7 +85,7 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
       return;
     }
     fp.sweep_ctas = ctas;
-    const int smem = (int)((4 * 32 * 33 + 5 * (size_t)nmax) * sizeof(double));
+    const int smem = (int)((4 * 32 * 17 + 5 * (size_t)nmax) * sizeof(double));
     if (cudaFuncSetAttribute(k_filter_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess ||
         cudaFuncSetAttribute(k_filter_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -83,6 +97,35 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   }
   fp.kind = PATH_F3;
   fp.active = 1;
+  fp.n_fast = fp.n_exact = 0;
+  if (sd.arith == 1) {
+    // interior tiles (every stencil inside or periodic) -> fast kernel
+    const Geom& g = in.g;
+    const int tk = (g.n[2] + F3_TK - 1) / F3_TK, tj = (g.n[1] + F3_TJ - 1) / F3_TJ;
+    std::vector<int> fastl(1, 0), exactl(1, 0);
+    for (int t = 0; t < tk * tj; ++t) {
+      const int k0 = (t % tk) * F3_TK, j0 = (t / tk) * F3_TJ;
+      const bool kf = g.per[2] ? (k0 + F3_TK <= g.n[2]) : (k0 >= F3_HP && k0 + F3_TK + F3_HP <= g.n[2]);
+      const bool jf = g.per[1] ? (j0 + F3_TJ <= g.n[1]) : (j0 >= F3_HP && j0 + F3_TJ + F3_HP <= g.n[1]);
+      (kf && jf ? fastl : exactl).push_back(t);
+    }
+    fastl[0] = (int)fastl.size() - 1;
+    exactl[0] = (int)exactl.size() - 1;
+    fp.n_fast = fastl[0];
+    fp.n_exact = exactl[0];
+    if (cudaMalloc(&fp.tiles_dev, (fastl.size() + exactl.size()) * sizeof(int)) != cudaSuccess ||
+        cudaMemcpy(fp.tiles_dev, fastl.data(), fastl.size() * sizeof(int),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(fp.tiles_dev + fastl.size(), exactl.data(), exactl.size() * sizeof(int),
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+      fp.active = 0;
+      return;
+    }
+    fp.fast_tiles = fp.tiles_dev;
+    fp.exact_tiles = fp.tiles_dev + fastl.size();
+    const size_t smf = 2 * F3_PH * F3_PW * sizeof(double);
+    (void)smf;
+  }
 }
 
 namespace {
@@ -118,7 +161,34 @@ F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
   int chunks = 1;
   while ((long long)tiles * chunks < 148LL * 8 && a.n0 / (chunks * 2) >= 32) chunks *= 2;
   a.chunk = (a.n0 + chunks - 1) / chunks;
-  *blocks = tiles * chunks;
+  *blocks = chunks;  // caller multiplies by its tile count
+  // fast-mode coefficients (host doubles)
+  const int R = sd.scheme == WD_E2 ? 1 : (sd.scheme == WD_E4 ? 2 : 3);
+  double c[4] = {0.0, 0.0, 0.0, 0.0};
+  if (R == 1) {
+    c[1] = E2_CA;
+  } else if (R == 2) {
+    c[1] = E4_CA;
+    c[2] = E4_CB;
+  } else {
+    c[1] = E6_CA;
+    c[2] = E6_CB;
+    c[3] = E6_CC;
+  }
+  for (int r = 0; r < 4; ++r) a.cr[r] = c[r];
+  double e[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int r = 1; r <= 3; ++r)
+    for (int q = 1; q <= 3; ++q) {
+      const double w = c[r] * c[q];
+      e[r + q] += w;                          // p_{+(r+q)}
+      if (r > q) e[r - q] -= w;               // -p_{r-q}
+      else if (q > r) e[q - r] -= w;          // -p_{-(r-q)} (symmetric)
+      else e[0] -= 2.0 * w;                   // r == q: -p_0 - p_0
+    }
+  for (int m = 0; m < 7; ++m) a.e[m] = e[m];
+  a.cc0 = a.c0 * a.c0;
+  a.cc1 = a.c1 * a.c1;
+  a.cc2 = a.c2 * a.c2;
   return a;
 }
 }  // namespace
@@ -132,8 +202,9 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
   double* bp = in.bufs[2];
   double* bk = in.bufs[3];
   double* tmp = in.bufs[4];
-  int blocks = 0;
-  F3Args a = f3_args(fp, A, st, &blocks);
+  int chunks = 0;
+  F3Args a = f3_args(fp, A, st, &chunks);
+  const int all_tiles = a.tiles_k * a.tiles_j;
   const int R = sd.scheme == WD_E2 ? 1 : (sd.scheme == WD_E4 ? 2 : 3);
   const bool eik = sd.kind == WD_EIKONAL;
   switch (kid) {
@@ -144,7 +215,12 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     default: break;
   }
   if (kid >= 1 && kid <= 4) {
-    stage_dispatch(R, eik, kid, a, blocks, s);
+    if (fp.fast_tiles) {
+      if (fp.n_fast) stage_dispatch(R, eik, kid, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+      if (fp.n_exact) stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+    } else {
+      stage_dispatch(R, eik, kid, a, chunks * all_tiles, nullptr, false, s);
+    }
   } else if (kid >= 5 && kid <= 7) {
     const int ax = kid - 5;
     const double* srcs[3] = {bk, tmp, bp};
@@ -175,7 +251,7 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     const long long groups = (L + 31) / 32;
     long long ctas = (groups + 3) / 4;
     if (ctas > fp.sweep_ctas) ctas = fp.sweep_ctas;
-    const size_t smem = (4 * 32 * 33 + 5 * (size_t)w.n) * sizeof(double);
+    const size_t smem = (4 * 32 * 17 + 5 * (size_t)w.n) * sizeof(double);
     if (ax == 2)
       k_filter_sweep<true><<<(int)ctas, 128, smem, s>>>(w);
     else
@@ -198,6 +274,8 @@ void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, dou
 }
 
 void fused_release(FusedPlan& fp) {
+  if (fp.tiles_dev) cudaFree(fp.tiles_dev);
+  fp.tiles_dev = nullptr;
   if (fp.scratch) cudaFree(fp.scratch);
   fp.scratch = nullptr;
   fp.active = 0;

@@ -26,6 +26,11 @@ struct FusedPlan {
   FusedInputs in;
   double* scratch = nullptr;  // filter-sweep forward values (L2-resident)
   int sweep_ctas = 0;
+  // fast arithmetic: interior tiles -> k_f3_fast, boundary tiles -> exact
+  int* tiles_dev = nullptr;
+  const int* fast_tiles = nullptr;
+  const int* exact_tiles = nullptr;
+  int n_fast = 0, n_exact = 0;
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).

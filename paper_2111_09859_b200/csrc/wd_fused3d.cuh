@@ -45,6 +45,11 @@ struct F3Args {
   int chunk;             // planes per CTA
   int tiles_k, tiles_j;
   const Status* st;
+  // fast mode: central coefficients c[r] (r = 1..3) and the composite
+  // (D o D) 13-point coefficients e[m] (m = 0..6), squared metrics
+  double cr[4];
+  double e[7];
+  double cc0, cc1, cc2;
 };
 
 template <int R>
@@ -191,14 +196,15 @@ __device__ __forceinline__ void f3_load_plane(const F3Args& a, const double* __r
 }
 
 template <int R, bool EIK, int STAGE>
-__global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
+__global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a, const int* tiles) {
   if (a.st->state != WD_STATE_RUNNING) return;
   constexpr int SCH = SchemeOf<R>::id;
   constexpr int NPW = 5 + 2 * R;
   extern __shared__ double smem[];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tile = blockIdx.x % (a.tiles_k * a.tiles_j);
-  const int chunk_id = blockIdx.x / (a.tiles_k * a.tiles_j);
+  const int ntile = tiles ? tiles[0] : a.tiles_k * a.tiles_j;
+  const int tile = tiles ? tiles[1 + blockIdx.x % ntile] : blockIdx.x % ntile;
+  const int chunk_id = blockIdx.x / ntile;
   const int k0 = (tile % a.tiles_k) * F3_TK;
   const int j0 = (tile / a.tiles_k) * F3_TJ;
   const int i0 = chunk_id * a.chunk;
@@ -398,6 +404,158 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) dw[s] = dw[s + 1];
     dw[4] = dq;
+  }
+}
+
+
+// ======================================================================
+// FAST arithmetic variant (opt-in, SolveConfig.arith = "fast"): same
+// discretisation, but the Laplacian term c_l D_l(c_l D_l p) is evaluated
+// as c_l^2 (D o D)_l p with the composite 13-point stencil and FMA
+// contraction, so no U_l staging or halo recomputation is needed.  Equal to
+// the exact path in real arithmetic; differs by round-off (tests bound the
+// drift and the converged field against the oracle).  Tiles that touch a
+// non-periodic boundary fall back to the exact kernel (wd_fused.cu).
+template <int R>
+__device__ __forceinline__ double f_d(const F3Args& a, double m3, double m2, double m1, double p1,
+                                      double p2, double p3) {
+  double d = a.cr[1] * (p1 - m1);
+  if (R >= 2) d = fma(a.cr[2], p2 - m2, d);
+  if (R >= 3) d = fma(a.cr[3], p3 - m3, d);
+  return d;
+}
+template <int R>
+__device__ __forceinline__ double f_dd(const F3Args& a, const double* w /* w[-2R..2R] centred */) {
+  double s = a.e[0] * w[0];
+#pragma unroll
+  for (int m = 1; m <= 2 * R; ++m) s = fma(a.e[m], w[m] + w[-m], s);
+  return s;
+}
+
+template <int R, bool EIK, int STAGE>
+__global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_fast(F3Args a, const int* tiles) {
+  if (a.st->state != WD_STATE_RUNNING) return;
+  constexpr int H = 2 * R;          // composite half-width
+  constexpr int NW = 2 * H + 1;     // axis-0 window p(i-H .. i+H)
+  extern __shared__ double smem[];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int ntile = tiles[0];
+  const int tile = tiles[1 + blockIdx.x % ntile];
+  const int chunk_id = blockIdx.x / ntile;
+  const int k0 = (tile % a.tiles_k) * F3_TK;
+  const int j0 = (tile / a.tiles_k) * F3_TJ;
+  const int i0 = chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.n0);
+  if (i0 >= i1) return;
+  const int k = k0 + tx, j = j0 + ty;  // interior tiles: always inside
+  const int n0 = a.n0;
+  const long long s0 = a.s0;
+  const long long col = (long long)j * a.n2 + k;
+  const F3Offs offs = f3_offsets(a, j0, k0, tx, ty, true);
+  double pw[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    const int pos = i0 - H + s;
+    double v = 0.0;
+    if (a.per0) v = a.p[(long long)wrapm(pos, n0) * s0 + col];
+    else if (pos >= 0 && pos < n0) v = a.p[(long long)pos * s0 + col];
+    pw[s] = v;
+  }
+  int inext = a.per0 ? wrapm(i0 + H + 1, n0) : i0 + H + 1;
+  const double* pp0 = a.p + (long long)i0 * s0;
+  double nA = __ldcs(a.A + (long long)i0 * s0 + col);
+  double ndt = STAGE > 1 ? __ldcs(a.dt + (long long)i0 * s0 + col) : 0.0;
+  double nacc = STAGE > 1 ? __ldcs(a.acc + (long long)i0 * s0 + col) : 0.0;
+  double njh = offs.jh >= 0 ? pp0[offs.jh] : 0.0;
+  double nkh = offs.kh >= 0 ? pp0[offs.kh] : 0.0;
+  double npn = (a.per0 || inext < n0) ? a.p[(long long)inext * s0 + col] : 0.0;
+  for (int i = i0; i < i1; ++i) {
+    double* Pb = smem + ((i - i0) & 1) * (F3_PH * F3_PW);
+    const long long plane = (long long)i * s0;
+    Pb[(ty + F3_HP) * F3_PW + tx + F3_HP] = pw[H];
+    if (ty < 2 * F3_HP) Pb[(ty < F3_HP ? ty : ty + F3_TJ) * F3_PW + tx + F3_HP] = njh;
+    if (tx < 2 * F3_HP) Pb[(ty + F3_HP) * F3_PW + (tx < F3_HP ? tx : tx + F3_TK)] = nkh;
+    const double Av = nA, dtin = ndt, accv = nacc, pnext = npn;
+    inext = inext + 1;
+    if (a.per0 && inext == n0) inext = 0;
+    if (i + 1 < i1) {
+      const double* pp = a.p + plane + s0;
+      nA = __ldcs(a.A + plane + s0 + col);
+      if (STAGE > 1) ndt = __ldcs(a.dt + plane + s0 + col);
+      if (STAGE > 1) nacc = __ldcs(a.acc + plane + s0 + col);
+      njh = offs.jh >= 0 ? pp[offs.jh] : 0.0;
+      nkh = offs.kh >= 0 ? pp[offs.kh] : 0.0;
+      npn = (a.per0 || inext < n0) ? a.p[(long long)inext * s0 + col] : 0.0;
+    }
+    __syncthreads();
+    const double* row = Pb + (ty + F3_HP) * F3_PW + tx + F3_HP;  // row[0] = own
+    const double* cl = row;                                       // column: cl[r*PW]
+    double wk[2 * H + 1], wj[2 * H + 1];
+#pragma unroll
+    for (int m = -H; m <= H; ++m) {
+      wk[m + H] = row[m];
+      wj[m + H] = cl[m * F3_PW];
+    }
+    const double d2 = f_d<R>(a, wk[H - 3 < 0 ? 0 : H - 3], wk[H - 2 < 0 ? 0 : H - 2], wk[H - 1],
+                             wk[H + 1], wk[H + 2 > 2 * H ? 2 * H : H + 2],
+                             wk[H + 3 > 2 * H ? 2 * H : H + 3]);
+    const double d1 = f_d<R>(a, wj[H - 3 < 0 ? 0 : H - 3], wj[H - 2 < 0 ? 0 : H - 2], wj[H - 1],
+                             wj[H + 1], wj[H + 2 > 2 * H ? 2 * H : H + 2],
+                             wj[H + 3 > 2 * H ? 2 * H : H + 3]);
+    const double dd2 = f_dd<R>(a, wk + H);
+    const double dd1 = f_dd<R>(a, wj + H);
+    double d0, dd0;
+    if (a.per0 || (i >= H && i <= n0 - 1 - H)) {
+      d0 = f_d<R>(a, pw[H - 3 < 0 ? 0 : H - 3], pw[H - 2 < 0 ? 0 : H - 2], pw[H - 1], pw[H + 1],
+                  pw[H + 2 > 2 * H ? 2 * H : H + 2], pw[H + 3 > 2 * H ? 2 * H : H + 3]);
+      dd0 = f_dd<R>(a, pw + H);
+    } else {  // non-periodic axis-0 boundary planes: closures via U_0 (exact order)
+      constexpr int SCH = SchemeOf<R>::id;
+      Line gl{a.p + col, s0, n0, 0, 0.0};
+      d0 = deriv_explicit_at(gl, i, n0, SCH, 0);
+      double u[9];
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+        const int q = i - 4 + s;
+        u[s] = (q >= 0 && q < n0) ? a.c0 * deriv_explicit_at(gl, q, n0, SCH, 0) : 0.0;
+      }
+      // D_0(U_0) at i then divide out c0: keep the c0 * D0(U0) product form
+      const double D0 = d0_from_window<R>(u, i, n0, 0);
+      dd0 = D0 / a.c0;  // lap term below multiplies by c0^2 -> c0 * D0
+    }
+    const double pv = pw[H];
+    const double h0 = a.cc0 * d0, h1 = a.cc1 * d1, h2 = a.cc2 * d2;
+    double adv = h0 * d0;
+    adv = fma(h1, d1, adv);
+    adv = fma(h2, d2, adv);
+    double kv;
+    if (EIK) {
+      kv = 1.0 - adv;
+    } else {
+      double lap = a.cc0 * dd0;
+      lap = fma(a.cc1, dd1, lap);
+      lap = fma(a.cc2, dd2, lap);
+      kv = fma(a.eps * pv, lap, 1.0) - adv;
+    }
+    const bool pinned = (i == 0 && a.wall[0]) || (i == n0 - 1 && a.wall[1]);
+    const long long idx = plane + col;
+    if (STAGE == 1) {
+      double den = fabs(h0) + fabs(h1) + fabs(h2);
+      if (!EIK) den = fma(2.0 * (a.eps * pv), a.sumS, den);
+      const double dtv = fmin(a.cfl / (den + 1e-30), a.cflms);
+      __stcs(a.dt + idx, dtv);
+      __stcs(a.acc + idx, kv);
+      a.out[idx] = pinned ? 0.0 : fma(0.5 * dtv, kv, Av);
+    } else if (STAGE == 2 || STAGE == 3) {
+      __stcs(a.acc + idx, fma(2.0, kv, accv));
+      const double cdt = STAGE == 3 ? dtin : 0.5 * dtin;
+      a.out[idx] = pinned ? 0.0 : fma(cdt, kv, Av);
+    } else {
+      a.out[idx] = pinned ? 0.0 : fma(dtin / 6.0, accv + kv, Av);
+    }
+#pragma unroll
+    for (int s = 0; s < NW - 1; ++s) pw[s] = pw[s + 1];
+    pw[NW - 1] = pnext;
   }
 }
 

@@ -85,12 +85,18 @@ class SolveConfig:
     tol: float = 1e-5
     max_iters: int = 50000
     l2_every: int = 0
+    # EXTENSION: "exact" (default) reproduces the reference bit for bit;
+    # "fast" lets the fused 3-D kernels use FMA and the composite Laplacian
+    # stencil (round-off-level differences).
+    arith: str = "exact"
 
     def __post_init__(self):
         if self.cfl <= 0.0:
             raise ValueError("cfl must be positive")
         if self.tol <= 0.0:
             raise ValueError("tol must be positive")
+        if self.arith not in ("exact", "fast"):
+            raise ValueError("arith must be 'exact' or 'fast'")
 
     def uses_filter(self) -> bool:
         return self.filter_config is not None and self.scheme != "UW"
@@ -209,7 +215,7 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
     fc = config.formulation
     ctx = NativeSolver(grid, boundary.faces, boundary.solid_mask, config.scheme, fc,
                        config.filter_config if config.uses_filter() else None, config.cfl,
-                       config.tol, config.max_iters)
+                       config.tol, config.max_iters, arith=config.arith)
     try:
         lib = ctx.lib
         if phi0 is None:

@@ -85,3 +85,25 @@ def test_fused_matches_generic(monkeypatch):
     b = W.solve_steady(pg, W.BoundarySpec(faces), cfg)
     assert same(a.residual_history, b.residual_history)
     assert same(a.phi, b.phi)
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "fast-" + "x".join(map(str, c[0])) + f"-{c[4]}")
+def test_fast_mode_close_to_oracle(case):
+    """arith='fast' (FMA + composite Laplacian) stays within round-off of
+    the exact oracle over the same steps."""
+    dims, per, kinds, kind, scheme, af, iters = case
+    faces = _faces(per, kinds)
+    og = wd.cartesian(*dims, Lx=0.9, Ly=1.0, Lz=1.1, periodic=per)
+    pg = W.build_cartesian(*dims, Lx=0.9, Ly=1.0, Lz=1.1, periodic=per)
+    rng = np.random.default_rng(sum(dims))
+    phi0 = 1e-3 * rng.random(dims)
+    bnd_o = wd.Boundary({k: v for k, v in faces.items() if v != "periodic"})
+    ro = wd.solve(og, bnd_o, wd.Config(wd.Formulation(kind), scheme, af, 0.5, 1e-15, iters),
+                  phi0=phi0, raise_on_divergence=False)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme=scheme,
+                        filter_config=None if af is None else W.FilterConfig(af), tol=1e-15,
+                        max_iters=iters, arith="fast")
+    rp = W.solve_steady(pg, W.BoundarySpec(faces), cfg, phi0=phi0)
+    assert rp.iters == ro.iters
+    np.testing.assert_allclose(rp.residual_history, ro.residual_history, rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(rp.phi, ro.phi, rtol=0, atol=1e-12 * max(1.0, np.abs(ro.phi).max()))
