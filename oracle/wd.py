@@ -196,8 +196,11 @@ def solve_tridiagonal(lower, diag, upper, rhs):
 # by Sherman-Morrison: A = B + u v^T with gamma = -1,
 #   B = A without corners, B00 = 1 - gamma, B_{n-1,n-1} = 1 - alpha^2/gamma
 #   u = (gamma, 0.., 0, alpha), v = (1, 0.., 0, alpha/gamma)
-#   x = y - ((y0 + vn y_{n-1}) / denom) z,  B y = r, B z = u,
+#   x = y - f z,  B y = r, B z = u,  f = (v . y) / denom,
 #   denom = 1 + (z0 + vn z_{n-1}).
+# B is symmetric, so v . y = v . B^-1 r = h . r with h = B^-1 v: f is
+# accumulated from the right-hand side, h_0 r_0 + h_1 r_1 + ... in row order,
+# which lets a single back substitution apply the correction.
 
 
 @dataclass
@@ -206,6 +209,7 @@ class CyclicFactor:
     alpha: float
     base: GtsvFactor
     z: np.ndarray
+    h: np.ndarray
     vn: float
     denom: float
 
@@ -225,17 +229,24 @@ def cyclic_factor(alpha: float, n: int) -> CyclicFactor:
     u[-1] = alpha
     z = gtsv_apply(base, u)
     vn = alpha / gamma
+    v = np.zeros(n)
+    v[0] = 1.0
+    v[-1] = vn
+    h = gtsv_apply(base, v)
     denom = 1.0 + (z[0] + vn * z[n - 1])
     if denom == 0.0:
         raise ZeroPivotError("singular cyclic system")
-    return CyclicFactor(n, alpha, base, z, vn, denom)
+    return CyclicFactor(n, alpha, base, z, h, vn, denom)
 
 
 def cyclic_apply(cf: CyclicFactor, b):
-    y = gtsv_apply(cf.base, b)
-    s = y[..., 0] + cf.vn * y[..., cf.n - 1]
+    b = np.asarray(b, dtype=float)
+    s = 0.0
+    for i in range(cf.n):
+        s = s + cf.h[i] * b[..., i]
     f = s / cf.denom
-    return y - f[..., None] * cf.z
+    y = gtsv_apply(cf.base, b)
+    return y - np.asarray(f)[..., None] * cf.z
 
 
 # --------------------------------------------------------------------------

@@ -63,7 +63,7 @@ const char* scheme_name(int s) {
 struct HostFactor {
   int n = 0;
   int cyclic = 0;
-  std::vector<double> fact, d, du, du2, swap, z;
+  std::vector<double> fact, d, du, du2, swap, z, h;
   double vn = 0.0, denom = 1.0;
 };
 
@@ -149,6 +149,11 @@ int cyclic_factor(double alpha, int n, HostFactor& F) {
   gtsv_apply_host(F, u);
   F.z = u;
   F.vn = alpha / gamma;
+  std::vector<double> v(n, 0.0);
+  v[0] = 1.0;
+  v[n - 1] = F.vn;
+  gtsv_apply_host(F, v);
+  F.h = v;
   F.denom = 1.0 + (u[0] + F.vn * u[n - 1]);
   if (F.denom == 0.0) return fail(WD_ERR_ZERO_PIVOT, "singular cyclic system");
   F.cyclic = 1;
@@ -212,7 +217,7 @@ FilterCoef filter_coefs(double af) {
 }
 
 // Device image of a HostFactor: 7 arrays of n doubles.
-size_t factor_doubles(int n) { return (size_t)7 * std::max(n, 1); }
+size_t factor_doubles(int n) { return (size_t)8 * std::max(n, 1); }
 
 TriDev factor_view(const HostFactor& F, double* dev) {
   const size_t n = std::max(F.n, 1);
@@ -226,6 +231,7 @@ TriDev factor_view(const HostFactor& F, double* dev) {
   T.swap = dev + 4 * n;
   T.z = dev + 5 * n;
   T.rinv = dev + 6 * n;
+  T.h = dev + 7 * n;
   T.vn = F.vn;
   T.denom = F.denom;
   return T;
@@ -246,6 +252,7 @@ void factor_pack(const HostFactor& F, std::vector<double>& out) {
   std::vector<double> rinv(n, 0.0);
   for (size_t i = 0; i < (size_t)F.n && i < F.d.size(); ++i) rinv[i] = 1.0 / F.d[i];
   put(6, rinv);
+  put(7, F.h);
 }
 
 Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) {

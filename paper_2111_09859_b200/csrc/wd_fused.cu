@@ -68,32 +68,13 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   if (sd.use_filter) {
     for (int a = 0; a < 3; ++a)
       if (in.filt_swaps[a]) return;
-    // one scratch slab of n * 32 doubles per resident warp
     int nmax = 0;
-    long long groups_min = 1LL << 62;
-    for (int a = 0; a < 3; ++a) {
-      nmax = in.g.n[a] > nmax ? in.g.n[a] : nmax;
-      const long long L = in.g.N / in.g.n[a];
-      const long long gr = (L + 31) / 32;
-      groups_min = gr < groups_min ? gr : groups_min;
-    }
-    int ctas = 296;
-    if (const char* env = getenv("WD_SWEEP_CTAS")) ctas = atoi(env) > 0 ? atoi(env) : ctas;
-    const size_t bytes = (size_t)ctas * 4 * nmax * 32 * sizeof(double);
-    if (cudaMalloc(&fp.scratch, bytes) != cudaSuccess) {
-      fp.scratch = nullptr;
+    for (int a = 0; a < 3; ++a) nmax = in.g.n[a] > nmax ? in.g.n[a] : nmax;
+    const int smem = (int)((6 * (size_t)nmax + (size_t)((nmax + FB - 1) / FB) * 128) *
+                           sizeof(double));
+    if (cudaFuncSetAttribute(k_filter_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
       return;
-    }
-    fp.sweep_ctas = ctas;
-    const int smem = (int)((4 * 32 * 17 + 5 * (size_t)nmax) * sizeof(double));
-    if (cudaFuncSetAttribute(k_filter_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_filter_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess) {
-      cudaFree(fp.scratch);
-      fp.scratch = nullptr;
-      return;
-    }
   }
   fp.kind = PATH_F3;
   fp.active = 1;
@@ -228,7 +209,6 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     SweepArgs w;
     w.in = srcs[ax];
     w.out = dsts[ax];
-    w.scratch = fp.scratch;
     w.n = g.n[ax];
     w.axis = ax;
     w.n0 = g.n[0];
@@ -242,20 +222,16 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     w.d = T.d;
     w.rinv = T.rinv;
     w.z = T.z;
-    w.vn = T.vn;
+    w.h = T.h;
     w.denom = T.denom;
     w.fc = in.fcoef;
     w.A = ax == 2 ? A : nullptr;
     w.st = st;
     const long long L = g.N / g.n[ax];
-    const long long groups = (L + 31) / 32;
-    long long ctas = (groups + 3) / 4;
-    if (ctas > fp.sweep_ctas) ctas = fp.sweep_ctas;
-    const size_t smem = (4 * 32 * 17 + 5 * (size_t)w.n) * sizeof(double);
-    if (ax == 2)
-      k_filter_sweep<true><<<(int)ctas, 128, smem, s>>>(w);
-    else
-      k_filter_sweep<false><<<(int)ctas, 128, smem, s>>>(w);
+    long long ctas = (L + 127) / 128;
+    if (ctas > 148LL * 8) ctas = 148LL * 8;
+    const size_t smem = (6 * (size_t)w.n + (size_t)((w.n + FB - 1) / FB) * 128) * sizeof(double);
+    k_filter_sweep<<<(int)ctas, 128, smem, s>>>(w);
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }
@@ -276,8 +252,6 @@ void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, dou
 void fused_release(FusedPlan& fp) {
   if (fp.tiles_dev) cudaFree(fp.tiles_dev);
   fp.tiles_dev = nullptr;
-  if (fp.scratch) cudaFree(fp.scratch);
-  fp.scratch = nullptr;
   fp.active = 0;
 }
 

@@ -24,8 +24,6 @@ struct FusedPlan {
   int active = 0;
   int kind = 0;          // which specialised path
   FusedInputs in;
-  double* scratch = nullptr;  // filter-sweep forward values (L2-resident)
-  int sweep_ctas = 0;
   // fast arithmetic: interior tiles -> k_f3_fast, boundary tiles -> exact
   int* tiles_dev = nullptr;
   const int* fast_tiles = nullptr;

@@ -23,6 +23,7 @@ struct TriDev {
   const double* swap;  // 0.0 / 1.0
   const double* z;     // cyclic correction vector
   const double* rinv;  // RN(1/d) per row (fused sweeps)
+  const double* h;     // cyclic: B^-1 v, f = (h . rhs) / denom
   double vn, denom;
 };
 
@@ -61,6 +62,9 @@ __device__ __forceinline__ void tri_solve_line(double* __restrict__ x, long long
     x[0] = x[0] / T.d[0];
     return;
   }
+  double hs = 0.0;  // cyclic: h . rhs in row order (oracle/wd.py:cyclic_apply)
+  if (T.cyclic)
+    for (int i = 0; i < n; ++i) hs = hs + T.h[i] * x[(long long)i * st];
   for (int i = 0; i < n - 1; ++i) {
     const double f = T.fact[i];
     double* xi = x + (long long)i * st;
@@ -82,8 +86,7 @@ __device__ __forceinline__ void tri_solve_line(double* __restrict__ x, long long
     *xi = ((*xi - T.du[i] * xi[st]) - T.du2[i] * xi[2 * st]) / T.d[i];
   }
   if (T.cyclic) {
-    const double s = x[0] + T.vn * x[(long long)(n - 1) * st];
-    const double f = s / T.denom;
+    const double f = hs / T.denom;
     for (int i = 0; i < n; ++i) {
       double* xi = x + (long long)i * st;
       *xi = *xi - f * T.z[i];
