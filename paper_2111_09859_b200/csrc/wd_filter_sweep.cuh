@@ -196,8 +196,14 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
     for (int b = nb - 1; b >= 0; --b) {
       const int r0 = b * FB;
       double u[FB + 10];
+      if (r0 >= 5 && r0 + FB + 5 <= n) {  // interior block: plain loads
+        const double* p = src + (long long)(r0 - 5) * rstride;
 #pragma unroll
-      for (int q = 0; q < FB + 10; ++q) u[q] = ld(r0 - 5 + q);
+        for (int q = 0; q < FB + 10; ++q) u[q] = p[(long long)q * rstride];
+      } else {
+#pragma unroll
+        for (int q = 0; q < FB + 10; ++q) u[q] = ld(r0 - 5 + q);
+      }
       double av[FB];
       if (a.A) {
 #pragma unroll
