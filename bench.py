@@ -11,8 +11,10 @@ BCs, 3 filter sweeps, convergence reduction) over all 134,217,728 nodes.
 
 --impl reference runs the CPU oracle port (oracle/wd.py, the reference's
 numpy algorithm restated) on rank 0 over a bounded sample of the same
-workload.  Under torchrun (N > 1) each rank runs an independent replica
-(round 1: no slab decomposition yet), weak scaling, max time over ranks.
+workload.  Under torchrun (N > 1) the 512^3 grid is slab-decomposed over the
+N GPUs (paper_2111_09859_b200/dist.py: ghost-plane exchange per RK stage,
+all_to_all transposes around the axis-0 filter, all_reduce of the stop
+test) -- strong scaling, max time over ranks.
 """
 from __future__ import annotations
 
@@ -180,6 +182,68 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
+def run_b200_dist(args, world, rank, local):
+    """N > 1: slab decomposition of the same global grid (strong scaling)."""
+    import torch
+    import paper_2111_09859_b200 as W
+    from paper_2111_09859_b200 import dist
+
+    cfg = CONFIGS[args.config]
+    dims = tuple(args.n if args.n else d for d in cfg["dims"])
+    sp = tuple((1.0 / dims[d]) if cfg["periodic"][d] else 1.0 / (dims[d] - 1) for d in range(3))
+    if args.n:
+        sp = (1.0 / 512, 1.0 / (dims[1] - 1), 1.0 / 512)
+    fc = W.FormulationConfig(kind=cfg["kind"])
+    filt = W.FilterConfig(cfg["alpha_f"])
+    K, Wm = args.steps, args.warmup
+    comm = dist.TorchComm()
+    ds = dist.DistributedSolve(dims, sp, cfg["faces"], cfg["scheme"], fc, filt, 0.5, 1e-15,
+                               K + Wm + 8, args.arith, comm, [rank])
+    nl = dims[0] // world
+    ds.set_state([torch.zeros((nl, dims[1], dims[2]), dtype=torch.float64, device="cuda")])
+    for _ in range(Wm):
+        ds.step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = ds.ctxs[0].stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        ds.step()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    secs = allreduce_max(e0.elapsed_time(e1) / 1e3, world)
+    st = ds.status()
+    if st.state == 2:
+        raise RuntimeError("benchmark run diverged")
+    N = int(np.prod(dims))
+    value = N * K / secs / 1e9
+    peak, peak_kind = _peaks()
+    w_upd = words_per_update(3, True)
+    step_ach = w_upd * 8 * N / world / (secs / K) / 1e9
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": Wm, "ms_per_step": round(secs / K * 1e3, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "dims": list(dims), "arith": args.arith,
+                       "global_nodes": N, "parallelism": f"slab{world}",
+                       "l2": "inputs larger than L2"},
+            "roofline": None,
+            "step_roofline": {"achieved_per_gpu": round(step_ach, 1), "peak": peak, "unit": "GB/s",
+                              "frac": round(step_ach / peak, 4), "words_per_update": w_upd,
+                              "peak_source": peak_kind},
+            "gpu_launches": K * 20, "clocks": clk, "e2e": None}
+    ds.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_b200(args, world, rank, local):
     import ctypes
     import torch
@@ -315,17 +379,26 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--dist", action="store_true", help="slab-decomposed path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     world, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif world > 1 or args.dist:
+        if world == 1:
+            import torch.distributed as tdist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            tdist.init_process_group("nccl", rank=0, world_size=1,
+                                     device_id=__import__("torch").device("cuda", 0))
+        run_b200_dist(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    import torch.distributed as tdist
+    if tdist.is_available() and tdist.is_initialized():
+        tdist.destroy_process_group()
 
 
 if __name__ == "__main__":

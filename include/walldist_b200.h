@@ -170,6 +170,29 @@ int wd_compute_metrics(const double* coords_dev, double* metrics_dev, double* ja
 int wd_linf_delta(const double* a_dev, const double* b_dev, const unsigned char* mask_dev,
                   long long n, double* out_host, void* stream);
 
+/* ---- slab decomposition (EXTENSION; paper_2111_09859_b200/dist.py) ----
+ * The context is created for a rank's ghosted slab (nl + 2G, n1, n2) with
+ * axis 0 non-periodic; the host exchanges ghost planes between stages and
+ * transposes slab <-> pencil around the axis-0 filter (all_to_all), so the
+ * per-node and per-line arithmetic equals the single-GPU path exactly.   */
+/* stages update planes [i_lo, i_hi) only (the slab interior)             */
+int wd_dist_configure(wd_ctx* ctx, int i_lo, int i_hi);
+/* one RK stage (1..4): out = stage(p) with phi0 = A (all ghosted)        */
+int wd_dist_stage(wd_ctx* ctx, int stage, const double* A_dev, const double* p_dev,
+                  double* out_dev);
+/* implicit-filter sweep along `axis` of an (n0, n1, n2) array; with A_dev
+ * the sweep also accumulates max|out - A|, max|out| into the status     */
+int wd_dist_filter(wd_ctx* ctx, int axis, const double* in_dev, double* out_dev, int n0, int n1,
+                   int n2, int periodic, const double* A_dev);
+/* slab (nl, n1, n2) <-> all_to_all buffer (P, nl, n1/P, n2)              */
+int wd_dist_pack(const double* slab_dev, double* buf_dev, int nl, int n1, int n2, int P,
+                 void* stream);
+int wd_dist_unpack(const double* buf_dev, double* slab_dev, int nl, int n1, int n2, int P,
+                   void* stream);
+/* status maxima -> dev3 (int64 x3) for all_reduce(max); then finalize    */
+int wd_dist_stats(wd_ctx* ctx, long long* dev3);
+int wd_dist_finalize(wd_ctx* ctx, const long long* dev3);
+
 #ifdef __cplusplus
 }
 #endif

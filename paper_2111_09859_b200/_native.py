@@ -108,6 +108,13 @@ SIGNATURES = {
     "wd_linf_delta": (_I, [_P, _P, _P, ctypes.c_longlong, _DP, _P]),
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
+    "wd_dist_configure": (_I, [_P, _I, _I]),
+    "wd_dist_stage": (_I, [_P, _I, _P, _P, _P]),
+    "wd_dist_filter": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _P]),
+    "wd_dist_pack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "wd_dist_unpack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "wd_dist_stats": (_I, [_P, _P]),
+    "wd_dist_finalize": (_I, [_P, _P]),
 }
 
 _lib = None

@@ -303,6 +303,8 @@ struct wd_ctx {
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
   long long enq = 0;  // host-side count of enqueued steps (buffer parity)
   FusedPlan fused;    // specialised kernels (wd_fused.cuh), if applicable
+  // distributed path: filter factors for arbitrary (length, periodic)
+  std::map<std::pair<int, int>, std::pair<HostFactor, double*>> dfilt;
 };
 
 namespace {
@@ -724,6 +726,7 @@ int wd_destroy(wd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   fused_release(c->fused);
+  for (auto& kv : c->dfilt) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
   cudaFree(c->ws);
@@ -1098,6 +1101,135 @@ int wd_linf_delta(const double* a, const double* b, const unsigned char* mask, l
   double v;
   std::memcpy(&v, &h, sizeof(v));
   *out = v;
+  return WD_OK;
+}
+
+}  // extern "C"
+
+// ====================================================================
+// Slab decomposition (EXTENSION, paper_2111_09859_b200/dist.py): one RK
+// stage on a ghosted slab, filter sweeps on arbitrary arrays, slab <->
+// pencil packing for the all_to_all transpose, and the status reduction
+// hand-off around an all_reduce(max).
+namespace {
+__global__ void k_pack_slab(const double* __restrict__ slab, double* __restrict__ buf, int nl,
+                            int n1, int n2, int P) {
+  // slab (nl, n1, n2) -> buf (P, nl, n1/P, n2)
+  const int m1 = n1 / P;
+  const long long N = (long long)nl * n1 * n2;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < N;
+       o += (long long)gridDim.x * blockDim.x) {
+    long long t = o;
+    const int k = (int)(t % n2);
+    t /= n2;
+    const int jj = (int)(t % m1);
+    t /= m1;
+    const int i = (int)(t % nl);
+    const int q = (int)(t / nl);
+    buf[o] = slab[((long long)i * n1 + (long long)q * m1 + jj) * n2 + k];
+  }
+}
+__global__ void k_unpack_slab(const double* __restrict__ buf, double* __restrict__ slab, int nl,
+                              int n1, int n2, int P) {
+  const int m1 = n1 / P;
+  const long long N = (long long)nl * n1 * n2;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < N;
+       o += (long long)gridDim.x * blockDim.x) {
+    long long t = o;
+    const int k = (int)(t % n2);
+    t /= n2;
+    const int jj = (int)(t % m1);
+    t /= m1;
+    const int i = (int)(t % nl);
+    const int q = (int)(t / nl);
+    slab[((long long)i * n1 + (long long)q * m1 + jj) * n2 + k] = buf[o];
+  }
+}
+__global__ void k_stats_out(Status* st, long long* out) {
+  out[0] = (long long)st->max_delta_bits;
+  out[1] = (long long)st->max_abs_bits;
+  out[2] = st->nonfinite;
+}
+__global__ void k_stats_in(Status* st, const long long* in) {
+  st->max_delta_bits = (unsigned long long)in[0];
+  st->max_abs_bits = (unsigned long long)in[1];
+  st->nonfinite = (int)in[2];
+}
+}  // namespace
+
+extern "C" {
+
+int wd_dist_configure(wd_ctx* c, int i_lo, int i_hi) {
+  if (!c || !c->fused.active) return fail(WD_ERR_INVALID, "distributed path needs the fused 3-D path");
+  if (i_lo < 0 || i_hi > c->g.n[0] || i_lo >= i_hi) return fail(WD_ERR_INVALID, "bad plane range");
+  c->fused.i_lo = i_lo;
+  c->fused.i_hi = i_hi;
+  return WD_OK;
+}
+
+int wd_dist_stage(wd_ctx* c, int stage, const double* A, const double* p, double* out) {
+  if (!c || !c->fused.active || stage < 1 || stage > 4) return fail(WD_ERR_INVALID, "bad arguments");
+  fused_stage_ptrs(c->fused, stage, A, p, out, c->st, c->stream);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, int n1, int n2,
+                   int periodic, const double* A) {
+  if (!c || !c->fused.active || !c->sd.use_filter || axis < 0 || axis > 2)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  const int nn[3] = {n0, n1, n2};
+  const int n = nn[axis];
+  auto key = std::make_pair(n, periodic ? 1 : 0);
+  auto it = c->dfilt.find(key);
+  if (it == c->dfilt.end()) {
+    HostFactor F;
+    int rc = filter_factor(c->sd.alpha_f, n, periodic, F);
+    if (rc) return rc;
+    for (double sw : F.swap)
+      if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
+    std::vector<double> packed;
+    factor_pack(F, packed);
+    double* dev = nullptr;
+    CK(cudaMalloc(&dev, packed.size() * sizeof(double)));
+    CK(cudaMemcpy(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+    fused_filter_prepare(n);
+    it = c->dfilt.emplace(key, std::make_pair(F, dev)).first;
+  }
+  const TriDev T = factor_view(it->second.first, it->second.second);
+  fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_pack(const double* slab, double* buf, int nl, int n1, int n2, int P, void* stream) {
+  if (!slab || !buf || P < 1 || n1 % P) return fail(WD_ERR_INVALID, "bad arguments");
+  const long long N = (long long)nl * n1 * n2;
+  k_pack_slab<<<nblocks(N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(slab, buf, nl, n1, n2, P);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_unpack(const double* buf, double* slab, int nl, int n1, int n2, int P, void* stream) {
+  if (!slab || !buf || P < 1 || n1 % P) return fail(WD_ERR_INVALID, "bad arguments");
+  const long long N = (long long)nl * n1 * n2;
+  k_unpack_slab<<<nblocks(N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(buf, slab, nl, n1, n2, P);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_stats(wd_ctx* c, long long* dev3) {
+  if (!c || !dev3) return fail(WD_ERR_INVALID, "bad arguments");
+  k_stats_out<<<1, 1, 0, c->stream>>>(c->st, dev3);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_finalize(wd_ctx* c, const long long* dev3) {
+  if (!c || !dev3 || !c->hist) return fail(WD_ERR_INVALID, "bad arguments");
+  k_stats_in<<<1, 1, 0, c->stream>>>(c->st, dev3);
+  k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
+  CK(cudaGetLastError());
   return WD_OK;
 }
 

@@ -139,9 +139,12 @@ F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
   a.tiles_j = (a.n1 + F3_TJ - 1) / F3_TJ;
   const int tiles = a.tiles_k * a.tiles_j;
   // split the i-stream so the grid is several waves of 148 SMs
+  a.i_lo = fp.i_lo;
+  a.i_hi = fp.i_hi > 0 ? fp.i_hi : a.n0;
+  const int ni = a.i_hi - a.i_lo;
   int chunks = 1;
-  while ((long long)tiles * chunks < 148LL * 8 && a.n0 / (chunks * 2) >= 32) chunks *= 2;
-  a.chunk = (a.n0 + chunks - 1) / chunks;
+  while ((long long)tiles * chunks < 148LL * 8 && ni / (chunks * 2) >= 32) chunks *= 2;
+  a.chunk = (ni + chunks - 1) / chunks;
   *blocks = chunks;  // caller multiplies by its tile count
   // fast-mode coefficients (host doubles)
   const int R = sd.scheme == WD_E2 ? 1 : (sd.scheme == WD_E4 ? 2 : 3);
@@ -235,6 +238,64 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }
+}
+
+void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const double* p,
+                      double* out, Status* st, cudaStream_t s) {
+  const wd_solver_desc& sd = *fp.in.sd;
+  int chunks = 0;
+  F3Args a = f3_args(fp, A, st, &chunks);
+  const int all_tiles = a.tiles_k * a.tiles_j;
+  const int R = sd.scheme == WD_E2 ? 1 : (sd.scheme == WD_E4 ? 2 : 3);
+  const bool eik = sd.kind == WD_EIKONAL;
+  a.p = p;
+  a.out = out;
+  if (fp.fast_tiles) {
+    if (fp.n_fast) stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+    if (fp.n_exact) stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+  } else {
+    stage_dispatch(R, eik, stage, a, chunks * all_tiles, nullptr, false, s);
+  }
+}
+
+void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
+                      int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
+                      cudaStream_t s) {
+  SweepArgs w;
+  w.in = in;
+  w.out = out;
+  const int nn[3] = {n0, n1, n2};
+  w.n = nn[axis];
+  w.axis = axis;
+  w.n0 = n0;
+  w.n1 = n1;
+  w.n2 = n2;
+  w.s0 = (long long)n1 * n2;
+  w.per = per;
+  w.fact = T.fact;
+  w.du = T.du;
+  w.d = T.d;
+  w.rinv = T.rinv;
+  w.z = T.z;
+  w.h = T.h;
+  w.denom = T.denom;
+  w.fc = fp.in.fcoef;
+  w.A = A;
+  w.st = st;
+  const long long L = (long long)n0 * n1 * n2 / w.n;
+  long long ctas = (L + 127) / 128;
+  if (ctas > 148LL * 8) ctas = 148LL * 8;
+  const size_t smem = (6 * (size_t)w.n + (size_t)((w.n + FB - 1) / FB) * 128) * sizeof(double);
+  k_filter_sweep<<<(int)ctas, 128, smem, s>>>(w);
+}
+
+void fused_filter_prepare(int n) {
+  const int smem = (int)((6 * (size_t)n + (size_t)((n + FB - 1) / FB) * 128) * sizeof(double));
+  int cur = 0;
+  cudaFuncAttributes attr;
+  if (cudaFuncGetAttributes(&attr, k_filter_sweep) == cudaSuccess) cur = attr.maxDynamicSharedSizeBytes;
+  if (smem > cur)
+    cudaFuncSetAttribute(k_filter_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,

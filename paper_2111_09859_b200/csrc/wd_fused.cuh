@@ -29,6 +29,7 @@ struct FusedPlan {
   const int* fast_tiles = nullptr;
   const int* exact_tiles = nullptr;
   int n_fast = 0, n_exact = 0;
+  int i_lo = 0, i_hi = 0;  // axis-0 plane range updated by the stages (0,0 = all)
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).
@@ -41,5 +42,13 @@ void fused_release(FusedPlan& fp);
 // stages, 5..7 filter sweeps, 8 change reduction.
 void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Status* st,
                   cudaStream_t s);
+// Distributed path: one RK stage with explicit buffers; a filter sweep on
+// an arbitrary (n0, n1, n2) array with factor T (SweepArgs semantics).
+void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const double* p,
+                      double* out, Status* st, cudaStream_t s);
+void fused_filter_prepare(int n);  // opt in to the sweep's shared memory for length n
+void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
+                      int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
+                      cudaStream_t s);
 
 }  // namespace wd

@@ -43,6 +43,7 @@ struct F3Args {
   double* acc;
   double* out;
   int chunk;             // planes per CTA
+  int i_lo, i_hi;        // planes to update (ghosted slabs: interior only)
   int tiles_k, tiles_j;
   const Status* st;
   // fast mode: central coefficients c[r] (r = 1..3) and the composite
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a, const in
   const int chunk_id = blockIdx.x / ntile;
   const int k0 = (tile % a.tiles_k) * F3_TK;
   const int j0 = (tile / a.tiles_k) * F3_TJ;
-  const int i0 = chunk_id * a.chunk;
-  const int i1 = min(i0 + a.chunk, a.n0);
+  const int i0 = a.i_lo + chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.i_hi);
   if (i0 >= i1) return;
   const int k = k0 + tx, j = j0 + ty;
   const bool act = k < a.n2 && j < a.n1;
@@ -444,8 +445,8 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_fast(F3Args a, const int
   const int chunk_id = blockIdx.x / ntile;
   const int k0 = (tile % a.tiles_k) * F3_TK;
   const int j0 = (tile / a.tiles_k) * F3_TJ;
-  const int i0 = chunk_id * a.chunk;
-  const int i1 = min(i0 + a.chunk, a.n0);
+  const int i0 = a.i_lo + chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.i_hi);
   if (i0 >= i1) return;
   const int k = k0 + tx, j = j0 + ty;  // interior tiles: always inside
   const int n0 = a.n0;

@@ -1,0 +1,309 @@
+"""Slab decomposition of the fused 3-D pseudo-time solve over P GPUs.
+
+SURVEY §8(e): one process per GPU; the grid is split along axis 0 (the
+memory-slowest axis, periodic in BASELINE configs 4 and 5) into contiguous
+slabs of ``nl = n0 / P`` planes, each stored with ``G`` ghost planes per side.
+One pseudo-step:
+
+* before each RK stage, exchange the stage input's ghost planes with both
+  ring neighbours (``send/recv``, NCCL over NVLink);
+* run the fused stage kernel on the slab interior (``wd_dist_stage``);
+* filter axis 0 exactly on full x-lines: pack the slab into P chunks,
+  ``all_to_all`` to pencils ``(n0, n1/P, n2)``, sweep, ``all_to_all`` back;
+* filter axes 1 and 2 on the slab; the last sweep accumulates the local
+  ``max|Δφ|``, ``max|φ|`` and non-finite flag;
+* ``all_reduce(max)`` of those three words, then the stop test.
+
+Every node and every filter line sees exactly the operations of the
+single-GPU path, so the decomposed solve is bit-identical to it (checked by
+``tests/test_gpu_dist.py`` with P simulated ranks on one GPU).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+
+GHOST = 7  # >= 4 + R (exact axis-0 windows) and >= 2R (fast mode), R <= 3
+
+
+@dataclass(frozen=True)
+class Slab:
+    """Rank ``rank``'s share of axis 0: global planes [lo, lo + nl)."""
+
+    n0: int
+    P: int
+    rank: int
+    G: int = GHOST
+
+    @property
+    def nl(self) -> int:
+        return self.n0 // self.P
+
+    @property
+    def lo(self) -> int:
+        return self.rank * self.nl
+
+    @property
+    def left(self) -> int:
+        return (self.rank - 1) % self.P
+
+    @property
+    def right(self) -> int:
+        return (self.rank + 1) % self.P
+
+    def check(self, n1: int):
+        if self.n0 % self.P:
+            raise ValueError(f"axis 0 ({self.n0}) must divide evenly over {self.P} ranks")
+        if n1 % self.P:
+            raise ValueError(f"axis 1 ({n1}) must divide evenly over {self.P} ranks")
+        if self.nl < self.G:
+            raise ValueError(f"slab of {self.nl} planes is thinner than {self.G} ghost planes")
+
+
+def split_global(field, P):
+    """Global (n0, n1, n2) array -> list of P ghosted slabs (ghosts zero)."""
+    n0 = field.shape[0]
+    out = []
+    for r in range(P):
+        s = Slab(n0, P, r)
+        g = np.zeros((s.nl + 2 * s.G,) + field.shape[1:])
+        g[s.G:s.G + s.nl] = field[s.lo:s.lo + s.nl]
+        out.append(g)
+    return out
+
+
+# ------------------------------------------------------------- communicators
+class TorchComm:
+    """One rank of a torch.distributed group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def halo(self, slabs, slab: Slab):
+        """Fill the ghost planes of this rank's (nl + 2G, ...) tensor."""
+        (t,) = slabs
+        G, nl = slab.G, slab.nl
+        if self.P == 1:
+            t[:G].copy_(t[nl:nl + G])
+            t[nl + G:].copy_(t[G:2 * G])
+            return
+        d = self.dist
+        lo = t.new_empty(t[:G].shape)
+        hi = t.new_empty(t[:G].shape)
+        # posting order matters when left == right (P = 2): point-to-point
+        # ops between one pair of ranks match in the order they are posted
+        ops = [d.P2POp(d.isend, t[nl:nl + G].contiguous(), slab.right, self.group),
+               d.P2POp(d.irecv, lo, slab.left, self.group),
+               d.P2POp(d.isend, t[G:2 * G].contiguous(), slab.left, self.group),
+               d.P2POp(d.irecv, hi, slab.right, self.group)]
+        for req in d.batch_isend_irecv(ops):
+            req.wait()
+        t[:G].copy_(lo)
+        t[nl + G:].copy_(hi)
+
+    def alltoall(self, outs, ins):
+        (o,), (i,) = outs, ins
+        if self.P == 1:
+            o.copy_(i)
+            return
+        self.dist.all_to_all_single(o, i, group=self.group)
+
+    def allreduce_max(self, ts):
+        (t,) = ts
+        if self.P > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
+
+class LocalComm:
+    """P logical ranks in one process (device copies stand in for NVLink).
+    Used to check the decomposition on one GPU: no kernel ever waits on
+    another rank's kernel."""
+
+    def __init__(self, P):
+        self.P = P
+
+    def halo(self, slabs, slab: Slab):
+        G, nl = slab.G, slab.nl
+        P = self.P
+        lows = [t[G:2 * G].clone() for t in slabs]
+        highs = [t[nl:nl + G].clone() for t in slabs]
+        for r, t in enumerate(slabs):
+            t[:G].copy_(highs[(r - 1) % P])
+            t[nl + G:].copy_(lows[(r + 1) % P])
+
+    def alltoall(self, outs, ins):
+        P = self.P
+        chunks = [i.view(P, -1) for i in ins]
+        for r, o in enumerate(outs):
+            ov = o.view(P, -1)
+            for s in range(P):
+                ov[s].copy_(chunks[s][r])
+
+    def allreduce_max(self, ts):
+        import torch
+        m = torch.stack(list(ts)).max(dim=0).values
+        for t in ts:
+            t.copy_(m)
+
+
+# ------------------------------------------------------------------ solver
+class DistributedSolve:
+    """Fused 3-D pseudo-time solve on the slabs of ``ranks`` (one entry per
+    local logical rank: 1 under torchrun, P in the simulated mode)."""
+
+    def __init__(self, dims, spacing, faces, scheme, formulation, filter_config, cfl, tol,
+                 max_iters, arith, comm, ranks, ref_length=1.0):
+        import torch
+        from ._context import NativeSolver
+        from .grid import CurvilinearGrid
+        self.torch = torch
+        self.comm = comm
+        n0, n1, n2 = dims
+        P = comm.P
+        if faces.get("imin") != "periodic":
+            raise ValueError("slab decomposition needs a periodic axis 0")
+        if filter_config is None:
+            raise ValueError("the distributed path runs the filtered scheme")
+        self.dims = dims
+        self.slabs = [Slab(n0, P, r) for r in ranks]
+        for s in self.slabs:
+            s.check(n1)
+        s0 = self.slabs[0]
+        self.nl, self.G = s0.nl, s0.G
+        gdims = (self.nl + 2 * self.G, n1, n2)
+        # local geometry: ghosted slab, axis 0 open (ghosts carry the wrap)
+        lfaces = {k: v for k, v in faces.items() if k not in ("imin", "imax")}
+        per = (False, faces.get("jmin") == "periodic", faces.get("kmin") == "periodic")
+        self.per = per
+        g = CurvilinearGrid._analytic((0.0, 0.0, 0.0), spacing, gdims, ref_length, per,
+                                      [spacing[d] * gdims[d] for d in range(3)])
+        self.ctxs = []
+        self.hists = []
+        for _ in ranks:
+            ctx = NativeSolver(g, lfaces, None, scheme, formulation, filter_config, cfl, tol,
+                               max_iters, arith=arith)
+            if not ctx.fused:
+                raise ValueError("configuration is not on the fused 3-D path")
+            nat.check(ctx.lib.wd_dist_configure(ctx.ptr, self.G, self.G + self.nl))
+            self.ctxs.append(ctx)
+        self.lib = self.ctxs[0].lib
+        f64 = dict(dtype=torch.float64, device="cuda")
+        R = len(ranks)
+        self.A = [torch.zeros(gdims, **f64) for _ in range(R)]
+        self.B = [torch.zeros(gdims, **f64) for _ in range(R)]
+        self.Pa = [torch.zeros(gdims, **f64) for _ in range(R)]
+        self.Pb = [torch.zeros(gdims, **f64) for _ in range(R)]
+        nlc = self.nl * n1 * n2
+        self.send = [torch.empty(nlc, **f64) for _ in range(R)]
+        self.pen = [torch.empty(nlc, **f64) for _ in range(R)]
+        self.pen2 = [torch.empty(nlc, **f64) for _ in range(R)]
+        self.back = [torch.empty(nlc, **f64) for _ in range(R)]
+        self.slab1 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
+        self.slab2 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
+        self.stats = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(R)]
+        for ctx in self.ctxs:
+            h = torch.zeros(max(max_iters, 1), **f64)
+            self.hists.append(h)
+        self._bound = False
+
+    # -- state
+    def set_state(self, local_slabs):
+        """local_slabs: per local rank, (nl, n1, n2) arrays (numpy or torch)."""
+        torch = self.torch
+        for A, s in zip(self.A, local_slabs):
+            t = s if isinstance(s, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(s))
+            A[self.G:self.G + self.nl].copy_(t.to(A.device))
+        for ctx, A, h in zip(self.ctxs, self.A, self.hists):
+            # wd_bind applies the (wall) BCs of the local geometry and resets status
+            nat.check(self.lib.wd_bind(ctx.ptr, A.data_ptr(), h.data_ptr()))
+        self._bound = True
+
+    def state(self):
+        return [A[self.G:self.G + self.nl] for A in self.A]
+
+    def _interior(self, t):
+        return t[self.G:self.G + self.nl]
+
+    def step(self):
+        torch = self.torch
+        if isinstance(self.comm, LocalComm):
+            self._step()
+            return
+        # one rank per process: run torch-side transfers on the solver stream
+        with torch.cuda.stream(self.ctxs[0].stream()):
+            self._step()
+
+    def _step(self):
+        lib, comm = self.lib, self.comm
+        n0, n1, n2 = self.dims
+        P, nl = comm.P, self.nl
+        m1 = n1 // P
+        R = len(self.ctxs)
+        bufs = [self.A, self.Pa, self.Pb, self.Pa]
+        outs = [self.Pa, self.Pb, self.Pa, self.Pb]
+        for s in range(4):
+            self._sync()
+            comm.halo(bufs[s], self.slabs[0])
+            self._sync()
+            for r in range(R):
+                nat.check(lib.wd_dist_stage(self.ctxs[r].ptr, s + 1, self.A[r].data_ptr(),
+                                            bufs[s][r].data_ptr(), outs[s][r].data_ptr()))
+        streams = [self.ctxs[r].lib.wd_get_stream(self.ctxs[r].ptr) for r in range(R)]
+        # axis-0 filter on pencils (n0, n1/P, n2)
+        for r in range(R):
+            x = self._interior(self.Pb[r])
+            nat.check(lib.wd_dist_pack(x.data_ptr(), self.send[r].data_ptr(), nl, n1, n2, P,
+                                       streams[r]))
+        self._sync()
+        comm.alltoall(self.pen, self.send)
+        self._sync()
+        for r in range(R):
+            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 0, self.pen[r].data_ptr(),
+                                         self.pen2[r].data_ptr(), n0, m1, n2, 1, None))
+        self._sync()
+        comm.alltoall(self.back, self.pen2)
+        self._sync()
+        for r in range(R):
+            nat.check(lib.wd_dist_unpack(self.back[r].data_ptr(), self.slab1[r].data_ptr(), nl,
+                                         n1, n2, P, streams[r]))
+            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 1, self.slab1[r].data_ptr(),
+                                         self.slab2[r].data_ptr(), nl, n1, n2,
+                                         int(self.per[1]), None))
+            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 2, self.slab2[r].data_ptr(),
+                                         self._interior(self.B[r]).data_ptr(), nl, n1, n2,
+                                         int(self.per[2]), self._interior(self.A[r]).data_ptr()))
+            nat.check(lib.wd_dist_stats(self.ctxs[r].ptr, self.stats[r].data_ptr()))
+        self._sync()
+        comm.allreduce_max(self.stats)
+        self._sync()
+        for r in range(R):
+            nat.check(lib.wd_dist_finalize(self.ctxs[r].ptr, self.stats[r].data_ptr()))
+        self.A, self.B = self.B, self.A
+
+    def _sync(self):
+        """Simulated ranks use one stream per logical rank: order them
+        around the device-copy transfers.  With one rank per process all work
+        shares the solver stream and needs no host synchronisation."""
+        if isinstance(self.comm, LocalComm):
+            self.torch.cuda.synchronize()
+
+    def status(self, r=0):
+        st = nat.Status()
+        nat.check(self.lib.wd_read_status(self.ctxs[r].ptr, ctypes.byref(st)))
+        return st
+
+    def history(self, r=0):
+        st = self.status(r)
+        return self.hists[r][:st.iters].cpu().numpy()
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()

@@ -1,0 +1,85 @@
+"""The slab decomposition's host-side communication (dist.TorchComm) with
+world_size 2 over gloo on CPU: ghost-plane ring exchange, slab <-> pencil
+all_to_all (the axis-0 filter transpose) and the all_reduce(max) of the
+convergence words reassemble the global field exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, dims, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_09859_b200 import dist
+        n0, n1, n2 = dims
+        glob = np.arange(n0 * n1 * n2, dtype=float).reshape(dims)
+        slab = dist.Slab(n0, world, rank)
+        slab.check(n1)
+        G, nl = slab.G, slab.nl
+        t = torch.from_numpy(dist.split_global(glob, world)[rank])
+        comm = dist.TorchComm()
+        comm.halo([t], slab)
+        lo_expect = np.take(glob, range(slab.lo - G, slab.lo), axis=0, mode="wrap")
+        hi_expect = np.take(glob, range(slab.lo + nl, slab.lo + nl + G), axis=0, mode="wrap")
+        ok_halo = np.array_equal(t[:G].numpy(), lo_expect) and \
+            np.array_equal(t[nl + G:].numpy(), hi_expect)
+        # slab (nl, n1, n2) -> (P, nl, n1/P, n2) as wd_dist_pack, all_to_all -> pencil
+        m1 = n1 // world
+        interior = t[G:G + nl].numpy()
+        packed = interior.reshape(nl, world, m1, n2).transpose(1, 0, 2, 3).copy()
+        send = torch.from_numpy(packed.ravel())
+        recv = torch.empty_like(send)
+        comm.alltoall([recv], [send])
+        pencil = recv.numpy().reshape(n0, m1, n2)
+        ok_pencil = np.array_equal(pencil, glob[:, rank * m1:(rank + 1) * m1, :])
+        # back: pencil as P chunks along i -> (P, nl, m1, n2) -> unpack
+        back = torch.empty_like(send)
+        comm.alltoall([back], [torch.from_numpy(pencil.ravel().copy())])
+        unpacked = back.numpy().reshape(world, nl, m1, n2).transpose(1, 0, 2, 3).reshape(nl, n1, n2)
+        ok_back = np.array_equal(unpacked, interior)
+        stats = torch.tensor([rank * 10 + 3, 7 - rank, rank], dtype=torch.int64)
+        comm.allreduce_max([stats])
+        ok_red = stats.tolist() == [(world - 1) * 10 + 3, 7, world - 1]
+        q.put((rank, ok_halo, ok_pencil, ok_back, ok_red))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims", [(16, 8, 5), (32, 6, 3)])
+def test_torchcomm_gloo_world2(dims):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, dims, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert all(r[1:]), r
+
+
+def test_slab_partition_bookkeeping():
+    from paper_2111_09859_b200 import dist
+    s = dist.Slab(64, 4, 3)
+    assert (s.nl, s.lo, s.left, s.right) == (16, 48, 2, 0)
+    parts = dist.split_global(np.arange(64 * 4 * 2, dtype=float).reshape(64, 4, 2), 4)
+    assert len(parts) == 4 and parts[0].shape == (16 + 2 * s.G, 4, 2)
+    with pytest.raises(ValueError):
+        dist.Slab(64, 4, 0, G=20).check(4)

@@ -111,18 +111,20 @@ def test_fast_mode_close_to_oracle(case):
 
 # ---------------------------------------------------------------- C4 strips
 # BASELINE config 4 (walls y = 0, 1; periodic x, z; HJ E6 F0.49) has an
-# x/z-invariant solution: a 40 x ny x 40 slab with the strip's spacings runs
-# the same operations on the same values as the oracle's 5 x ny x 5 strip
-# (tests/golden/make_strip_golden.py), so its columns match bit for bit.
+# x/z-invariant solution, so the oracle's 5 x ny x 5 strip
+# (tests/golden/make_strip_golden.py) gives its iteration count and profile.
+# The same 5 x ny x 5 grid on the GPU must match bit for bit; wider slabs
+# differ at round-off only (the periodic filter of a constant line depends on
+# the line length), which the fast-mode tolerance test covers.
 import goldens  # noqa: E402
 
 
-def _strip_case(ny, arith):
+def _strip_case(ny, arith, width):
     z = goldens.load(f"strip_c4_ny{ny}")
     n = int(z["n"])
     faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "wall",
              "kmin": "periodic", "kmax": "periodic"}
-    g = W.build_cartesian(40, ny, 40, Lx=40.0 / n, Ly=1.0, Lz=40.0 / n,
+    g = W.build_cartesian(width, ny, width, Lx=width / n, Ly=1.0, Lz=width / n,
                           periodic=(True, False, True))
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj", epsilon=0.2), scheme="E6",
                         filter_config=W.FilterConfig(0.49), cfl=0.5, tol=float(z["tol"]),
@@ -133,18 +135,17 @@ def _strip_case(ny, arith):
 
 @pytest.mark.parametrize("ny", [129, 512])
 def test_c4_strip_exact_converged(ny):
-    z, rep = _strip_case(ny, "exact")
+    z, rep = _strip_case(ny, "exact", 5)
     assert rep.converged and rep.iters == int(z["iters"])
     assert same(rep.residual_history, z["residual_history"])
-    prof = z["profile"]
-    assert same(rep.phi, np.broadcast_to(prof[None, :, None], rep.phi.shape))
+    assert same(rep.phi, z["phi"])
 
 
 @pytest.mark.parametrize("ny", [129, 512])
 def test_c4_strip_fast_converged(ny):
     """North-star tolerance: converged field within 1e-10 of max wall
     distance, iteration count within 1."""
-    z, rep = _strip_case(ny, "fast")
+    z, rep = _strip_case(ny, "fast", 40)
     assert rep.converged and abs(rep.iters - int(z["iters"])) <= 1
     prof = z["profile"]
     err = np.max(np.abs(rep.phi - prof[None, :, None])) / np.max(prof)
