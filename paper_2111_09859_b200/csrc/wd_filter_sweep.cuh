@@ -81,6 +81,55 @@ __device__ __forceinline__ double filt_rhs5(const double* w, const FilterCoef& f
          c[4] * (w[9] + w[1]) + c[5] * (w[10] + w[0]);
 }
 
+// Rows [r0, r0+16) of the warp's 32 lines -> v[s] (lane = line).  Axes
+// 0/1: direct coalesced loads.  Axis 2: 16 loads of two 128-byte line
+// segments each, transposed through the warp's 32x17 shared tile.
+template <bool CONTIG>
+__device__ __forceinline__ void sw_rows(const double* __restrict__ in, long long lbase,
+                                        long long gbase, long long rstride, long long lstride,
+                                        int nl, int n, int per, int r0, double (*T)[17], int lane,
+                                        double* v) {
+  if (CONTIG) {
+    int r = r0 + (lane & 15);
+    bool ok = true;
+    if (per) {
+      while (r < 0) r += n;
+      while (r >= n) r -= n;
+    } else {
+      ok = r >= 0 && r < n;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int m = 2 * q + (lane >> 4);
+      T[m][lane & 15] = (ok && m < nl) ? __ldcs(in + gbase + (long long)m * lstride + r) : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = T[lane][s];
+    __syncwarp();
+  } else {
+    if (!per && r0 >= 0 && r0 + 16 <= n) {
+      const double* p = in + lbase + (long long)r0 * rstride;
+#pragma unroll
+      for (int s = 0; s < 16; ++s) v[s] = __ldcs(p + (long long)s * rstride);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        int r = r0 + s;
+        bool ok = true;
+        if (per) {
+          while (r < 0) r += n;
+          while (r >= n) r -= n;
+        } else {
+          ok = r >= 0 && r < n;
+        }
+        v[s] = ok ? __ldcs(in + lbase + (long long)r * rstride) : 0.0;
+      }
+    }
+  }
+}
+
+template <bool CONTIG>
 __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double sw_smem[];
@@ -93,6 +142,7 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
   double* sz = srinv + n;
   double* sh = sz + n;
   double* ck = sh + n;  // [nb][blockDim.x]
+  double(*tiles)[32][17] = reinterpret_cast<double(*)[32][17]>(ck + (size_t)nb * blockDim.x);
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     sfact[t] = a.fact[t];
     sdu[t] = a.du[t];
@@ -102,152 +152,175 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
     sh[t] = a.per ? a.h[t] : 0.0;
   }
   __syncthreads();
-  const int tid = threadIdx.x;
-  // lines: axis 0 -> (j, k), axis 1 -> (i, k), axis 2 -> (i, j); the
-  // fastest-varying index of the line id is k (axes 0/1) or j (axis 2)
-  long long L, rstride;
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  double(*T)[17] = tiles[wib];
+  // a warp owns 32 lines: consecutive k (axes 0/1) or consecutive j (axis 2)
+  long long groups, per_row_blk, rstride, lstride;
   int fast_n;
   if (a.axis == 0) {
-    L = (long long)a.n1 * a.n2;
+    fast_n = a.n2;
+    per_row_blk = (a.n2 + 31) / 32;
+    groups = (long long)a.n1 * per_row_blk;
     rstride = a.s0;
-    fast_n = a.n2;
+    lstride = 1;
   } else if (a.axis == 1) {
-    L = (long long)a.n0 * a.n2;
-    rstride = a.n2;
     fast_n = a.n2;
+    per_row_blk = (a.n2 + 31) / 32;
+    groups = (long long)a.n0 * per_row_blk;
+    rstride = a.n2;
+    lstride = 1;
   } else {
-    L = (long long)a.n0 * a.n1;
-    rstride = 1;
     fast_n = a.n1;
+    per_row_blk = (a.n1 + 31) / 32;
+    groups = (long long)a.n0 * per_row_blk;
+    rstride = 1;
+    lstride = a.n2;
   }
-  const bool interior_ok = a.per != 0;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int per = a.per;
   double md = 0.0, ma = 0.0;
   int bad = 0;
-  for (long long line = blockIdx.x * (long long)blockDim.x + tid; line < L;
-       line += (long long)gridDim.x * blockDim.x) {
-    const long long outer = line / fast_n;
-    const int inner = (int)(line % fast_n);
-    long long base;
-    if (a.axis == 0) base = outer * a.n2 + inner;
-    else if (a.axis == 1) base = outer * a.s0 + inner;
-    else base = outer * a.s0 + (long long)inner * a.n2;
-    const double* __restrict__ src = a.in + base;
-    auto ld = [&](int row) -> double {
-      int r = row;
-      if (a.per) {
-        while (r < 0) r += n;
-        while (r >= n) r -= n;
-      } else if (r < 0 || r >= n) {
-        return 0.0;
-      }
-      return src[(long long)r * rstride];
-    };
+  for (long long g = gw; g < groups; g += nwarps) {
+    const long long outer = g / per_row_blk;
+    const int blk = (int)(g % per_row_blk);
+    const int inner0 = blk * 32;
+    const int nl = min(32, fast_n - inner0);
+    const bool valid = lane < nl;
+    long long gbase;  // element (row 0) of the group's first line
+    if (a.axis == 0) gbase = outer * a.n2 + inner0;
+    else if (a.axis == 1) gbase = outer * a.s0 + inner0;
+    else gbase = outer * a.s0 + (long long)inner0 * a.n2;
+    const long long lbase = gbase + (valid ? lane : 0) * lstride;
     // ---------------- pass 1: forward elimination, checkpoints
-    double w[11];
+    // u[q] = row 16b - 5 + q; 10 rows carried between blocks, 16 loaded
+    double u[FB + 10];
+    {
+      double v[16];
+      sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, -5, T, lane, v);
 #pragma unroll
-    for (int s = 0; s < 6; ++s) w[s] = 0.0;
-#pragma unroll
-    for (int s = 6; s < 11; ++s) w[s] = ld(s - 11);  // rows -5..-1
+      for (int q = 0; q < 10; ++q) u[q] = v[q];
+    }
     double y = 0.0, hs = 0.0;
-    for (int c = 0; c < nb; ++c) {
-      const int r0 = c * FB;
-      double v[FB];
-#pragma unroll
-      for (int s = 0; s < FB; ++s) v[s] = r0 + s < n ? src[(long long)(r0 + s) * rstride] : 0.0;
-      const bool full = interior_ok || (r0 >= 10 && r0 + FB <= n);
-#pragma unroll
-      for (int s = 0; s < FB; ++s) {
-        const int t = r0 + s;  // newest row in the window
-        if (t >= n) continue;
-#pragma unroll
-        for (int q = 0; q < 10; ++q) w[q] = w[q + 1];
-        w[10] = v[s];
-        const int r = t - 5;
-        if (r < 0) continue;
-        double rhs;
-        if (full) {
-          rhs = filt_rhs5(w, a.fc);
-        } else {
-          const int hh = (r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5);
-          rhs = filt_rhs(w, hh, a.fc);
-        }
-        y = r == 0 ? rhs : rhs - sfact[r - 1] * y;
-        if (a.per) hs = hs + sh[r] * rhs;
-        if ((r % FB) == FB - 1) ck[(r / FB) * blockDim.x + tid] = y;
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {  // rows n..n+4 complete the last 5 RHS
-      const int t = n + s;
-#pragma unroll
-      for (int q = 0; q < 10; ++q) w[q] = w[q + 1];
-      w[10] = ld(t);
-      const int r = t - 5;
-      if (r < 0) continue;
-      const int hh = a.per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
-      const double rhs = filt_rhs(w, hh, a.fc);
-      y = r == 0 ? rhs : rhs - sfact[r - 1] * y;
-      if (a.per) hs = hs + sh[r] * rhs;
-      if ((r % FB) == FB - 1) ck[(r / FB) * blockDim.x + tid] = y;
-    }
-    const double f = a.per ? hs / a.denom : 0.0;
-    // ---------------- pass 2: blocks backwards, recompute y, back-substitute
-    double xn = 0.0;
-    for (int b = nb - 1; b >= 0; --b) {
+    for (int b = 0; b < nb; ++b) {
       const int r0 = b * FB;
-      double u[FB + 10];
-      if (r0 >= 5 && r0 + FB + 5 <= n) {  // interior block: plain loads
-        const double* p = src + (long long)(r0 - 5) * rstride;
+      {
+        double v[16];
+        sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, r0 + 5, T, lane, v);
 #pragma unroll
-        for (int q = 0; q < FB + 10; ++q) u[q] = p[(long long)q * rstride];
+        for (int s = 0; s < 16; ++s) u[10 + s] = v[s];
+      }
+      if ((per && r0 + FB <= n) || (!per && r0 >= 5 && r0 + FB + 5 <= n)) {
+        // interior block: full-order rows, no conditionals
+#pragma unroll
+        for (int s = 0; s < FB; ++s) {
+          const int r = r0 + s;
+          const double rhs = filt_rhs5(u + s, a.fc);
+          y = r == 0 ? rhs : rhs - sfact[r > 0 ? r - 1 : 0] * y;
+          if (per) hs = hs + sh[r] * rhs;
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < FB + 10; ++q) u[q] = ld(r0 - 5 + q);
+        for (int s = 0; s < FB; ++s) {
+          const int r = r0 + s;
+          if (r >= n) break;
+          const int hh = per ? 5 : ((r == 0 || r == n - 1) ? 0 : min(min(r, n - 1 - r), 5));
+          const double rhs = filt_rhs(u + s, hh, a.fc);
+          y = r == 0 ? rhs : rhs - sfact[r - 1] * y;
+          if (per) hs = hs + sh[r] * rhs;
+        }
       }
-      double av[FB];
-      if (a.A) {
+      if (b + 1 < nb) ck[b * blockDim.x + tid] = y;  // y at row 16b + 15
 #pragma unroll
-        for (int s = 0; s < FB; ++s)
-          av[s] = r0 + s < n ? __ldcs(a.A + base + (long long)(r0 + s) * rstride) : 0.0;
+      for (int q = 0; q < 10; ++q) u[q] = u[16 + q];
+    }
+    const double f = per ? hs / a.denom : 0.0;
+    // ---------------- pass 2: blocks backwards, recompute y, back-substitute
+    // u[q] = row 16b - 5 + q; rows 16b+11.. carried from block b+1
+    double xn = 0.0;
+    {
+      const int r0 = (nb - 1) * FB;
+      double v[16];
+      sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, r0 + 11, T, lane, v);
+#pragma unroll
+      for (int q = 0; q < 10; ++q) u[16 + q] = v[q];
+    }
+    for (int b = nb - 1; b >= 0; --b) {
+      const int r0 = b * FB;
+      {
+        double v[16];
+        sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, r0 - 5, T, lane, v);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) u[s] = v[s];
       }
-      const bool full = interior_ok || (r0 >= 5 && r0 + FB + 5 <= n);
+      double av[16];
+      if (a.A) sw_rows<CONTIG>(a.A, lbase, gbase, rstride, lstride, nl, n, 0, r0, T, lane, av);
       double yp = b > 0 ? ck[(b - 1) * blockDim.x + tid] : 0.0;
       double yb[FB];
+      if ((per && r0 + FB <= n) || (!per && r0 >= 5 && r0 + FB + 5 <= n)) {
 #pragma unroll
-      for (int s = 0; s < FB; ++s) {
-        const int r = r0 + s;
-        double rhs;
-        if (full) {
-          rhs = filt_rhs5(u + s, a.fc);
-        } else {
-          const int hh = (r == 0 || r >= n - 1) ? 0 : min(min(r, n - 1 - r), 5);
-          rhs = filt_rhs(u + s, hh, a.fc);
+        for (int s = 0; s < FB; ++s) {
+          const int r = r0 + s;
+          const double rhs = filt_rhs5(u + s, a.fc);
+          yp = r == 0 ? rhs : rhs - sfact[r > 0 ? r - 1 : 0] * yp;
+          yb[s] = yp;
         }
-        yp = r == 0 ? rhs : rhs - sfact[r > 0 ? r - 1 : 0] * yp;
-        yb[s] = yp;
+      } else {
+#pragma unroll
+        for (int s = 0; s < FB; ++s) {
+          const int r = r0 + s;
+          const int hh =
+              per ? (r < n ? 5 : 0) : ((r == 0 || r >= n - 1) ? 0 : min(min(r, n - 1 - r), 5));
+          const double rhs = filt_rhs(u + s, hh, a.fc);
+          yp = r == 0 ? rhs : rhs - sfact[r > 0 && r <= n ? r - 1 : 0] * yp;
+          yb[s] = yp;
+        }
       }
+      double xo[FB];
 #pragma unroll
       for (int s = FB - 1; s >= 0; --s) {
         const int r = r0 + s;
-        if (r >= n) continue;
-        const double x = r == n - 1 ? yb[s] / sd[r] : div_rn(yb[s] - sdu[r] * xn, sd[r], srinv[r]);
-        xn = x;
-        const double xv = a.per ? x - f * sz[r] : x;
-        const long long idx = base + (long long)r * rstride;
-        __stcs(a.out + idx, xv);
-        if (a.A) {
-          if (!isfinite(xv)) bad = 1;
-          ma = fmax(ma, fabs(xv));
-          md = fmax(md, fabs(xv - av[s]));
+        double xv = 0.0;
+        if (r < n) {
+          const double x =
+              r == n - 1 ? yb[s] / sd[r] : div_rn(yb[s] - sdu[r] * xn, sd[r], srinv[r]);
+          xn = x;
+          xv = per ? x - f * sz[r] : x;
+          if (a.A && valid) {
+            if (!isfinite(xv)) bad = 1;
+            ma = fmax(ma, fabs(xv));
+            md = fmax(md, fabs(xv - av[s]));
+          }
         }
+        xo[s] = xv;
       }
+      // store rows [r0, r0+16)
+      if (CONTIG) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) T[lane][s] = xo[s];
+        __syncwarp();
+        const int r = r0 + (lane & 15);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int m = 2 * q + (lane >> 4);
+          if (m < nl && r < n) __stcs(a.out + gbase + (long long)m * lstride + r, T[m][lane & 15]);
+        }
+        __syncwarp();
+      } else if (valid) {
+        double* p = a.out + lbase + (long long)r0 * rstride;
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+          if (r0 + s < n) __stcs(p + (long long)s * rstride, xo[s]);
+      }
+#pragma unroll
+      for (int q = 0; q < 10; ++q) u[16 + q] = u[q];
     }
   }
   if (a.A) {
     md = warp_max(md);
     ma = warp_max(ma);
     bad = __any_sync(0xffffffffu, bad);
-    if ((tid & 31) == 0) {
+    if (lane == 0) {
       atomicMax(&a.st->max_delta_bits, (unsigned long long)__double_as_longlong(md));
       atomicMax(&a.st->max_abs_bits, (unsigned long long)__double_as_longlong(ma));
       if (bad) atomicOr(&a.st->nonfinite, 1);

@@ -44,6 +44,22 @@ void launch_stage(int stage, const F3Args& a, int blocks, const int* tiles, bool
   }
 }
 
+size_t sweep_smem(int n) {
+  return (6 * (size_t)n + (size_t)((n + FB - 1) / FB) * 128 + 4 * 32 * 17) * sizeof(double);
+}
+
+void launch_sweep(const SweepArgs& w, cudaStream_t s) {
+  const int per_row = ((w.axis == 2 ? w.n1 : w.n2) + 31) / 32;
+  const long long outer = w.axis == 0 ? w.n1 : w.n0;
+  const long long groups = outer * per_row;
+  long long ctas = (groups + 3) / 4;
+  if (ctas > 148LL * 8) ctas = 148LL * 8;
+  if (w.axis == 2)
+    k_filter_sweep<true><<<(int)ctas, 128, sweep_smem(w.n), s>>>(w);
+  else
+    k_filter_sweep<false><<<(int)ctas, 128, sweep_smem(w.n), s>>>(w);
+}
+
 void stage_dispatch(int R, bool eik, int stage, const F3Args& a, int blocks, const int* tiles,
                     bool fast, cudaStream_t s) {
   if (R == 1) eik ? launch_stage<1, true>(stage, a, blocks, tiles, fast, s) : launch_stage<1, false>(stage, a, blocks, tiles, fast, s);
@@ -70,9 +86,10 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
       if (in.filt_swaps[a]) return;
     int nmax = 0;
     for (int a = 0; a < 3; ++a) nmax = in.g.n[a] > nmax ? in.g.n[a] : nmax;
-    const int smem = (int)((6 * (size_t)nmax + (size_t)((nmax + FB - 1) / FB) * 128) *
-                           sizeof(double));
-    if (cudaFuncSetAttribute(k_filter_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int smem = (int)sweep_smem(nmax);
+    if (cudaFuncSetAttribute(k_filter_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_filter_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem) != cudaSuccess)
       return;
   }
@@ -230,11 +247,7 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     w.fc = in.fcoef;
     w.A = ax == 2 ? A : nullptr;
     w.st = st;
-    const long long L = g.N / g.n[ax];
-    long long ctas = (L + 127) / 128;
-    if (ctas > 148LL * 8) ctas = 148LL * 8;
-    const size_t smem = (6 * (size_t)w.n + (size_t)((w.n + FB - 1) / FB) * 128) * sizeof(double);
-    k_filter_sweep<<<(int)ctas, 128, smem, s>>>(w);
+    launch_sweep(w, s);
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }
@@ -282,20 +295,18 @@ void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* o
   w.fc = fp.in.fcoef;
   w.A = A;
   w.st = st;
-  const long long L = (long long)n0 * n1 * n2 / w.n;
-  long long ctas = (L + 127) / 128;
-  if (ctas > 148LL * 8) ctas = 148LL * 8;
-  const size_t smem = (6 * (size_t)w.n + (size_t)((w.n + FB - 1) / FB) * 128) * sizeof(double);
-  k_filter_sweep<<<(int)ctas, 128, smem, s>>>(w);
+  launch_sweep(w, s);
 }
 
 void fused_filter_prepare(int n) {
-  const int smem = (int)((6 * (size_t)n + (size_t)((n + FB - 1) / FB) * 128) * sizeof(double));
-  int cur = 0;
+  const int smem = (int)sweep_smem(n);
   cudaFuncAttributes attr;
-  if (cudaFuncGetAttributes(&attr, k_filter_sweep) == cudaSuccess) cur = attr.maxDynamicSharedSizeBytes;
-  if (smem > cur)
-    cudaFuncSetAttribute(k_filter_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (cudaFuncGetAttributes(&attr, k_filter_sweep<true>) == cudaSuccess &&
+      smem > attr.maxDynamicSharedSizeBytes)
+    cudaFuncSetAttribute(k_filter_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (cudaFuncGetAttributes(&attr, k_filter_sweep<false>) == cudaSuccess &&
+      smem > attr.maxDynamicSharedSizeBytes)
+    cudaFuncSetAttribute(k_filter_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,
