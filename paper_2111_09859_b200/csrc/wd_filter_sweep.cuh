@@ -92,11 +92,13 @@ __device__ __forceinline__ void sw_rows(const double* __restrict__ in, long long
   if (CONTIG) {
     int r = r0 + (lane & 15);
     bool ok = true;
-    if (per) {
-      while (r < 0) r += n;
-      while (r >= n) r -= n;
-    } else {
-      ok = r >= 0 && r < n;
+    if (r < 0 || r >= n) {
+      if (per) {
+        while (r < 0) r += n;
+        while (r >= n) r -= n;
+      } else {
+        ok = false;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -108,7 +110,7 @@ __device__ __forceinline__ void sw_rows(const double* __restrict__ in, long long
     for (int s = 0; s < 16; ++s) v[s] = T[lane][s];
     __syncwarp();
   } else {
-    if (!per && r0 >= 0 && r0 + 16 <= n) {
+    if (r0 >= 0 && r0 + 16 <= n) {  // in range: no wrap, no bounds
       const double* p = in + lbase + (long long)r0 * rstride;
 #pragma unroll
       for (int s = 0; s < 16; ++s) v[s] = __ldcs(p + (long long)s * rstride);
