@@ -26,13 +26,24 @@ void launch_stage(int stage, const F3Args& a, int blocks, const int* tiles, bool
                   cudaStream_t s) {
   const dim3 thr(F3_TK, F3_TJ);
   const size_t sm = F3_SMEM_DOUBLES * sizeof(double);
-  const size_t smf = 2 * F3_PH * F3_PW * sizeof(double);
-  if (fast) {
+  if (fast && (a.n2 & 1)) {  // odd rows: 16-byte pairs would be misaligned
+    const size_t smf = 2 * F3_PH * F3_PW * sizeof(double);
     switch (stage) {
       case 1: k_f3_fast<R, EIK, 1><<<blocks, thr, smf, s>>>(a, tiles); break;
       case 2: k_f3_fast<R, EIK, 2><<<blocks, thr, smf, s>>>(a, tiles); break;
       case 3: k_f3_fast<R, EIK, 3><<<blocks, thr, smf, s>>>(a, tiles); break;
       default: k_f3_fast<R, EIK, 4><<<blocks, thr, smf, s>>>(a, tiles); break;
+    }
+    return;
+  }
+  if (fast) {
+    const dim3 thr2(16, F3_TJ);
+    const size_t smf = 2 * F2_PH * F2_PW * sizeof(double);
+    switch (stage) {
+      case 1: k_f3_fast2<R, EIK, 1><<<blocks, thr2, smf, s>>>(a, tiles); break;
+      case 2: k_f3_fast2<R, EIK, 2><<<blocks, thr2, smf, s>>>(a, tiles); break;
+      case 3: k_f3_fast2<R, EIK, 3><<<blocks, thr2, smf, s>>>(a, tiles); break;
+      default: k_f3_fast2<R, EIK, 4><<<blocks, thr2, smf, s>>>(a, tiles); break;
     }
     return;
   }

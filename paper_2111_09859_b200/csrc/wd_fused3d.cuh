@@ -560,4 +560,192 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_fast(F3Args a, const int
   }
 }
 
+// ----------------------------------------------------------------------
+// FAST variant, paired: 256 threads = 16 k-pairs x 16 j-rows; each thread
+// owns the adjacent nodes (k, k+1) of its row, so the k stencils of both
+// nodes come from 7 aligned 16-byte shared loads, the j stencils from 13,
+// and every global access is a 16-byte vector.  Tile 32 (k) x 16 (j), plane
+// tile with an 8-wide k halo (16-byte alignment) and a 7-row j halo.
+constexpr int F2_PW = F3_TK + 16;        // 48 doubles per plane row
+constexpr int F2_PH = F3_TJ + 2 * F3_HP; // 30 rows
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ double2 ldcs2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ void stcs2(double* p, double x, double y) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(x, y));
+}
+
+template <int R, bool EIK, int STAGE>
+__global__ void __launch_bounds__(256, 1) k_f3_fast2(F3Args a, const int* tiles) {
+  if (a.st->state != WD_STATE_RUNNING) return;
+  constexpr int H = 2 * R;       // composite half-width (<= 6)
+  constexpr int NW = 2 * H + 1;  // axis-0 window
+  extern __shared__ double smem[];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // tx: 0..15 (pairs), ty: 0..15
+  const int ntile = tiles[0];
+  const int tile = tiles[1 + blockIdx.x % ntile];
+  const int chunk_id = blockIdx.x / ntile;
+  const int k0 = (tile % a.tiles_k) * F3_TK;
+  const int j0 = (tile / a.tiles_k) * F3_TJ;
+  const int i0 = a.i_lo + chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.i_hi);
+  if (i0 >= i1) return;
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const long long s0 = a.s0;
+  const int k = k0 + 2 * tx, j = j0 + ty;
+  const int col = j * n2 + k;  // in-plane offset of the pair
+  // halo offsets (in-plane), fixed over the stream
+  int jh = -1, kh = -1;
+  if (ty < 2 * F3_HP) {  // j-halo rows: row jj, pair tx
+    const int jg = j0 - F3_HP + (ty < F3_HP ? ty : ty + F3_TJ);
+    jh = (a.per1 ? wrapm(jg, n1) : jg) * n2 + k;
+  }
+  if (tx < 8) {  // k-halo: 4 pairs left (k0-8..k0-1), 4 pairs right (k0+32..)
+    const int kg = tx < 4 ? k0 - 8 + 2 * tx : k0 + F3_TK + 2 * (tx - 4);
+    kh = j * n2 + (a.per2 ? wrapm(kg, n2) : kg);
+  }
+  double2 pw[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    const int pos = a.per0 ? wrapm(i0 - H + s, n0) : i0 - H + s;
+    pw[s] = (pos >= 0 && pos < n0) ? ld2(a.p + (long long)pos * s0 + col) : make_double2(0.0, 0.0);
+  }
+  int inext = a.per0 ? wrapm(i0 + H + 1, n0) : i0 + H + 1;
+  const long long pl0 = (long long)i0 * s0;
+  double2 nA = ldcs2(a.A + pl0 + col);
+  double2 ndt = STAGE > 1 ? ldcs2(a.dt + pl0 + col) : make_double2(0.0, 0.0);
+  double2 nacc = STAGE > 1 ? ldcs2(a.acc + pl0 + col) : make_double2(0.0, 0.0);
+  double2 njh = jh >= 0 ? ld2(a.p + pl0 + jh) : make_double2(0.0, 0.0);
+  double2 nkh = kh >= 0 ? ld2(a.p + pl0 + kh) : make_double2(0.0, 0.0);
+  double2 npn = (a.per0 || inext < n0) ? ld2(a.p + (long long)inext * s0 + col)
+                                        : make_double2(0.0, 0.0);
+  for (int i = i0; i < i1; ++i) {
+    double* Pb = smem + ((i - i0) & 1) * (F2_PH * F2_PW);
+    const long long plane = (long long)i * s0;
+    // own pair at row ty+7, col 8+2tx; halos
+    *reinterpret_cast<double2*>(Pb + (ty + F3_HP) * F2_PW + 8 + 2 * tx) = pw[H];
+    if (jh >= 0 || ty < 2 * F3_HP)
+      *reinterpret_cast<double2*>(Pb + (ty < F3_HP ? ty : ty + F3_TJ) * F2_PW + 8 + 2 * tx) = njh;
+    if (tx < 8)
+      *reinterpret_cast<double2*>(Pb + (ty + F3_HP) * F2_PW +
+                                  (tx < 4 ? 2 * tx : F3_TK + 8 + 2 * (tx - 4))) = nkh;
+    const double2 Av = nA, dtin = ndt, accv = nacc, pnext = npn;
+    inext = inext + 1;
+    if (a.per0 && inext == n0) inext = 0;
+    if (i + 1 < i1) {
+      const long long pl = plane + s0;
+      nA = ldcs2(a.A + pl + col);
+      if (STAGE > 1) ndt = ldcs2(a.dt + pl + col);
+      if (STAGE > 1) nacc = ldcs2(a.acc + pl + col);
+      if (jh >= 0) njh = ld2(a.p + pl + jh);
+      if (kh >= 0) nkh = ld2(a.p + pl + kh);
+      npn = (a.per0 || inext < n0) ? ld2(a.p + (long long)inext * s0 + col)
+                                   : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    // k row: values k-6 .. k+7 (cols 2tx+2 .. 2tx+15)
+    const double* rowp = Pb + (ty + F3_HP) * F2_PW + 2 * tx + 2;
+    double rk[14];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const double2 v = ld2(rowp + 2 * q);
+      rk[2 * q] = v.x;
+      rk[2 * q + 1] = v.y;
+    }
+    // j columns (pair): rows j-6 .. j+6
+    const double* colp = Pb + (ty + F3_HP - 6) * F2_PW + 8 + 2 * tx;
+    double cj0[13], cj1[13];
+#pragma unroll
+    for (int q = 0; q < 13; ++q) {
+      const double2 v = ld2(colp + q * F2_PW);
+      cj0[q] = v.x;
+      cj1[q] = v.y;
+    }
+    double out2[2], acc2[2], dt2[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double* wk = rk + 6 + e - H + H;  // centre of node e: rk[6 + e]
+      const double* ck = wk;
+      const double* cjv = e == 0 ? cj0 + 6 : cj1 + 6;
+      const double* pwc;  // axis-0 window of node e (struct of pairs)
+      double w0[NW];
+#pragma unroll
+      for (int s = 0; s < NW; ++s) w0[s] = e == 0 ? pw[s].x : pw[s].y;
+      pwc = w0 + H;
+      (void)pwc;
+      const double d2 = f_d<R>(a, ck[-3 < -H ? -H : -3], ck[-2], ck[-1], ck[1], ck[2],
+                               ck[3 > H ? H : 3]);
+      const double d1 = f_d<R>(a, cjv[-3 < -H ? -H : -3], cjv[-2], cjv[-1], cjv[1], cjv[2],
+                               cjv[3 > H ? H : 3]);
+      const double dd2 = f_dd<R>(a, ck);
+      const double dd1 = f_dd<R>(a, cjv);
+      double d0, dd0;
+      if (a.per0 || (i >= H && i <= n0 - 1 - H)) {
+        d0 = f_d<R>(a, w0[H - 3 < 0 ? 0 : H - 3], w0[H - 2 < 0 ? 0 : H - 2], w0[H - 1],
+                    w0[H + 1], w0[H + 2 > 2 * H ? 2 * H : H + 2],
+                    w0[H + 3 > 2 * H ? 2 * H : H + 3]);
+        dd0 = f_dd<R>(a, w0 + H);
+      } else {
+        constexpr int SCH = SchemeOf<R>::id;
+        Line gl{a.p + col + e, s0, n0, 0, 0.0};
+        d0 = deriv_explicit_at(gl, i, n0, SCH, 0);
+        double u[9];
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+          const int q = i - 4 + s;
+          u[s] = (q >= 0 && q < n0) ? a.c0 * deriv_explicit_at(gl, q, n0, SCH, 0) : 0.0;
+        }
+        dd0 = d0_from_window<R>(u, i, n0, 0) / a.c0;
+      }
+      const double pv = w0[H];
+      const double h0 = a.cc0 * d0, h1 = a.cc1 * d1, h2 = a.cc2 * d2;
+      double adv = h0 * d0;
+      adv = fma(h1, d1, adv);
+      adv = fma(h2, d2, adv);
+      double kv;
+      if (EIK) {
+        kv = 1.0 - adv;
+      } else {
+        double lap = a.cc0 * dd0;
+        lap = fma(a.cc1, dd1, lap);
+        lap = fma(a.cc2, dd2, lap);
+        kv = fma(a.eps * pv, lap, 1.0) - adv;
+      }
+      const bool pinned = (i == 0 && a.wall[0]) || (i == n0 - 1 && a.wall[1]);
+      const double Ae = e == 0 ? Av.x : Av.y;
+      const double dte = e == 0 ? dtin.x : dtin.y;
+      const double acce = e == 0 ? accv.x : accv.y;
+      if (STAGE == 1) {
+        double den = fabs(h0) + fabs(h1) + fabs(h2);
+        if (!EIK) den = fma(2.0 * (a.eps * pv), a.sumS, den);
+        const double dtv = fmin(a.cfl / (den + 1e-30), a.cflms);
+        dt2[e] = dtv;
+        acc2[e] = kv;
+        out2[e] = pinned ? 0.0 : fma(0.5 * dtv, kv, Ae);
+      } else if (STAGE == 2 || STAGE == 3) {
+        acc2[e] = fma(2.0, kv, acce);
+        const double cdt = STAGE == 3 ? dte : 0.5 * dte;
+        out2[e] = pinned ? 0.0 : fma(cdt, kv, Ae);
+      } else {
+        out2[e] = pinned ? 0.0 : fma(dte / 6.0, acce + kv, Ae);
+      }
+    }
+    const long long idx = plane + col;
+    if (STAGE == 1) {
+      stcs2(a.dt + idx, dt2[0], dt2[1]);
+      stcs2(a.acc + idx, acc2[0], acc2[1]);
+    } else if (STAGE == 2 || STAGE == 3) {
+      stcs2(a.acc + idx, acc2[0], acc2[1]);
+    }
+    *reinterpret_cast<double2*>(a.out + idx) = make_double2(out2[0], out2[1]);
+#pragma unroll
+    for (int s = 0; s < NW - 1; ++s) pw[s] = pw[s + 1];
+    pw[NW - 1] = pnext;
+  }
+}
+
 }  // namespace wd
