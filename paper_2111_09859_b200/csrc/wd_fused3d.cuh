@@ -656,21 +656,36 @@ __global__ void __launch_bounds__(256, 1) k_f3_fast2(F3Args a, const int* tiles)
       rk[2 * q] = v.x;
       rk[2 * q + 1] = v.y;
     }
-    // j columns (pair): rows j-6 .. j+6
-    const double* colp = Pb + (ty + F3_HP - 6) * F2_PW + 8 + 2 * tx;
-    double cj0[13], cj1[13];
+    // j stencils of both nodes, accumulated over symmetric row pairs
+    const double* colp = Pb + (ty + F3_HP) * F2_PW + 8 + 2 * tx;  // row j
+    double dj[2], ddj[2];
+    {
+      const double2 c = ld2(colp);
+      ddj[0] = a.e[0] * c.x;
+      ddj[1] = a.e[0] * c.y;
+      dj[0] = dj[1] = 0.0;
 #pragma unroll
-    for (int q = 0; q < 13; ++q) {
-      const double2 v = ld2(colp + q * F2_PW);
-      cj0[q] = v.x;
-      cj1[q] = v.y;
+      for (int m = 1; m <= H; ++m) {
+        const double2 lo = ld2(colp - m * F2_PW);
+        const double2 hi = ld2(colp + m * F2_PW);
+        ddj[0] = fma(a.e[m], hi.x + lo.x, ddj[0]);
+        ddj[1] = fma(a.e[m], hi.y + lo.y, ddj[1]);
+        if (m <= R) {
+          if (m == 1) {
+            dj[0] = a.cr[1] * (hi.x - lo.x);
+            dj[1] = a.cr[1] * (hi.y - lo.y);
+          } else {
+            dj[0] = fma(a.cr[m], hi.x - lo.x, dj[0]);
+            dj[1] = fma(a.cr[m], hi.y - lo.y, dj[1]);
+          }
+        }
+      }
     }
     double out2[2], acc2[2], dt2[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const double* wk = rk + 6 + e - H + H;  // centre of node e: rk[6 + e]
       const double* ck = wk;
-      const double* cjv = e == 0 ? cj0 + 6 : cj1 + 6;
       const double* pwc;  // axis-0 window of node e (struct of pairs)
       double w0[NW];
 #pragma unroll
@@ -679,10 +694,9 @@ __global__ void __launch_bounds__(256, 1) k_f3_fast2(F3Args a, const int* tiles)
       (void)pwc;
       const double d2 = f_d<R>(a, ck[-3 < -H ? -H : -3], ck[-2], ck[-1], ck[1], ck[2],
                                ck[3 > H ? H : 3]);
-      const double d1 = f_d<R>(a, cjv[-3 < -H ? -H : -3], cjv[-2], cjv[-1], cjv[1], cjv[2],
-                               cjv[3 > H ? H : 3]);
+      const double d1 = dj[e];
       const double dd2 = f_dd<R>(a, ck);
-      const double dd1 = f_dd<R>(a, cjv);
+      const double dd1 = ddj[e];
       double d0, dd0;
       if (a.per0 || (i >= H && i <= n0 - 1 - H)) {
         d0 = f_d<R>(a, w0[H - 3 < 0 ? 0 : H - 3], w0[H - 2 < 0 ? 0 : H - 2], w0[H - 1],
