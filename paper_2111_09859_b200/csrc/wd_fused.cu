@@ -132,6 +132,12 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
     }
     fp.fast_tiles = fp.tiles_dev;
     fp.exact_tiles = fp.tiles_dev + fastl.size();
+    if (fp.n_exact && fp.n_fast) {
+      if (cudaStreamCreateWithFlags(&fp.side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&fp.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&fp.ev_join, cudaEventDisableTiming) != cudaSuccess)
+        fp.side = nullptr;
+    }
     const size_t smf = 2 * F3_PH * F3_PW * sizeof(double);
     (void)smf;
   }
@@ -228,8 +234,18 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
   }
   if (kid >= 1 && kid <= 4) {
     if (fp.fast_tiles) {
+      // boundary tiles (exact kernel) on a forked stream so they overlap the
+      // interior tiles instead of running as a thin serial tail
+      if (fp.n_exact && fp.side) {
+        cudaEventRecord(fp.ev_fork, s);
+        cudaStreamWaitEvent(fp.side, fp.ev_fork, 0);
+        stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, fp.side);
+        cudaEventRecord(fp.ev_join, fp.side);
+      } else if (fp.n_exact) {
+        stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+      }
       if (fp.n_fast) stage_dispatch(R, eik, kid, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
-      if (fp.n_exact) stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+      if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
     } else {
       stage_dispatch(R, eik, kid, a, chunks * all_tiles, nullptr, false, s);
     }
@@ -275,8 +291,16 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
   a.p = p;
   a.out = out;
   if (fp.fast_tiles) {
+    if (fp.n_exact && fp.side) {
+      cudaEventRecord(fp.ev_fork, s);
+      cudaStreamWaitEvent(fp.side, fp.ev_fork, 0);
+      stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, fp.side);
+      cudaEventRecord(fp.ev_join, fp.side);
+    } else if (fp.n_exact) {
+      stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+    }
     if (fp.n_fast) stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
-    if (fp.n_exact) stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
+    if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
   } else {
     stage_dispatch(R, eik, stage, a, chunks * all_tiles, nullptr, false, s);
   }
@@ -333,6 +357,13 @@ void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, dou
 }
 
 void fused_release(FusedPlan& fp) {
+  if (fp.side) {
+    cudaStreamSynchronize(fp.side);
+    cudaStreamDestroy(fp.side);
+    cudaEventDestroy(fp.ev_fork);
+    cudaEventDestroy(fp.ev_join);
+    fp.side = nullptr;
+  }
   if (fp.tiles_dev) cudaFree(fp.tiles_dev);
   fp.tiles_dev = nullptr;
   fp.active = 0;
