@@ -182,6 +182,52 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
+def _device_steps(grid, cfg, fc, filt, K, Wm, arith):
+    """K device-timed steps of the same workload in another arithmetic mode."""
+    import torch
+    from paper_2111_09859_b200 import _context, _native as nat
+    ctx = _context.NativeSolver(grid, cfg["faces"], None, cfg["scheme"], fc, filt, 0.5, 1e-15,
+                                10**9, arith=arith)
+    dims = tuple(grid.dims)
+    phi = torch.zeros(dims, dtype=torch.float64, device="cuda")
+    hist = torch.zeros(K + Wm + 8, dtype=torch.float64, device="cuda")
+    nat.check(ctx.lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
+    stream = ctx.stream()
+    nat.check(ctx.lib.wd_steps(ctx.ptr, Wm))
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    nat.check(ctx.lib.wd_steps(ctx.ptr, K))
+    e1.record(stream)
+    e1.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3
+    ctx.close()
+    del phi, hist
+    torch.cuda.empty_cache()
+    N = int(np.prod(dims))
+    return {"arith": arith, "value": round(N * K / secs / 1e9, 4), "unit": UNIT,
+            "ms_per_step": round(secs / K * 1e3, 4),
+            "parity": "bit-identical to the reference algorithm (oracle/wd.py)"}
+
+
+def _time_to_converge(ms_per_step, arith):
+    """Iterations to tol 1e-8 measured for this configuration (profiles/
+    converge.json, written from tools/converge.py / the strip goldens) x the
+    measured step time."""
+    path = os.path.join(ROOT, "profiles", "converge.json")
+    try:
+        rec = json.load(open(path))["c4"]
+    except Exception:
+        return None
+    iters = rec.get("iters")
+    out = {"iters_to_tol_1e-8": iters, "source": rec.get("source"),
+           "est_seconds": round(iters * ms_per_step / 1e3, 2) if iters else None}
+    if rec.get("measured_s") and rec.get("arith") == arith:
+        out["measured_seconds"] = rec["measured_s"]
+    return out
+
+
 def run_b200_dist(args, world, rank, local):
     """N > 1: slab decomposition of the same global grid (strong scaling)."""
     import torch
@@ -348,6 +394,10 @@ def run_b200(args, world, rank, local):
                "d2h_bytes_per_step": int((N * 8 + 8 * K) / K),
                "seconds": t_e2e, "includes": "context setup + H2D phi0 (pinned) + K steps + "
                                              "residual history + D2H phi"}
+    exact_side = None
+    if args.arith == "fast" and not args.no_exact:
+        exact_side = _device_steps(grid, cfg, fc, filt, K, Wm, "exact")
+    ttc = _time_to_converge(secs_max / K * 1e3, args.arith)
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": Wm, "ms_per_step": round(secs_max / K * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -360,8 +410,9 @@ def run_b200(args, world, rank, local):
             "step_roofline": {"achieved": round(step_ach, 1), "peak": peak, "unit": "GB/s",
                               "frac": round(step_ach / peak, 4), "words_per_update": w_upd},
             "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
-            "gpu_launches": K * (8 if kern else 0),
-            "clocks": clk, "e2e": e2e}
+            "gpu_launches": K * (12 if kern else 0),
+            "clocks": clk, "e2e": e2e,
+            "exact_mode": exact_side, "time_to_converge": ttc}
     if rank == 0 and not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_sample(cfg, 3, 1)
     if rank == 0:
@@ -378,7 +429,10 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override grid size (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--arith", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--arith", default="fast", choices=["exact", "fast"],
+                    help="fast: FMA + composite Laplacian (round-off differences, parity "
+                         "within 1e-10); exact: bit-identical to the reference algorithm")
+    ap.add_argument("--no-exact", action="store_true", help="skip the exact-mode side run")
     ap.add_argument("--dist", action="store_true", help="slab-decomposed path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:

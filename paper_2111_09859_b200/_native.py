@@ -13,7 +13,10 @@ import os
 from . import errors
 
 LIB_NAME = "libwd_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# WD_B200_LIB selects another build of the same library (A/B timing of
+# kernel variants); default: the in-tree build.
+LIB_PATH = os.environ.get("WD_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # status codes / enums (walldist_b200.h)
 WD_OK = 0

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "wd_kernels.cuh"
+#include "wd_line_sweep.cuh"
 #include "wd_fused.cuh"
 
 using namespace wd;
@@ -330,11 +331,45 @@ Epi epi_metric(const wd_ctx* c, int l, int m, bool first, double* acc) {
 
 // D_axis(in) with `scheme` (central) -> out via epilogue.  scratch is
 // needed for compact schemes when the epilogue is not plain.
+// generic line solves: parallel right-hand sides + warp-per-32-lines
+// dgtsv recurrences (wd_line_sweep.cuh).  `scratch` holds rhs / y and must
+// not alias `in`; it may equal `out` when the output does not read `out`.
+bool line_solve_ok(int n) { return n >= 3 && line_solve_smem(n) <= kLineSolveMaxSmem; }
+void line_solve_prepare() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_line_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
+  cudaFuncSetAttribute(k_line_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
+  done = true;
+}
+template <int JOB>
+void launch_line_solve(const double* in, double* scratch, double* out, const Geom& g, int axis,
+                       int per, double off, int scheme, const TriDev& T, const Epi& e,
+                       const FilterCoef& fc, const uint8_t* pin, int use_geom_pin,
+                       const Status* st, cudaStream_t s) {
+  const int n = g.n[axis];
+  const long long L = g.N / n;
+  k_line_rhs<JOB><<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, scratch, g, axis, per, off,
+                                                                scheme, fc, st);
+  const long long warps = (L + 31) / 32;
+  const int blocks = (int)std::min<long long>((warps + LS_WARPS - 1) / LS_WARPS, 148LL * 8);
+  k_line_solve<JOB><<<blocks, LS_WARPS * 32, line_solve_smem(n), s>>>(
+      in, scratch, out, g, axis, T, e, pin, use_geom_pin, st);
+}
+
 void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int axis, int scheme,
                   Epi e, const Status* st) {
   const Geom& g = c->g;
   if (scheme == WD_C4 || scheme == WD_C6) {
     const long long L = g.N / g.n[axis];
+    double* ys = (e.mode == 0 && out != in) ? out : scratch;
+    if (line_solve_ok(g.n[axis]) && ys != in) {
+      launch_line_solve<0>(in, ys, out, g, axis, g.per[axis], 0.0, scheme, c->comp[axis], e,
+                           c->fcoef, nullptr, 0, st, c->stream);
+      return;
+    }
     double* scr = (e.mode == 0) ? out : scratch;
     k_deriv_compact<<<nblocks(L, kLineThreads), kLineThreads, 0, c->stream>>>(
         in, scr, out, g, axis, scheme, g.per[axis], 0.0, c->comp[axis], e, st);
@@ -482,8 +517,13 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
   for (int a = 0; a < g.nd; ++a) {
     double* nxt = bufs[a & 1];
     const long long L = g.N / g.n[a];
-    k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, c->stream>>>(
-        cur, nxt, g, a, g.per[a], c->fcoef, c->filt[a], nullptr, 1, st);
+    if (line_solve_ok(g.n[a])) {
+      launch_line_solve<1>(cur, nxt, nxt, g, a, g.per[a], 0.0, 0, c->filt[a], epi_plain(),
+                           c->fcoef, nullptr, 1, st, c->stream);
+    } else {
+      k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, c->stream>>>(
+          cur, nxt, g, a, g.per[a], c->fcoef, c->filt[a], nullptr, 1, st);
+    }
     cur = nxt;
   }
   k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
@@ -574,6 +614,7 @@ int wd_device_count(void) {
 }
 
 int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd_ctx** out) {
+  line_solve_prepare();
   if (!gd || !sd || !out) return fail(WD_ERR_INVALID, "null argument");
   int rc = validate(gd, sd);
   if (rc) return rc;
@@ -934,9 +975,14 @@ int wd_derivative(const double* in, double* out, int ndim, const int* dims, int 
     CK(cudaMemcpyAsync(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice,
                        s));
     const long long L = g.N / n;
-    k_deriv_compact<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(
-        in, out, out, g, axis, scheme, periodic, offset, factor_view(F, dev), epi_plain(),
-        nullptr);
+    line_solve_prepare();
+    if (line_solve_ok(n) && in != out)
+      launch_line_solve<0>(in, out, out, g, axis, periodic, offset, scheme, factor_view(F, dev),
+                           epi_plain(), FilterCoef{}, nullptr, 0, nullptr, s);
+    else
+      k_deriv_compact<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(
+          in, out, out, g, axis, scheme, periodic, offset, factor_view(F, dev), epi_plain(),
+          nullptr);
     CK(cudaFreeAsync(dev, s));
     CK(cudaStreamSynchronize(s));
   } else {
@@ -992,9 +1038,14 @@ int wd_filter(const double* in, double* out, const unsigned char* pinned, int nd
     T = factor_view(F, dev);
   }
   const long long L = g.N / n;
-  k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(in, out, g, axis, periodic,
-                                                               filter_coefs(alpha_f), T, pinned, 0,
-                                                               nullptr);
+  line_solve_prepare();
+  if (line_solve_ok(n))
+    launch_line_solve<1>(in, out, out, g, axis, periodic, 0.0, 0, T, epi_plain(),
+                         filter_coefs(alpha_f), pinned, 0, nullptr, s);
+  else
+    k_filter<<<nblocks(L, kLineThreads), kLineThreads, 0, s>>>(in, out, g, axis, periodic,
+                                                                 filter_coefs(alpha_f), T, pinned,
+                                                                 0, nullptr);
   CK(cudaGetLastError());
   if (dev) CK(cudaFreeAsync(dev, s));
   CK(cudaStreamSynchronize(s));
@@ -1005,8 +1056,8 @@ int wd_filter(const double* in, double* out, const unsigned char* pinned, int nd
 
 namespace {
 __global__ void k_tri_lines(double* x, Geom g, int axis, TriDev T) {
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   const long long L = g.N / n;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
        q += (long long)gridDim.x * blockDim.x)

@@ -18,6 +18,18 @@ namespace wd {
 
 constexpr int kMaxDim = 3;
 
+// Runtime-indexed read of a small kernel-parameter array as a select chain:
+// indexing a by-value struct member with a runtime index would copy the
+// whole struct to local memory (stack) in every thread.
+template <class T, int K>
+__device__ __forceinline__ T pick(const T (&a)[K], int i) {
+  T r = a[0];
+#pragma unroll
+  for (int k = 1; k < K; ++k)
+    if (i == k) r = a[k];
+  return r;
+}
+
 // Structured-grid geometry: C-order (n0, n1[, n2]); unused axes have n = 1.
 struct Geom {
   int nd;
@@ -36,7 +48,7 @@ struct Metric {
   long long N;
   int nd;
   __device__ __forceinline__ double get(int l, int mm, long long idx) const {
-    if (m == nullptr) return l == mm ? c[l] : 0.0;
+    if (m == nullptr) return l == mm ? pick(c, l) : 0.0;
     return m[(long long)(l * nd + mm) * N + idx];
   }
 };
@@ -151,12 +163,25 @@ __device__ __forceinline__ double d4_at(const L& w, int i, int n, int per) {
 // ---- boundary conditions (solver.py:87-110) as a source redirect:
 // after the reference's far-field copies, node x holds the pre-BC value of
 // src(x) (separable per axis); walls and the solid mask are then zeroed.
+// Index arithmetic: 32-bit unsigned division whenever every index fits
+// (N <= 2^32 - 1: every grid the generic path can hold), 64-bit otherwise;
+// a 64-bit division costs several times the 32-bit one.
+__device__ __forceinline__ int axis_coord(const Geom& g, long long idx, int a) {
+  const long long s = pick(g.s, a);
+  const int n = pick(g.n, a);
+  if (g.N <= 0xffffffffLL) return (int)(((unsigned)idx / (unsigned)s) % (unsigned)n);
+  return (int)((idx / s) % n);
+}
+
 __device__ __forceinline__ void node_coords(const Geom& g, long long idx, int c[kMaxDim]) {
-  for (int a = 0; a < kMaxDim; ++a) c[a] = (int)((idx / g.s[a]) % g.n[a]);
+#pragma unroll
+  for (int a = 0; a < kMaxDim; ++a) c[a] = axis_coord(g, idx, a);
 }
 
 __device__ __forceinline__ bool is_pinned(const Geom& g, long long idx, const int c[kMaxDim]) {
-  for (int a = 0; a < g.nd; ++a) {
+#pragma unroll
+  for (int a = 0; a < kMaxDim; ++a) {
+    if (a >= g.nd) break;
     if (c[a] == 0 && g.face[2 * a] == WD_FACE_WALL) return true;
     if (c[a] == g.n[a] - 1 && g.face[2 * a + 1] == WD_FACE_WALL) return true;
   }
@@ -166,7 +191,9 @@ __device__ __forceinline__ bool is_pinned(const Geom& g, long long idx, const in
 __device__ __forceinline__ long long bc_source(const Geom& g, long long idx,
                                                const int c[kMaxDim]) {
   long long src = idx;
-  for (int a = 0; a < g.nd; ++a) {
+#pragma unroll
+  for (int a = 0; a < kMaxDim; ++a) {
+    if (a >= g.nd) break;
     if (c[a] == 0 && g.face[2 * a] == WD_FACE_FARFIELD) src += g.s[a];
     if (c[a] == g.n[a] - 1 && g.face[2 * a + 1] == WD_FACE_FARFIELD) src -= g.s[a];
   }

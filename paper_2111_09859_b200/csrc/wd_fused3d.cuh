@@ -279,10 +279,14 @@ __global__ void __launch_bounds__(F3_TK* F3_TJ, 1) k_f3_stage(F3Args a, const in
       const double* row = Pb + (ty + F3_HP) * F3_PW + 3;  // row[t] <-> kg = k0 - 4 + t
       Ukb[ty * F3_UKW + tx] = a.c2 * central<R>(row[tx - 3], row[tx - 2], row[tx - 1],
                                                 row[tx + 1], row[tx + 2], row[tx + 3]);
-      if (tx < 2 * F3_HU) {
-        const int t = tx + F3_TK;
-        Ukb[ty * F3_UKW + t] = a.c2 * central<R>(row[t - 3], row[t - 2], row[t - 1], row[t + 1],
-                                                 row[t + 2], row[t + 3]);
+      {  // the 16 x 8 extra halo positions on 4 full warps (no 8-of-32 lanes)
+        const int L = ty * F3_TK + tx;
+        if (L < F3_TJ * 2 * F3_HU) {
+          const int rr = L / (2 * F3_HU), t = F3_TK + L % (2 * F3_HU);
+          const double* row2 = Pb + (rr + F3_HP) * F3_PW + 3;
+          Ukb[rr * F3_UKW + t] = a.c2 * central<R>(row2[t - 3], row2[t - 2], row2[t - 1],
+                                                   row2[t + 1], row2[t + 2], row2[t + 3]);
+        }
       }
       const int c = tx + 4;
       d2 = central<R>(row[c - 3], row[c - 2], row[c - 1], row[c + 1], row[c + 2], row[c + 3]);

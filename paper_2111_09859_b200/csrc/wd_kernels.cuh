@@ -46,6 +46,19 @@ struct Epi {
 
 __device__ __forceinline__ long long line_base(const Geom& g, int axis, long long q) {
   long long base = 0;
+  if (g.N <= 0xffffffffLL) {
+    unsigned u = (unsigned)q;
+#pragma unroll
+    for (int a = kMaxDim - 1; a >= 0; --a) {
+      if (a == axis) continue;
+      const unsigned n = (unsigned)g.n[a];
+      const unsigned qn = u / n;
+      base += (long long)(u - qn * n) * g.s[a];
+      u = qn;
+    }
+    return base;
+  }
+#pragma unroll
   for (int a = kMaxDim - 1; a >= 0; --a) {
     if (a == axis) continue;
     long long c = q % g.n[a];
@@ -100,11 +113,11 @@ __device__ __forceinline__ void tri_solve_line(double* __restrict__ x, long long
 static __global__ void k_deriv_explicit(const double* __restrict__ in, double* out, Geom g, int axis,
                                  int scheme, int per, double off, Epi epi, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)((idx / sa) % n);
+    const int i = axis_coord(g, idx, axis);
     Line w{in + (idx - (long long)i * sa), sa, n, per, off};
     out[idx] = epi.apply(deriv_explicit_at(w, i, n, scheme, per), idx);
   }
@@ -117,8 +130,8 @@ static __global__ void k_deriv_compact(const double* __restrict__ in, double* sc
                                 Geom g, int axis, int scheme, int per, double off, TriDev T,
                                 Epi epi, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   const long long L = g.N / n;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
        q += (long long)gridDim.x * blockDim.x) {
@@ -139,11 +152,11 @@ static __global__ void k_deriv_compact(const double* __restrict__ in, double* sc
 static __global__ void k_d4(const double* __restrict__ in, double* out, Geom g, int axis, int per,
                      Epi epi, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)((idx / sa) % n);
+    const int i = axis_coord(g, idx, axis);
     Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
     out[idx] = epi.apply(d4_at(w, i, n, per), idx);
   }
@@ -162,8 +175,8 @@ static __global__ void k_filter(const double* __restrict__ in, double* out, Geom
                          FilterCoef fc, TriDev T, const uint8_t* pin, int use_geom_pin,
                          const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   const long long L = g.N / n;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < L;
        q += (long long)gridDim.x * blockDim.x) {
@@ -216,11 +229,11 @@ __device__ __forceinline__ double sign1(double x) { return x >= 0.0 ? 1.0 : -1.0
 static __global__ void k_uw_bf(const double* __restrict__ in, double* Bo, double* Fo, double* dphi,
                         Geom g, int axis, int per, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = g.s[axis];
-  const int n = g.n[axis];
+  const long long sa = pick(g.s, axis);
+  const int n = pick(g.n, axis);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)((idx / sa) % n);
+    const int i = axis_coord(g, idx, axis);
     Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
     double B, F;
     if (per) {
@@ -254,17 +267,26 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     double d[kMaxDim], u[kMaxDim];
-    for (int l = 0; l < nd; ++l) d[l] = dphi.p[l][idx];
-    for (int m = 0; m < nd; ++m) {
+#pragma unroll
+    for (int l = 0; l < kMaxDim; ++l) d[l] = l < nd ? dphi.p[l][idx] : 0.0;
+#pragma unroll
+    for (int m = 0; m < kMaxDim; ++m) {
+      if (m >= nd) break;
       double s = M.get(0, m, idx) * d[0];
-      for (int l = 1; l < nd; ++l) s = s + M.get(l, m, idx) * d[l];
+#pragma unroll
+      for (int l = 1; l < kMaxDim; ++l)
+        if (l < nd) s = s + M.get(l, m, idx) * d[l];
       u[m] = s;
       U.p[m][idx] = s;
     }
     if (Uh.p[0] != nullptr)
-      for (int l = 0; l < nd; ++l) {
+#pragma unroll
+      for (int l = 0; l < kMaxDim; ++l) {
+        if (l >= nd) break;
         double s = M.get(l, 0, idx) * u[0];
-        for (int m = 1; m < nd; ++m) s = s + M.get(l, m, idx) * u[m];
+#pragma unroll
+        for (int m = 1; m < kMaxDim; ++m)
+          if (m < nd) s = s + M.get(l, m, idx) * u[m];
         Uh.p[l][idx] = s;
       }
   }
@@ -278,12 +300,16 @@ static __global__ void k_normal(Vec3 U, MVec3 nrm, long long N, int nd, double e
        idx += (long long)gridDim.x * blockDim.x) {
     double u[kMaxDim];
     double s = 0.0;
-    for (int m = 0; m < nd; ++m) {
+#pragma unroll
+    for (int m = 0; m < kMaxDim; ++m) {
+      if (m >= nd) break;
       u[m] = U.p[m][idx];
       s = m == 0 ? u[0] * u[0] : s + u[m] * u[m];
     }
     const double gm = sqrt(s);
-    for (int m = 0; m < nd; ++m) nrm.p[m][idx] = u[m] / (gm + eps0);
+#pragma unroll
+    for (int m = 0; m < kMaxDim; ++m)
+      if (m < nd) nrm.p[m][idx] = u[m] / (gm + eps0);
   }
 }
 
@@ -318,7 +344,9 @@ static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const 
       continue;
     }
     double adv = 0.0;
-    for (int l = 0; l < a.nd; ++l) {
+#pragma unroll
+    for (int l = 0; l < kMaxDim; ++l) {
+      if (l >= a.nd) break;
       const double uh = a.Uh.p[l][idx];
       double t;
       if (a.scheme == WD_UW) {
@@ -336,7 +364,9 @@ static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const 
       k[idx] = 1.0 + gam * a.lap[idx] - adv;
     } else {  // WD_HJ_CURVATURE
       double s = 0.0;
-      for (int m = 0; m < a.nd; ++m) {
+#pragma unroll
+      for (int m = 0; m < kMaxDim; ++m) {
+        if (m >= a.nd) break;
         const double u = a.U.p[m][idx];
         s = m == 0 ? u * u : s + u * u;
       }
@@ -373,7 +403,9 @@ static __global__ void k_timestep(DtArgs a, double* dt, long long N, const Statu
       continue;
     }
     double den = fabs(a.Uh.p[0][idx]);
-    for (int l = 1; l < a.nd; ++l) den = den + fabs(a.Uh.p[l][idx]);
+#pragma unroll
+    for (int l = 1; l < kMaxDim; ++l)
+      if (l < a.nd) den = den + fabs(a.Uh.p[l][idx]);
     if (a.kind == WD_HJ || a.kind == WD_HJ_CURVATURE)
       den = den + 2.0 * (a.eps * a.p[idx]) * sS;
     else if (a.kind == WD_HJ_LAD)
@@ -507,7 +539,9 @@ static __global__ void k_poisson_map(const double* __restrict__ pp, Vec3 U, doub
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     double gs = 0.0;
-    for (int m = 0; m < nd; ++m) {
+#pragma unroll
+    for (int m = 0; m < kMaxDim; ++m) {
+      if (m >= nd) break;
       const double u = U.p[m][idx];
       gs = m == 0 ? u * u : gs + u * u;
     }
