@@ -351,12 +351,13 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
                        const Status* st, cudaStream_t s) {
   const int n = g.n[axis];
   const long long L = g.N / n;
-  k_line_rhs<JOB><<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, scratch, g, axis, per, off,
+  k_line_rhs<JOB><<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, scratch, axis_geom(g, axis),
+                                                                per, off,
                                                                 scheme, fc, st);
   const long long warps = (L + 31) / 32;
   const int blocks = (int)std::min<long long>((warps + LS_WARPS - 1) / LS_WARPS, 148LL * 8);
   k_line_solve<JOB><<<blocks, LS_WARPS * 32, line_solve_smem(n), s>>>(
-      in, scratch, out, g, axis, T, e, pin, use_geom_pin, st);
+      in, scratch, out, g, axis, n, g.s[axis], T, e, pin, use_geom_pin, st);
 }
 
 void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int axis, int scheme,
@@ -375,7 +376,7 @@ void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int
         in, scr, out, g, axis, scheme, g.per[axis], 0.0, c->comp[axis], e, st);
   } else {
     k_deriv_explicit<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(
-        in, out, g, axis, scheme, g.per[axis], 0.0, e, st);
+        in, out, axis_geom(g, axis), scheme, g.per[axis], 0.0, e, st);
   }
 }
 
@@ -409,7 +410,8 @@ void launch_dphi(wd_ctx* c, const double* p, const Status* st) {
   for (int l = 0; l < c->g.nd; ++l) {
     if (c->sd.scheme == WD_UW)
       k_uw_bf<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(p, c->B[l], c->F[l],
-                                                                      c->dphi[l], c->g, l,
+                                                                      c->dphi[l],
+                                                                      axis_geom(c->g, l),
                                                                       c->g.per[l], st);
     else
       launch_deriv(c, p, c->dphi[l], c->tmp, l, c->sd.scheme, epi_plain(), st);
@@ -424,7 +426,7 @@ void launch_gamma_lad(wd_ctx* c, const double* p, const Status* st) {
     e.acc = c->tmp2;
     e.cfield = c->sums_dev ? c->sums_dev + (2 + l) * g.N : nullptr;
     e.cscal = c->sqrtS_c[l];
-    k_d4<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, g, l, g.per[l], e, st);
+    k_d4<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, axis_geom(g, l), g.per[l], e, st);
   }
   k_gamma_lad<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, c->gam, g.N,
                                                                    c->sd.epsilon, c->sd.lad_c, st);
@@ -986,7 +988,7 @@ int wd_derivative(const double* in, double* out, int ndim, const int* dims, int 
     CK(cudaFreeAsync(dev, s));
     CK(cudaStreamSynchronize(s));
   } else {
-    k_deriv_explicit<<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, out, g, axis, scheme,
+    k_deriv_explicit<<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, out, axis_geom(g, axis), scheme,
                                                                    periodic, offset, epi_plain(),
                                                                    nullptr);
   }
@@ -1004,7 +1006,7 @@ int wd_fourth_derivative(const double* in, double* out, int ndim, const int* dim
   int face[6] = {0, 0, 0, 0, 0, 0};
   if (periodic) face[2 * axis] = face[2 * axis + 1] = WD_FACE_PERIODIC;
   Geom g = make_geom(ndim, dims, face, nullptr);
-  k_d4<<<nblocks(g.N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(in, out, g, axis, periodic,
+  k_d4<<<nblocks(g.N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(in, out, axis_geom(g, axis), periodic,
                                                                        epi_plain(), nullptr);
   CK(cudaGetLastError());
   return WD_OK;

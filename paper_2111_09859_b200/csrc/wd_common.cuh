@@ -173,6 +173,20 @@ __device__ __forceinline__ int axis_coord(const Geom& g, long long idx, int a) {
   return (int)((idx / s) % n);
 }
 
+// One axis of a Geom as plain scalars (per-node kernels along an axis).
+struct AxisGeom {
+  long long N;   // total nodes
+  long long sa;  // stride of the axis
+  int n;         // length of the axis
+  __device__ __forceinline__ int coord(long long idx) const {
+    if (N <= 0xffffffffLL) return (int)(((unsigned)idx / (unsigned)sa) % (unsigned)n);
+    return (int)((idx / sa) % n);
+  }
+};
+__host__ __device__ __forceinline__ AxisGeom axis_geom(const Geom& g, int axis) {
+  return AxisGeom{g.N, g.s[axis], g.n[axis]};
+}
+
 __device__ __forceinline__ void node_coords(const Geom& g, long long idx, int c[kMaxDim]) {
 #pragma unroll
   for (int a = 0; a < kMaxDim; ++a) c[a] = axis_coord(g, idx, a);

@@ -131,6 +131,24 @@ __device__ __forceinline__ void sw_rows(const double* __restrict__ in, long long
   }
 }
 
+// L2 prefetch of rows [r0, r0+16) of the lane's line (in range only):
+// the sweep consumes each 16-row block right after loading it, so blocks
+// are prefetched SW_PF blocks ahead to keep HBM latency off the recurrence.
+constexpr int SW_PF = 2;
+template <bool CONTIG>
+__device__ __forceinline__ void sw_prefetch(const double* __restrict__ in, long long lbase,
+                                            long long rstride, int n, int r0) {
+  if (r0 < 0 || r0 + 16 > n) return;
+  const double* p = in + lbase + (long long)r0 * rstride;
+  if (CONTIG) {  // the lane's 16 rows are 128 contiguous bytes
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p + 15));
+  } else {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p + s * rstride));
+  }
+}
+
 template <bool CONTIG>
 __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
@@ -208,6 +226,7 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
       const int r0 = b * FB;
       {
         double v[16];
+        if (valid) sw_prefetch<CONTIG>(a.in, lbase, rstride, n, r0 + 5 + SW_PF * FB);
         sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, r0 + 5, T, lane, v);
 #pragma unroll
         for (int s = 0; s < 16; ++s) u[10 + s] = v[s];
@@ -251,6 +270,8 @@ __global__ void __launch_bounds__(128) k_filter_sweep(SweepArgs a) {
       const int r0 = b * FB;
       {
         double v[16];
+        if (valid) sw_prefetch<CONTIG>(a.in, lbase, rstride, n, r0 - 5 - SW_PF * FB);
+        if (valid && a.A) sw_prefetch<CONTIG>(a.A, lbase, rstride, n, r0 - SW_PF * FB);
         sw_rows<CONTIG>(a.in, lbase, gbase, rstride, lstride, nl, n, per, r0 - 5, T, lane, v);
 #pragma unroll
         for (int s = 0; s < 16; ++s) u[s] = v[s];

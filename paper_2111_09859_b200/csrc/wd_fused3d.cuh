@@ -583,6 +583,11 @@ __device__ __forceinline__ void stcs2(double* p, double x, double y) {
   __stcs(reinterpret_cast<double2*>(p), make_double2(x, y));
 }
 
+constexpr int F2_PF = 3;  // L2 prefetch distance (planes)
+__device__ __forceinline__ void l2_prefetch(const double* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p));
+}
+
 template <int R, bool EIK, int STAGE>
 __global__ void __launch_bounds__(256, 1) k_f3_fast2(F3Args a, const int* tiles) {
   if (a.st->state != WD_STATE_RUNNING) return;
@@ -649,6 +654,17 @@ __global__ void __launch_bounds__(256, 1) k_f3_fast2(F3Args a, const int* tiles)
       if (kh >= 0) nkh = ld2(a.p + pl + kh);
       npn = (a.per0 || inext < n0) ? ld2(a.p + (long long)inext * s0 + col)
                                    : make_double2(0.0, 0.0);
+    }
+    // L2 prefetch F2_PF planes ahead: the register prefetch above is only
+    // one plane deep, so without it the loads it issues see full HBM latency
+    if (i + F2_PF < i1) {
+      const long long pl = plane + F2_PF * s0;
+      l2_prefetch(a.A + pl + col);
+      if (STAGE > 1) l2_prefetch(a.dt + pl + col);
+      if (STAGE > 1) l2_prefetch(a.acc + pl + col);
+      int ip = inext + F2_PF - 1;
+      if (a.per0) ip = ip >= n0 ? ip - n0 : ip;
+      if (ip < n0) l2_prefetch(a.p + (long long)ip * s0 + col);
     }
     __syncthreads();
     // k row: values k-6 .. k+7 (cols 2tx+2 .. 2tx+15)

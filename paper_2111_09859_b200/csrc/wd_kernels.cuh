@@ -110,14 +110,14 @@ __device__ __forceinline__ void tri_solve_line(double* __restrict__ x, long long
 // ---------------------------------------------------------------- kernels
 
 // Explicit first derivative along `axis` (operators.py:109-128) + epilogue.
-static __global__ void k_deriv_explicit(const double* __restrict__ in, double* out, Geom g, int axis,
+static __global__ void k_deriv_explicit(const double* __restrict__ in, double* out, AxisGeom ag,
                                  int scheme, int per, double off, Epi epi, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = pick(g.s, axis);
-  const int n = pick(g.n, axis);
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+  const long long sa = ag.sa;
+  const int n = ag.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < ag.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = axis_coord(g, idx, axis);
+    const int i = ag.coord(idx);
     Line w{in + (idx - (long long)i * sa), sa, n, per, off};
     out[idx] = epi.apply(deriv_explicit_at(w, i, n, scheme, per), idx);
   }
@@ -149,14 +149,14 @@ static __global__ void k_deriv_compact(const double* __restrict__ in, double* sc
 }
 
 // 4th derivative (operators.py:236-250) + epilogue.
-static __global__ void k_d4(const double* __restrict__ in, double* out, Geom g, int axis, int per,
+static __global__ void k_d4(const double* __restrict__ in, double* out, AxisGeom ag, int per,
                      Epi epi, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = pick(g.s, axis);
-  const int n = pick(g.n, axis);
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+  const long long sa = ag.sa;
+  const int n = ag.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < ag.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = axis_coord(g, idx, axis);
+    const int i = ag.coord(idx);
     Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
     out[idx] = epi.apply(d4_at(w, i, n, per), idx);
   }
@@ -227,13 +227,13 @@ __device__ __forceinline__ double sign1(double x) { return x >= 0.0 ? 1.0 : -1.0
 // UW one-sided differences + front-selected derivative
 // (operators.py:151-193).
 static __global__ void k_uw_bf(const double* __restrict__ in, double* Bo, double* Fo, double* dphi,
-                        Geom g, int axis, int per, const Status* st) {
+                        AxisGeom ag, int per, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = pick(g.s, axis);
-  const int n = pick(g.n, axis);
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+  const long long sa = ag.sa;
+  const int n = ag.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < ag.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = axis_coord(g, idx, axis);
+    const int i = ag.coord(idx);
     Line w{in + (idx - (long long)i * sa), sa, n, per, 0.0};
     double B, F;
     if (per) {

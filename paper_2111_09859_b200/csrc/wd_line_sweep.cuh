@@ -41,15 +41,15 @@ __device__ __forceinline__ double ls_div(double s, double d, double r) {
 }
 
 template <int JOB>
-static __global__ void k_line_rhs(const double* __restrict__ in, double* __restrict__ rhs, Geom g,
-                                  int axis, int per, double off, int scheme, FilterCoef fc,
+static __global__ void k_line_rhs(const double* __restrict__ in, double* __restrict__ rhs,
+                                  AxisGeom ag, int per, double off, int scheme, FilterCoef fc,
                                   const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const long long sa = pick(g.s, axis);
-  const int n = pick(g.n, axis);
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+  const long long sa = ag.sa;
+  const int n = ag.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < ag.N;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = axis_coord(g, idx, axis);
+    const int i = ag.coord(idx);
     Line w{in + (idx - (long long)i * sa), sa, n, per, off};
     double r;
     if (JOB == 0) {
@@ -71,11 +71,12 @@ static __global__ void k_line_rhs(const double* __restrict__ in, double* __restr
 template <int JOB>
 static __global__ void __launch_bounds__(LS_WARPS * 32)
     k_line_solve(const double* __restrict__ in, double* y, double* out, Geom g, int axis,
-                 TriDev T, Epi epi, const uint8_t* pin, int use_geom_pin, const Status* st) {
+                 int n, long long sa, TriDev T, Epi epi, const uint8_t* pin, int use_geom_pin,
+                 const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  extern __shared__ double ls_f[];  // factor rows: fact, swap, du, du2, d, rinv, z, h
-  const int n = pick(g.n, axis);
-  const long long sa = pick(g.s, axis);
+  // factor rows: fact, swap, du, du2, d, rinv, z, h; then one flag per
+  // forward group (any row interchange in the group)
+  extern __shared__ double ls_f[];
   const long long L = g.N / n;
   double* sfact = ls_f;
   double* sswap = sfact + n;
@@ -94,6 +95,15 @@ static __global__ void __launch_bounds__(LS_WARPS * 32)
     srinv[t] = T.rinv[t];
     sz[t] = T.cyclic ? T.z[t] : 0.0;
     sh[t] = T.cyclic ? T.h[t] : 0.0;
+  }
+  int* gswap = reinterpret_cast<int*>(sh + n);
+  for (int k = threadIdx.x; k * LS_U < n; k += blockDim.x) {
+    int any = 0;
+    for (int s2 = 0; s2 < LS_U; ++s2) {
+      const int t = k * LS_U + s2;
+      if (t < n - 1 && T.swap[t] != 0.0) any = 1;
+    }
+    gswap[k] = any;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -131,6 +141,17 @@ static __global__ void __launch_bounds__(LS_WARPS * 32)
       for (int s = 0; s < LS_U; ++s) b[s] = yl[(long long)(k * LS_U + s + 1) * sa];
     };
     auto fproc = [&](int k, const double (&b)[LS_U]) {
+      if (!gswap[k]) {  // no interchange in this group (CTA-uniform branch)
+#pragma unroll
+        for (int s = 0; s < LS_U; ++s) {
+          const int i = k * LS_U + s;
+          const double yv = carry;
+          carry = b[s] - sfact[i] * carry;
+          if (T.cyclic) hs = hs + sh[i + 1] * b[s];
+          yl[(long long)i * sa] = yv;
+        }
+        return;
+      }
 #pragma unroll
       for (int s = 0; s < LS_U; ++s) {
         const int i = k * LS_U + s;
@@ -262,7 +283,9 @@ static __global__ void __launch_bounds__(LS_WARPS * 32)
   }
 }
 
-__host__ __forceinline__ size_t line_solve_smem(int n) { return (size_t)8 * n * sizeof(double); }
+__host__ __forceinline__ size_t line_solve_smem(int n) {
+  return (size_t)8 * n * sizeof(double) + (size_t)((n + LS_U - 1) / LS_U) * sizeof(int);
+}
 constexpr size_t kLineSolveMaxSmem = 200 * 1024;
 
 }  // namespace wd
