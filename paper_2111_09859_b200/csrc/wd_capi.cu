@@ -66,6 +66,8 @@ struct HostFactor {
   int cyclic = 0;
   std::vector<double> fact, d, du, du2, swap, z, h;
   double vn = 0.0, denom = 1.0;
+  int scan_m = 0;       // dist filters: scan-form tables appended at scan_off
+  size_t scan_off = 0;
 };
 
 int gtsv_factor(int n, const double* lower, const double* diag, const double* upper,
@@ -256,6 +258,46 @@ void factor_pack(const HostFactor& F, std::vector<double>& out) {
   put(7, F.h);
 }
 
+// Scan form of a swap-free factor for the fast filter (wd_filter_scan.cuh):
+// y_r = rhs_r - fm_r y_{r-1}, x_r = y_r rinv_r - g_r x_{r+1}; per segment of
+// m rows P_r = prod_{k=r0..r} (-fm_k), Q_r = prod_{k=r..r1-1} (-g_k).
+int scan_pack(const HostFactor& F, std::vector<double>& out, int& m) {
+  const int n = F.n;
+  if (n < 12 || n > FS_NMAX) return 0;
+  for (int i = 0; i < n; ++i)
+    if (F.swap[i] != 0.0) return 0;
+  m = (n + FS_S - 1) / FS_S;
+  // device layout: (fm, h)[n], (P, g)[n], (Q, z)[n] as double2, rinv[n]
+  std::vector<double> fm(n), P(n), ri(n), g(n), Q(n), z(n, 0.0), h(n, 0.0);
+  for (int r = 0; r < n; ++r) {
+    fm[r] = r > 0 ? F.fact[r - 1] : 0.0;
+    ri[r] = 1.0 / F.d[r];
+    g[r] = r < n - 1 ? F.du[r] * ri[r] : 0.0;
+    if (F.cyclic) {
+      z[r] = F.z[r];
+      h[r] = F.h[r];
+    }
+  }
+  for (int r0 = 0; r0 < n; r0 += m) {
+    const int r1 = std::min(n, r0 + m);
+    P[r0] = -fm[r0];
+    for (int r = r0 + 1; r < r1; ++r) P[r] = -fm[r] * P[r - 1];
+    Q[r1 - 1] = -g[r1 - 1];
+    for (int r = r1 - 2; r >= r0; --r) Q[r] = -g[r] * Q[r + 1];
+  }
+  out.assign((size_t)7 * n, 0.0);
+  for (int r = 0; r < n; ++r) {
+    out[2 * r] = fm[r];
+    out[2 * r + 1] = h[r];
+    out[2 * n + 2 * r] = P[r];
+    out[2 * n + 2 * r + 1] = g[r];
+    out[4 * n + 2 * r] = Q[r];
+    out[4 * n + 2 * r + 1] = z[r];
+    out[6 * n + r] = ri[r];
+  }
+  return 1;
+}
+
 Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) {
   Geom g;
   std::memset(&g, 0, sizeof(g));
@@ -285,6 +327,7 @@ struct wd_ctx {
   // factors
   HostFactor hcomp[3], hfilt[3];
   TriDev comp[3], filt[3];
+  ScanDev scan[3];
   double* factor_dev = nullptr;
   FilterCoef fcoef;
   // per-node metric sums (curvilinear) or scalars (uniform)
@@ -637,7 +680,8 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   }
   // factors
   std::vector<double> packed, all;
-  size_t off_comp[3] = {0, 0, 0}, off_filt[3] = {0, 0, 0};
+  size_t off_comp[3] = {0, 0, 0}, off_filt[3] = {0, 0, 0}, off_scan[3] = {0, 0, 0};
+  int scan_m[3] = {0, 0, 0};
   for (int a = 0; a < g.nd; ++a) {
     if (sd->scheme == WD_C4 || sd->scheme == WD_C6) {
       rc = compact_factor(sd->scheme, g.n[a], g.per[a], c->hcomp[a]);
@@ -658,6 +702,12 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
       factor_pack(c->hfilt[a], packed);
       off_filt[a] = all.size();
       all.insert(all.end(), packed.begin(), packed.end());
+      if (sd->arith == 1 && scan_pack(c->hfilt[a], packed, scan_m[a])) {
+        off_scan[a] = all.size();
+        all.insert(all.end(), packed.begin(), packed.end());
+      } else {
+        scan_m[a] = 0;
+      }
     }
   }
   if (c->sd.use_filter) c->fcoef = filter_coefs(sd->alpha_f);
@@ -671,6 +721,12 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
     for (int a = 0; a < g.nd; ++a) {
       if (c->hcomp[a].n) c->comp[a] = factor_view(c->hcomp[a], c->factor_dev + off_comp[a]);
       if (c->hfilt[a].n) c->filt[a] = factor_view(c->hfilt[a], c->factor_dev + off_filt[a]);
+      if (scan_m[a]) {
+        c->scan[a].n = c->hfilt[a].n;
+        c->scan[a].m = scan_m[a];
+        c->scan[a].tab = c->factor_dev + off_scan[a];
+        c->scan[a].denom = c->hfilt[a].cyclic ? c->hfilt[a].denom : 1.0;
+      }
     }
   }
   // workspace
@@ -742,6 +798,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
     fi.fcoef = c->fcoef;
     for (int a = 0; a < 3; ++a) {
       fi.filt[a] = c->filt[a];
+      fi.scan[a] = c->scan[a];
       fi.filt_swaps[a] = 0;
       for (double sw : c->hfilt[a].swap) fi.filt_swaps[a] |= sw != 0.0;
     }
@@ -1241,16 +1298,29 @@ int wd_dist_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, i
     if (rc) return rc;
     for (double sw : F.swap)
       if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
-    std::vector<double> packed;
+    std::vector<double> packed, sc;
     factor_pack(F, packed);
+    int m = 0;
+    const size_t nf = packed.size();
+    if (c->sd.arith == 1 && scan_pack(F, sc, m)) packed.insert(packed.end(), sc.begin(), sc.end());
     double* dev = nullptr;
     CK(cudaMalloc(&dev, packed.size() * sizeof(double)));
     CK(cudaMemcpy(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
     fused_filter_prepare(n);
+    F.scan_m = m;
+    F.scan_off = nf;
     it = c->dfilt.emplace(key, std::make_pair(F, dev)).first;
   }
   const TriDev T = factor_view(it->second.first, it->second.second);
-  fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream);
+  ScanDev SD;
+  if (it->second.first.scan_m) {
+    SD.n = n;
+    SD.m = it->second.first.scan_m;
+    SD.tab = it->second.second + it->second.first.scan_off;
+    SD.denom = it->second.first.cyclic ? it->second.first.denom : 1.0;
+  }
+  fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream,
+                   SD.n ? &SD : nullptr);
   CK(cudaGetLastError());
   return WD_OK;
 }

@@ -7,6 +7,7 @@
 #include "wd_fused.cuh"
 #include "wd_fused3d.cuh"
 #include "wd_filter_sweep.cuh"
+#include "wd_filter_scan.cuh"
 
 #include <vector>
 
@@ -71,6 +72,66 @@ void launch_sweep(const SweepArgs& w, cudaStream_t s) {
     k_filter_sweep<false><<<(int)ctas, 128, sweep_smem(w.n), s>>>(w);
 }
 
+// fast arithmetic: segmented-scan filter (wd_filter_scan.cuh), persistent
+// grid of resident CTAs
+int scan_ctas(int axis) {
+  static int ctas[2] = {0, 0};
+  const int k = axis == 2;
+  if (!ctas[k]) {
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t sm = scan_smem(FS_NMAX);
+    if (k) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<true, FS_M>, FS_T, sm);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<false, FS_M>, FS_T, sm);
+    ctas[k] = sms * (occ > 0 ? occ : 1);
+  }
+  return ctas[k];
+}
+
+bool scan_prepare() {
+  static int ok = -1;
+  if (ok < 0) {
+    const int sm = (int)scan_smem(FS_NMAX);
+    auto set = [&](const void* f) {
+      return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess;
+    };
+    ok = set((const void*)k_filter_scan<true, FS_M>) && set((const void*)k_filter_scan<false, FS_M>) &&
+         set((const void*)k_filter_scan<true, 0>) && set((const void*)k_filter_scan<false, 0>);
+  }
+  return ok == 1;
+}
+
+void launch_scan(const SweepArgs& w, const ScanDev& T, cudaStream_t s) {
+  ScanArgs a;
+  a.in = w.in;
+  a.out = w.out;
+  a.axis = w.axis;
+  a.n0 = w.n0;
+  a.n1 = w.n1;
+  a.n2 = w.n2;
+  a.s0 = w.s0;
+  a.per = w.per;
+  a.T = T;
+  a.fc = w.fc;
+  a.A = w.A;
+  a.st = w.st;
+  const long long inner = w.axis == 2 ? w.n1 : w.n2;
+  const long long outer = w.axis == 0 ? w.n1 : w.n0;
+  const long long groups = outer * ((inner + FS_L - 1) / FS_L);
+  long long ctas = scan_ctas(w.axis);
+  if (ctas > groups) ctas = groups;
+  const size_t sm = scan_smem(T.n);
+  const bool full = T.n == FS_S * FS_M;
+  if (w.axis == 2) {
+    if (full) k_filter_scan<true, FS_M><<<(int)ctas, FS_T, sm, s>>>(a);
+    else k_filter_scan<true, 0><<<(int)ctas, FS_T, sm, s>>>(a);
+  } else {
+    if (full) k_filter_scan<false, FS_M><<<(int)ctas, FS_T, sm, s>>>(a);
+    else k_filter_scan<false, 0><<<(int)ctas, FS_T, sm, s>>>(a);
+  }
+}
+
 void stage_dispatch(int R, bool eik, int stage, const F3Args& a, int blocks, const int* tiles,
                     bool fast, cudaStream_t s) {
   if (R == 1) eik ? launch_stage<1, true>(stage, a, blocks, tiles, fast, s) : launch_stage<1, false>(stage, a, blocks, tiles, fast, s);
@@ -106,6 +167,12 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   }
   fp.kind = PATH_F3;
   fp.active = 1;
+  fp.use_scan = 0;
+  if (sd.use_filter && sd.arith == 1 && scan_prepare()) {
+    fp.use_scan = 1;
+    for (int a = 0; a < 3; ++a)
+      if (in.scan[a].n != in.g.n[a]) fp.use_scan = 0;
+  }
   fp.n_fast = fp.n_exact = 0;
   if (sd.arith == 1) {
     // interior tiles (every stencil inside or periodic) -> fast kernel
@@ -274,7 +341,8 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     w.fc = in.fcoef;
     w.A = ax == 2 ? A : nullptr;
     w.st = st;
-    launch_sweep(w, s);
+    if (fp.use_scan) launch_scan(w, in.scan[ax], s);
+    else launch_sweep(w, s);
   } else if (kid == 8) {
     k_change<<<grid_blocks(g.N, 256), 256, 0, s>>>(B, A, nullptr, st, g.N);
   }
@@ -308,7 +376,7 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
 
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
                       int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
-                      cudaStream_t s) {
+                      cudaStream_t s, const ScanDev* scan) {
   SweepArgs w;
   w.in = in;
   w.out = out;
@@ -330,7 +398,8 @@ void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* o
   w.fc = fp.in.fcoef;
   w.A = A;
   w.st = st;
-  launch_sweep(w, s);
+  if (scan && scan->n == w.n && scan_prepare()) launch_scan(w, *scan, s);
+  else launch_sweep(w, s);
 }
 
 void fused_filter_prepare(int n) {

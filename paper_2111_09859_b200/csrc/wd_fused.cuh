@@ -8,6 +8,22 @@
 
 namespace wd {
 
+// Fast-arithmetic filter in scan form (wd_filter_scan.cuh): 16 lines per
+// CTA x 16 segments of <= 32 rows; 7 tables of n doubles per axis
+// (f_{r-1}, P, 1/d, du/d, Q, z, h).
+constexpr int FS_L = 16;
+constexpr int FS_S = 16;
+constexpr int FS_M = 32;
+constexpr int FS_T = FS_L * FS_S;
+constexpr int FS_NMAX = FS_S * FS_M;
+constexpr int FS_G = 5;
+
+struct ScanDev {
+  int n = 0, m = 0;
+  const double* tab = nullptr;
+  double denom = 1.0;
+};
+
 struct FusedInputs {
   const wd_grid_desc* gd;
   const wd_solver_desc* sd;
@@ -15,6 +31,7 @@ struct FusedInputs {
   Metric M;
   FilterCoef fcoef;
   TriDev filt[3];
+  ScanDev scan[3];  // n = 0: no scan form for this axis
   int filt_swaps[3];
   double sumS_c, cflms_c, lref;
   double* bufs[6];  // dt, acc, p, k, tmp, tmp2 (N each)
@@ -32,6 +49,7 @@ struct FusedPlan {
   cudaStream_t side = nullptr;  // boundary tiles overlap the interior launch
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int i_lo = 0, i_hi = 0;  // axis-0 plane range updated by the stages (0,0 = all)
+  int use_scan = 0;        // fast arithmetic: segmented-scan filter sweeps
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).
@@ -51,6 +69,6 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
 void fused_filter_prepare(int n);  // opt in to the sweep's shared memory for length n
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
                       int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
-                      cudaStream_t s);
+                      cudaStream_t s, const ScanDev* scan = nullptr);
 
 }  // namespace wd
