@@ -98,8 +98,10 @@ __device__ __forceinline__ double fs_rhsh(const double* w, int h, const double* 
   return v;
 }
 
-// MM > 0: every segment has exactly MM rows (n = 16 MM); MM = 0: any n <= 512
-template <bool AX2, int MM>
+// MM > 0: every segment has exactly MM rows (n = 16 MM); MM = 0: any n <= 512.
+// RED: fused convergence reduction against a.A (separate instantiation, so
+// the plain sweeps carry no predicated reduction code).
+template <bool AX2, int MM, bool RED>
 __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double fs_smem[];
@@ -154,10 +156,12 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
     const double* in = a.in + base;
     if (AX2) {
       // main rows: consecutive threads -> consecutive rows of one line
+      const double* src = in + tid;
+      double* dst = tile + FS_G + tid;
       for (int ll = 0; ll < nl; ++ll) {
-        const double* src = in + (long long)ll * lstride;
-        double* dst = tile + ll * LS + FS_G;
-        for (int r = tid; r < n; r += FS_T) cp_async8(dst + r, src + r, true);
+        for (int r = 0; r + tid < n; r += FS_T) cp_async8(dst + r, src + r, true);
+        src += lstride;
+        dst += LS;
       }
       if (tid < 2 * FS_G * FS_L) {  // ghosts: 10 rows x 16 lines
         const int ll = tid / (2 * FS_G), gq = tid - ll * 2 * FS_G;
@@ -169,24 +173,35 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
       const int c = tid & 7;  // line pair
       const int bytes = 2 * c < nl ? (2 * c + 1 < nl ? 16 : 8) : 0;
       const double* src = in + 2 * c;
-      double* dst = tile + FS_G * FS_L + 2 * c;
-      for (int r = tid >> 3; r < n; r += FS_T / 8)
-        cp_async16(dst + r * FS_L, src + (long long)r * rstride, bytes);
       if (tid < 2 * FS_G * 8) {
         const int gq = tid >> 3;
         const int rr = gq < FS_G ? gq : n + gq;
         const int r = per ? (gq < FS_G ? n - FS_G + gq : gq - FS_G) : 0;
         cp_async16(tile + rr * FS_L + 2 * c, src + (long long)r * rstride, per ? bytes : 0);
       }
+      const long long step = (FS_T / 8) * rstride;
+      src += (long long)(tid >> 3) * rstride;
+      double* dst = tile + (FS_G + (tid >> 3)) * FS_L + 2 * c;
+      for (int r = tid >> 3; r < n; r += FS_T / 8) {
+        cp_async16(dst, src, bytes);
+        src += step;
+        dst += (FS_T / 8) * FS_L;
+      }
     } else {
       const bool ok = l < nl;
       const double* src = in + l;
-      double* dst = tile + FS_G * FS_L + l;
-      for (int r = s; r < n; r += FS_S) cp_async8(dst + r * FS_L, src + (long long)r * rstride, ok);
       if (s < 2 * FS_G) {
         const int rr = s < FS_G ? s : n + s;
         const int r = per ? (s < FS_G ? n - FS_G + s : s - FS_G) : 0;
         cp_async8(tile + rr * FS_L + l, src + (long long)r * rstride, per && ok);
+      }
+      const long long step = FS_S * rstride;
+      src += (long long)s * rstride;
+      double* dst = tile + (FS_G + s) * FS_L + l;
+      for (int r = s; r < n; r += FS_S) {
+        cp_async8(dst, src, ok);
+        src += step;
+        dst += FS_S * FS_L;
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -306,28 +321,37 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
       return x;
     };
     // ---- 4. store (+ convergence reduction against A)
-    auto emit = [&](long long idx, double x) {
-      __stcs(a.out + idx, x);
-      if (a.A) {
+    auto emit = [&](double* po, const double* pa, double x) {
+      __stcs(po, x);
+      if (RED) {
         if (!isfinite(x)) bad = 1;
         ma = fmax(ma, fabs(x));
-        md = fmax(md, fabs(x - __ldcs(a.A + idx)));
+        md = fmax(md, fabs(x - __ldcs(pa)));
       }
     };
     if (!AX2) {
       if (l < nl) {
-        const long long b = base + l;
+        const long long b = base + l + (long long)r0 * rstride;
+        double* po = a.out + b;
+        const double* pa = RED ? a.A + b : nullptr;
         if constexpr (MM > 0) {
 #pragma unroll
           for (int rr = 0; rr < MM; ++rr) {
             const bool reg = rr < 5 || rr >= MM - 5;
             const int ri = rr < 5 ? rr : rr - MM + 10;
-            emit(b + (long long)(r0 + rr) * rstride, xfin(rr, reg ? yv[ri] : tl[rr * RS]));
+            emit(po, pa, xfin(rr, reg ? yv[ri] : tl[rr * RS]));
+            po += rstride;
+            if (RED) pa += rstride;
           }
         } else {
 #pragma unroll
-          for (int rr = 0; rr < FS_M; ++rr)
-            if (rr < cnt) emit(b + (long long)(r0 + rr) * rstride, xfin(rr, yv[rr]));
+          for (int rr = 0; rr < FS_M; ++rr) {
+            if (rr < cnt) {
+              emit(po, pa, xfin(rr, yv[rr]));
+              po += rstride;
+              if (RED) pa += rstride;
+            }
+          }
         }
       }
       if (MM == 0) {
@@ -352,9 +376,52 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
           if (rr < cnt) tl[rr] = xfin(rr, yv[rr]);
       }
       __syncthreads();
-      for (int ll = 0; ll < nl; ++ll) {
-        const long long b = base + (long long)ll * lstride;
-        for (int r = tid; r < n; r += FS_T) emit(b + r, tile[ll * LS + FS_G + r]);
+      {
+        double* po = a.out + base + tid;
+        const double* pa = RED ? a.A + base + tid : nullptr;
+        const double* pt = tile + FS_G + tid;
+        if (MM > 0 && !RED) {
+          for (int ll = 0; ll < nl; ++ll) {
+#pragma unroll
+            for (int r = 0; r < FS_S * MM; r += FS_T) __stcs(po + r, pt[r]);
+            po += lstride;
+            pt += LS;
+          }
+        } else if (MM > 0) {
+          // batches of 4 lines: 8 independent loads of A in flight per thread
+          for (int l0 = 0; l0 < nl; l0 += 4) {
+            constexpr int KK = MM > 0 ? FS_S * MM / FS_T : 1;
+            double av[4][KK];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int k = 0; k < KK; ++k)
+                av[u][k] = l0 + u < nl ? __ldcs(pa + u * lstride + k * FS_T) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (l0 + u < nl) {
+#pragma unroll
+                for (int k = 0; k < KK; ++k) {
+                  const double x = pt[u * LS + k * FS_T];
+                  __stcs(po + u * lstride + k * FS_T, x);
+                  if (!isfinite(x)) bad = 1;
+                  ma = fmax(ma, fabs(x));
+                  md = fmax(md, fabs(x - av[u][k]));
+                }
+              }
+            }
+            po += 4 * lstride;
+            pa += 4 * lstride;
+            pt += 4 * LS;
+          }
+        } else {
+          for (int ll = 0; ll < nl; ++ll) {
+            for (int r = 0; r + tid < n; r += FS_T) emit(po + r, pa + r, pt[r]);
+            po += lstride;
+            if (RED) pa += lstride;
+            pt += LS;
+          }
+        }
       }
       if (q + gridDim.x < groups) {
         __syncthreads();  // tile fully read before it is overwritten
@@ -363,7 +430,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
       }
     }
   }
-  if (a.A) {
+  if (RED) {
     md = warp_max(md);
     ma = warp_max(ma);
     bad = __any_sync(0xffffffffu, bad);

@@ -74,33 +74,30 @@ void launch_sweep(const SweepArgs& w, cudaStream_t s) {
 
 // fast arithmetic: segmented-scan filter (wd_filter_scan.cuh), persistent
 // grid of resident CTAs
-int scan_ctas(int axis) {
-  static int ctas[2] = {0, 0};
-  const int k = axis == 2;
-  if (!ctas[k]) {
+template <bool AX2, int MM, bool RED>
+void scan_one(const ScanArgs& a, long long groups, cudaStream_t s) {
+  static int ctas = 0;
+  const size_t smax = scan_smem(FS_NMAX);
+  if (!ctas) {
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t sm = scan_smem(FS_NMAX);
-    if (k) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<true, FS_M>, FS_T, sm);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<false, FS_M>, FS_T, sm);
-    ctas[k] = sms * (occ > 0 ? occ : 1);
+    cudaFuncSetAttribute(k_filter_scan<AX2, MM, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smax);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<AX2, MM, RED>, FS_T, smax);
+    ctas = sms * (occ > 0 ? occ : 1);
   }
-  return ctas[k];
+  const long long c = ctas < groups ? ctas : groups;
+  k_filter_scan<AX2, MM, RED><<<(int)c, FS_T, scan_smem(a.T.n), s>>>(a);
 }
 
-bool scan_prepare() {
-  static int ok = -1;
-  if (ok < 0) {
-    const int sm = (int)scan_smem(FS_NMAX);
-    auto set = [&](const void* f) {
-      return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess;
-    };
-    ok = set((const void*)k_filter_scan<true, FS_M>) && set((const void*)k_filter_scan<false, FS_M>) &&
-         set((const void*)k_filter_scan<true, 0>) && set((const void*)k_filter_scan<false, 0>);
-  }
-  return ok == 1;
+template <bool AX2, bool RED>
+void scan_mm(const ScanArgs& a, long long groups, cudaStream_t s) {
+  if (a.T.n == FS_S * FS_M) scan_one<AX2, FS_M, RED>(a, groups, s);
+  else scan_one<AX2, 0, RED>(a, groups, s);
 }
+
+bool scan_prepare() { return FS_NMAX > 0; }
 
 void launch_scan(const SweepArgs& w, const ScanDev& T, cudaStream_t s) {
   ScanArgs a;
@@ -119,16 +116,12 @@ void launch_scan(const SweepArgs& w, const ScanDev& T, cudaStream_t s) {
   const long long inner = w.axis == 2 ? w.n1 : w.n2;
   const long long outer = w.axis == 0 ? w.n1 : w.n0;
   const long long groups = outer * ((inner + FS_L - 1) / FS_L);
-  long long ctas = scan_ctas(w.axis);
-  if (ctas > groups) ctas = groups;
-  const size_t sm = scan_smem(T.n);
-  const bool full = T.n == FS_S * FS_M;
   if (w.axis == 2) {
-    if (full) k_filter_scan<true, FS_M><<<(int)ctas, FS_T, sm, s>>>(a);
-    else k_filter_scan<true, 0><<<(int)ctas, FS_T, sm, s>>>(a);
+    if (w.A) scan_mm<true, true>(a, groups, s);
+    else scan_mm<true, false>(a, groups, s);
   } else {
-    if (full) k_filter_scan<false, FS_M><<<(int)ctas, FS_T, sm, s>>>(a);
-    else k_filter_scan<false, 0><<<(int)ctas, FS_T, sm, s>>>(a);
+    if (w.A) scan_mm<false, true>(a, groups, s);
+    else scan_mm<false, false>(a, groups, s);
   }
 }
 
