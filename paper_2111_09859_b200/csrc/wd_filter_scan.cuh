@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
   const double2* T4 = T2 + n;
   const double* T3 = fs_smem + 6 * n;
   double* shc = fs_smem + 7 * n;  // FilterCoef (dynamic h: generic path)
-  double* tile = shc + 36;
+  double* tile = fs_smem + ((7 * n + 36 + 3) & ~3);  // 32-byte aligned (16-byte cp.async)
   const int NR = n + 2 * FS_G;
   const int LS = NR | 1;  // AX2 line stride (odd)
   const int tsz = AX2 ? FS_L * LS : NR * FS_L;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
 inline size_t scan_smem(int n) {
   const int NR = n + 2 * FS_G;
   const size_t tile = (size_t)FS_L * (size_t)(NR | 1);  // >= NR * FS_L
-  return (7 * (size_t)n + 36 + tile + 3 * FS_T) * sizeof(double);
+  return ((((size_t)7 * n + 36 + 3) & ~(size_t)3) + tile + 3 * FS_T) * sizeof(double);
 }
 
 }  // namespace wd

@@ -9,9 +9,16 @@
 #include "wd_filter_sweep.cuh"
 #include "wd_filter_scan.cuh"
 
+#include <cmath>
 #include <vector>
 
 namespace wd {
+
+// wd_stage_fast.cu
+template <bool EIK> bool fast3_prepare();
+template <bool EIK>
+void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s);
+int fast3_chunks(int ntiles, int ni);
 
 namespace {
 constexpr int PATH_F3 = 1;
@@ -160,6 +167,10 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
   }
   fp.kind = PATH_F3;
   fp.active = 1;
+  fp.use_fast3 = 0;
+  if (sd.arith == 1 && sd.scheme == WD_E6 && (in.g.n[2] % 2) == 0 &&
+      in.g.N < (1LL << 31) - (1LL << 24) && !getenv("WD_NO_FAST3"))
+    fp.use_fast3 = sd.kind == WD_EIKONAL ? fast3_prepare<true>() : fast3_prepare<false>();
   fp.use_scan = 0;
   if (sd.use_filter && sd.arith == 1 && scan_prepare()) {
     fp.use_scan = 1;
@@ -204,6 +215,11 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
 }
 
 namespace {
+// fast3 needs every updated plane 2R = 6 away from a non-periodic axis-0 end
+bool fast3_ok(const FusedPlan& fp, const F3Args& a) {
+  return fp.use_fast3 && (a.per0 || (a.i_lo >= 6 && a.i_hi <= a.n0 - 6));
+}
+
 F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
   const FusedInputs& in = fp.in;
   const wd_grid_desc& gd = *in.gd;
@@ -304,7 +320,15 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
       } else if (fp.n_exact) {
         stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
       }
-      if (fp.n_fast) stage_dispatch(R, eik, kid, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+      if (fp.n_fast) {
+        if (fast3_ok(fp, a)) {
+          const int c3 = fast3_chunks(fp.n_fast, a.i_hi - a.i_lo);
+          if (eik) launch_fast3<true>(kid, a, fp.n_fast, fp.fast_tiles, c3, s);
+          else launch_fast3<false>(kid, a, fp.n_fast, fp.fast_tiles, c3, s);
+        } else {
+          stage_dispatch(R, eik, kid, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+        }
+      }
       if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
     } else {
       stage_dispatch(R, eik, kid, a, chunks * all_tiles, nullptr, false, s);
@@ -360,7 +384,15 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
     } else if (fp.n_exact) {
       stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
     }
-    if (fp.n_fast) stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+    if (fp.n_fast) {
+      if (fast3_ok(fp, a)) {
+        const int c3 = fast3_chunks(fp.n_fast, a.i_hi - a.i_lo);
+        if (eik) launch_fast3<true>(stage, a, fp.n_fast, fp.fast_tiles, c3, s);
+        else launch_fast3<false>(stage, a, fp.n_fast, fp.fast_tiles, c3, s);
+      } else {
+        stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+      }
+    }
     if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
   } else {
     stage_dispatch(R, eik, stage, a, chunks * all_tiles, nullptr, false, s);

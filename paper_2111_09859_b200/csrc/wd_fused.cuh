@@ -50,6 +50,7 @@ struct FusedPlan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int i_lo = 0, i_hi = 0;  // axis-0 plane range updated by the stages (0,0 = all)
   int use_scan = 0;        // fast arithmetic: segmented-scan filter sweeps
+  int use_fast3 = 0;       // fast arithmetic, E6: cp.async-pipelined stage kernel
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).

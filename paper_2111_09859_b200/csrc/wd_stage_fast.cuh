@@ -1,0 +1,277 @@
+// Fast-arithmetic RK stage for interior tiles of the fused 3-D path
+// (SolveConfig.arith = "fast"; same discretisation as k_f3_stage /
+// formulations.py:135-197 + solver.py:160-205, round-off differences only).
+//
+// B200 data movement, one CTA = 32 (k) x 16 (j) column tile streaming along i:
+//   * every global -> shared transfer is cp.async (16 B, L2 only) in a
+//     3-slot ring, issued two planes ahead of the plane being computed, so
+//     no registers are spent on prefetch and HBM latency is covered by the
+//     ring depth rather than by occupancy;
+//   * per plane a slot holds the p tile with a 2R-row j halo and an 8-wide
+//     k halo (16-byte aligned), the pointwise fields A / dt / acc, and the
+//     interior of plane i + 2R + 1, the entry of the axis-0 register window;
+//   * the axis-0 window (13 pairs for E6) lives in registers and is indexed
+//     modulo its length inside a loop unrolled by that length, so it is
+//     never shifted (no register moves per plane);
+//   * each thread owns two adjacent k nodes: the k stencils of both come
+//     from 7 16-byte shared loads, the j stencils from 2R + 1.
+// Registers <= 128 with 256 threads -> two CTAs (16 warps) per SM.
+// Interior tiles only (no non-periodic k / j boundary inside the stencil
+// reach; tiles touching one run the exact kernel, wd_fused.cu) and planes
+// at least 2R from a non-periodic axis-0 end (periodic axis 0, or the
+// ghosted slabs of the decomposed solve); otherwise k_f3_fast2.
+#pragma once
+
+#include "wd_fused3d.cuh"
+
+namespace wd {
+
+constexpr int S3_TK = F3_TK;       // 32
+constexpr int S3_TJ = F3_TJ;       // 16
+constexpr int S3_PW = S3_TK + 16;  // 48 doubles per plane row (8-wide k halo)
+constexpr int S3_D = 2;            // planes in flight ahead of the computed one
+constexpr int S3_SLOTS = S3_D + 1;
+
+template <int R>
+struct S3Layout {
+  static constexpr int H = 2 * R;                   // composite half-width
+  static constexpr int PH = S3_TJ + 2 * H;          // plane rows
+  static constexpr int PLANE = PH * S3_PW;          // doubles per plane slot
+  static constexpr int PT = S3_TJ * S3_TK;          // 512 doubles per pointwise tile
+  static constexpr int SLOT = PLANE + 4 * PT;       // plane + A + dt + acc + window entry
+  static constexpr int CHUNKS = PH * (S3_PW / 2);   // 16-byte chunks of a plane slot
+  static constexpr int CPT = (CHUNKS + 255) / 256;  // chunks per thread
+  static constexpr size_t SMEM = (size_t)S3_SLOTS * SLOT * sizeof(double);
+};
+
+__device__ __forceinline__ void s3_cp16(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void s3_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void s3_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// fast correctly-rounded-to-a-few-ulp quotient a / b (MUFU seed + Newton)
+__device__ __forceinline__ double s3_div(double a, double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+
+template <int R, bool EIK, int STAGE>
+__global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles) {
+  using LY = S3Layout<R>;
+  constexpr int H = LY::H;
+  constexpr int NW = 2 * H + 1;
+  if (a.st->state != WD_STATE_RUNNING) return;
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // pair, row
+  const int ntile = tiles[0];
+  const int tile = tiles[1 + blockIdx.x % ntile];
+  const int chunk_id = blockIdx.x / ntile;
+  const int k0 = (tile % a.tiles_k) * S3_TK;
+  const int j0 = (tile / a.tiles_k) * S3_TJ;
+  const int i0 = a.i_lo + chunk_id * a.chunk;
+  const int i1 = min(i0 + a.chunk, a.i_hi);
+  if (i0 >= i1) return;
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const long long s0 = a.s0;
+  const int col = (j0 + ty) * n2 + k0 + 2 * tx;  // in-plane offset of the pair
+
+  // ---- per-thread copy assignments (fixed over the stream)
+  int coff[LY::CPT];  // in-plane source offset, -1 = zero fill, -2 = none
+  int cdst[LY::CPT];
+#pragma unroll
+  for (int q = 0; q < LY::CPT; ++q) {
+    const int c = tid + 256 * q;
+    coff[q] = -2;
+    cdst[q] = 0;
+    if (c < LY::CHUNKS) {
+      const int row = c / (S3_PW / 2), cc = c - row * (S3_PW / 2);
+      int jg = j0 - H + row, kg = k0 - 8 + 2 * cc;
+      bool ok = true;
+      if (a.per1) jg = wrapm(jg, n1);
+      else ok = ok && jg >= 0 && jg < n1;
+      if (a.per2) kg = wrapm(kg, n2);
+      else ok = ok && kg >= 0 && kg + 1 < n2;
+      coff[q] = ok ? jg * n2 + kg : -1;
+      cdst[q] = row * S3_PW + 2 * cc;
+    }
+  }
+  const int own = ty * S3_TK + 2 * tx;  // pointwise slot offset of the pair
+  // 32-bit element offsets (the plan guarantees N < 2^31)
+  const int is0 = (int)s0;
+  const int wrap0 = n0 * is0;
+  // loads of plane ip into slot `slot`; the axis-0 window entry is plane
+  // ip + H + 1 (periodic axis 0)
+  auto issue = [&](int ip, int slot) {
+    double* sl = smem + slot * LY::SLOT;
+    if (ip < i1) {
+      const int po = ip * is0;
+#pragma unroll
+      for (int q = 0; q < LY::CPT; ++q)
+        if (coff[q] != -2) s3_cp16(sl + cdst[q], a.p + (coff[q] >= 0 ? po + coff[q] : 0), coff[q] >= 0);
+      const int pl = po + col;
+      double* pt = sl + LY::PLANE + own;
+      s3_cp16(pt, a.A + pl, true);
+      if (STAGE > 1) {
+        s3_cp16(pt + LY::PT, a.dt + pl, true);
+        s3_cp16(pt + 2 * LY::PT, a.acc + pl, true);
+      }
+      int pw_off = pl + (H + 1) * is0;
+      bool wok = true;
+      if (pw_off >= wrap0) {
+        if (a.per0) pw_off -= wrap0;
+        else wok = false;  // beyond the last plane: never used, zero fill
+      }
+      s3_cp16(pt + 3 * LY::PT, a.p + (wok ? pw_off : 0), wok);
+    }
+    s3_commit();
+  };
+
+  // ---- prologue: axis-0 window p(i0-H .. i0+H), pipeline fill
+  double2 pw[NW];
+#pragma unroll
+  for (int s = 0; s < NW; ++s) {
+    int pos = i0 - H + s;
+    bool ok = true;
+    if (a.per0) pos = wrapm(pos, n0);
+    else ok = pos >= 0 && pos < n0;
+    pw[s] = ok ? *reinterpret_cast<const double2*>(a.p + (long long)pos * s0 + col)
+               : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int d = 0; d < S3_D; ++d) issue(i0 + d, d);
+
+  // slot of plane ib + u = (sb + u) mod SLOTS; NW = 13 = 1 (mod 3)
+  static_assert(S3_SLOTS == 3 && NW % 3 == 1, "slot rotation assumes 3 slots, NW = 1 mod 3");
+  int sb = 0;
+  for (int ib = i0; ib < i1; ib += NW) {
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      const int i = ib + u;
+      if (i < i1) {
+        int scur = sb + u % 3;
+        scur = scur >= 3 ? scur - 3 : scur;
+        int snext = scur + S3_D;
+        snext = snext >= 3 ? snext - 3 : snext;
+        s3_wait<S3_D - 1>();
+        __syncthreads();
+        issue(i + S3_D, snext);
+        const double* sl = smem + scur * LY::SLOT;
+        const double* pt = sl + LY::PLANE;
+        // k row of the pair: values k-H .. k+1+H  (cols 8-H+2tx .. 9+H+2tx)
+        const double* rowp = sl + (ty + H) * S3_PW + 2 * tx + 8 - H;
+        double rk[2 * H + 2];
+#pragma unroll
+        for (int q = 0; q < H + 1; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(rowp + 2 * q);
+          rk[2 * q] = v.x;
+          rk[2 * q + 1] = v.y;
+        }
+        // j column of the pair, accumulated over symmetric row pairs
+        const double* colp = sl + (ty + H) * S3_PW + 8 + 2 * tx;
+        double dj0, dj1, ddj0, ddj1;
+        {
+          const double2 c = *reinterpret_cast<const double2*>(colp);
+          ddj0 = a.e[0] * c.x;
+          ddj1 = a.e[0] * c.y;
+          dj0 = dj1 = 0.0;
+#pragma unroll
+          for (int m = 1; m <= H; ++m) {
+            const double2 lo = *reinterpret_cast<const double2*>(colp - m * S3_PW);
+            const double2 hi = *reinterpret_cast<const double2*>(colp + m * S3_PW);
+            ddj0 = fma(a.e[m], hi.x + lo.x, ddj0);
+            ddj1 = fma(a.e[m], hi.y + lo.y, ddj1);
+            if (m <= R) {
+              dj0 = fma(a.cr[m], hi.x - lo.x, dj0);
+              dj1 = fma(a.cr[m], hi.y - lo.y, dj1);
+            }
+          }
+        }
+        const double2 Av = *reinterpret_cast<const double2*>(pt + own);
+        double2 dtv2 = make_double2(0.0, 0.0), accv2 = make_double2(0.0, 0.0);
+        if (STAGE > 1) {
+          dtv2 = *reinterpret_cast<const double2*>(pt + LY::PT + own);
+          accv2 = *reinterpret_cast<const double2*>(pt + 2 * LY::PT + own);
+        }
+        double o[2], ac[2], dtn[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double* ck = rk + H + e;  // centre of node e
+          double d2 = a.cr[1] * (ck[1] - ck[-1]);
+          if (R >= 2) d2 = fma(a.cr[2], ck[2] - ck[-2], d2);
+          if (R >= 3) d2 = fma(a.cr[3], ck[3] - ck[-3], d2);
+          double dd2 = a.e[0] * ck[0];
+#pragma unroll
+          for (int m = 1; m <= H; ++m) dd2 = fma(a.e[m], ck[m] + ck[-m], dd2);
+          // axis 0 from the modular register window: p(i+m) = pw[(u+m+H) % NW]
+          auto w0 = [&](int m) -> double {
+            const double2 v = pw[(u + m + H + 2 * NW) % NW];
+            return e == 0 ? v.x : v.y;
+          };
+          double d0 = a.cr[1] * (w0(1) - w0(-1));
+          if (R >= 2) d0 = fma(a.cr[2], w0(2) - w0(-2), d0);
+          if (R >= 3) d0 = fma(a.cr[3], w0(3) - w0(-3), d0);
+          double dd0 = a.e[0] * w0(0);
+#pragma unroll
+          for (int m = 1; m <= H; ++m) dd0 = fma(a.e[m], w0(m) + w0(-m), dd0);
+          const double d1 = e == 0 ? dj0 : dj1;
+          const double dd1 = e == 0 ? ddj0 : ddj1;
+          const double pv = w0(0);
+          const double h0 = a.cc0 * d0, h1 = a.cc1 * d1, h2 = a.cc2 * d2;
+          double adv = h0 * d0;
+          adv = fma(h1, d1, adv);
+          adv = fma(h2, d2, adv);
+          double kv;
+          if (EIK) {
+            kv = 1.0 - adv;
+          } else {
+            double lap = a.cc0 * dd0;
+            lap = fma(a.cc1, dd1, lap);
+            lap = fma(a.cc2, dd2, lap);
+            kv = fma(a.eps * pv, lap, 1.0) - adv;
+          }
+          const double Ae = e == 0 ? Av.x : Av.y;
+          if (STAGE == 1) {
+            double den = fabs(h0) + fabs(h1) + fabs(h2);
+            if (!EIK) den = fma(2.0 * (a.eps * pv), a.sumS, den);
+            const double dtv = fmin(s3_div(a.cfl, den + 1e-30), a.cflms);
+            dtn[e] = dtv;
+            ac[e] = kv;
+            o[e] = fma(0.5 * dtv, kv, Ae);
+          } else if (STAGE == 2 || STAGE == 3) {
+            const double dte = e == 0 ? dtv2.x : dtv2.y;
+            const double acce = e == 0 ? accv2.x : accv2.y;
+            ac[e] = fma(2.0, kv, acce);
+            o[e] = fma(STAGE == 3 ? dte : 0.5 * dte, kv, Ae);
+          } else {
+            const double dte = e == 0 ? dtv2.x : dtv2.y;
+            const double acce = e == 0 ? accv2.x : accv2.y;
+            o[e] = fma(dte * (1.0 / 6.0), acce + kv, Ae);
+          }
+        }
+        const int idx = i * is0 + col;
+        if (STAGE == 1) __stcs(reinterpret_cast<double2*>(a.dt + idx), make_double2(dtn[0], dtn[1]));
+        if (STAGE <= 3) __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
+        __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
+        // window entry p(i + H + 1) replaces p(i - H)
+        pw[u] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
+      }
+    }
+    sb = sb + 1 == 3 ? 0 : sb + 1;
+  }
+  s3_wait<0>();
+}
+
+}  // namespace wd

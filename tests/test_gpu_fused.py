@@ -30,6 +30,9 @@ CASES = [
     ((19, 18, 33), (False, True, False), ("wall", None, "wall", "wall"), "hj", "E2", 0.48, 8),
     ((70, 11, 12), (False, False, True), ("wall", "wall", "wall", None), "eikonal", "E6", 0.49, 6),
     ((12, 40, 37), (True, True, False), (None, "wall"), "hj", "E4", None, 8),
+    # many interior tiles (fast mode: cp.async-pipelined k_f3_fast3, scan filter)
+    ((40, 64, 96), (True, False, True), ("wall", "wall"), "hj", "E6", 0.49, 6),
+    ((30, 56, 64), (True, False, True), ("wall", "wall"), "eikonal", "E6", 0.49, 5),
 ]
 
 
