@@ -17,7 +17,8 @@ namespace wd {
 // wd_stage_fast.cu
 template <bool EIK> bool fast3_prepare();
 template <bool EIK>
-void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s);
+void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s,
+                  bool jb);
 int fast3_chunks(int ntiles, int ni);
 
 namespace {
@@ -182,28 +183,37 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
     // interior tiles (every stencil inside or periodic) -> fast kernel
     const Geom& g = in.g;
     const int tk = (g.n[2] + F3_TK - 1) / F3_TK, tj = (g.n[1] + F3_TJ - 1) / F3_TJ;
-    std::vector<int> fastl(1, 0), exactl(1, 0);
+    // fast: every stencil inside or periodic; jb: k interior, touching a
+    // non-periodic j end (fast3 closure variant, else exact); exact: the rest
+    std::vector<int> fastl(1, 0), jbl(1, 0), exactl(1, 0);
     for (int t = 0; t < tk * tj; ++t) {
       const int k0 = (t % tk) * F3_TK, j0 = (t / tk) * F3_TJ;
       const bool kf = g.per[2] ? (k0 + F3_TK <= g.n[2]) : (k0 >= F3_HP && k0 + F3_TK + F3_HP <= g.n[2]);
       const bool jf = g.per[1] ? (j0 + F3_TJ <= g.n[1]) : (j0 >= F3_HP && j0 + F3_TJ + F3_HP <= g.n[1]);
-      (kf && jf ? fastl : exactl).push_back(t);
+      const bool jb = kf && !jf && !g.per[1] && j0 + F3_TJ <= g.n[1] && g.n[1] >= 2 * F3_TJ;
+      (kf && jf ? fastl : (jb ? jbl : exactl)).push_back(t);
     }
     fastl[0] = (int)fastl.size() - 1;
+    jbl[0] = (int)jbl.size() - 1;
     exactl[0] = (int)exactl.size() - 1;
     fp.n_fast = fastl[0];
+    fp.n_jb = jbl[0];
     fp.n_exact = exactl[0];
-    if (cudaMalloc(&fp.tiles_dev, (fastl.size() + exactl.size()) * sizeof(int)) != cudaSuccess ||
+    const size_t nt = fastl.size() + jbl.size() + exactl.size();
+    if (cudaMalloc(&fp.tiles_dev, nt * sizeof(int)) != cudaSuccess ||
         cudaMemcpy(fp.tiles_dev, fastl.data(), fastl.size() * sizeof(int),
                    cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(fp.tiles_dev + fastl.size(), exactl.data(), exactl.size() * sizeof(int),
-                   cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(fp.tiles_dev + fastl.size(), jbl.data(), jbl.size() * sizeof(int),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(fp.tiles_dev + fastl.size() + jbl.size(), exactl.data(),
+                   exactl.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
       fp.active = 0;
       return;
     }
     fp.fast_tiles = fp.tiles_dev;
-    fp.exact_tiles = fp.tiles_dev + fastl.size();
-    if (fp.n_exact && fp.n_fast) {
+    fp.jb_tiles = fp.tiles_dev + fastl.size();
+    fp.exact_tiles = fp.tiles_dev + fastl.size() + jbl.size();
+    if ((fp.n_exact || fp.n_jb) && fp.n_fast) {
       if (cudaStreamCreateWithFlags(&fp.side, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&fp.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&fp.ev_join, cudaEventDisableTiming) != cudaSuccess)
@@ -218,6 +228,41 @@ namespace {
 // fast3 needs every updated plane 2R = 6 away from a non-periodic axis-0 end
 bool fast3_ok(const FusedPlan& fp, const F3Args& a) {
   return fp.use_fast3 && (a.per0 || (a.i_lo >= 6 && a.i_hi <= a.n0 - 6));
+}
+
+// One RK stage over the tile lists of a fast-arithmetic plan: boundary
+// tiles (exact kernel, or the fast3 j-wall variant) on the forked side
+// stream so they overlap the interior tiles on `s`.
+void stage_tiles(const FusedPlan& fp, int stage, const F3Args& a, int chunks, int R, bool eik,
+                 cudaStream_t s) {
+  const bool f3 = fast3_ok(fp, a);
+  const bool side = fp.side != nullptr;
+  const cudaStream_t ss = side ? fp.side : s;
+  const bool any_side = fp.n_exact || fp.n_jb;
+  if (any_side && side) {
+    cudaEventRecord(fp.ev_fork, s);
+    cudaStreamWaitEvent(fp.side, fp.ev_fork, 0);
+  }
+  const int c3 = f3 ? fast3_chunks(fp.n_fast + fp.n_jb, a.i_hi - a.i_lo) : 0;
+  if (fp.n_jb) {
+    if (f3) {
+      if (eik) launch_fast3<true>(stage, a, fp.n_jb, fp.jb_tiles, c3, ss, true);
+      else launch_fast3<false>(stage, a, fp.n_jb, fp.jb_tiles, c3, ss, true);
+    } else {
+      stage_dispatch(R, eik, stage, a, chunks * fp.n_jb, fp.jb_tiles, false, ss);
+    }
+  }
+  if (fp.n_exact) stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, ss);
+  if (any_side && side) cudaEventRecord(fp.ev_join, fp.side);
+  if (fp.n_fast) {
+    if (f3) {
+      if (eik) launch_fast3<true>(stage, a, fp.n_fast, fp.fast_tiles, c3, s, false);
+      else launch_fast3<false>(stage, a, fp.n_fast, fp.fast_tiles, c3, s, false);
+    } else {
+      stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
+    }
+  }
+  if (any_side && side) cudaStreamWaitEvent(s, fp.ev_join, 0);
 }
 
 F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
@@ -283,6 +328,14 @@ F3Args f3_args(const FusedPlan& fp, const double* A, Status* st, int* blocks) {
   a.cc0 = a.c0 * a.c0;
   a.cc1 = a.c1 * a.c1;
   a.cc2 = a.c2 * a.c2;
+  const double cc[3] = {a.cc0, a.cc1, a.cc2};
+  a.fE0 = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    a.fsq[l] = std::sqrt(cc[l]);
+    for (int m = 0; m < 4; ++m) a.fC[l][m] = a.fsq[l] * c[m];
+    for (int m = 0; m < 7; ++m) a.fE[l][m] = cc[l] * e[m];
+    a.fE0 += cc[l] * e[0];
+  }
   return a;
 }
 }  // namespace
@@ -310,26 +363,7 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
   }
   if (kid >= 1 && kid <= 4) {
     if (fp.fast_tiles) {
-      // boundary tiles (exact kernel) on a forked stream so they overlap the
-      // interior tiles instead of running as a thin serial tail
-      if (fp.n_exact && fp.side) {
-        cudaEventRecord(fp.ev_fork, s);
-        cudaStreamWaitEvent(fp.side, fp.ev_fork, 0);
-        stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, fp.side);
-        cudaEventRecord(fp.ev_join, fp.side);
-      } else if (fp.n_exact) {
-        stage_dispatch(R, eik, kid, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
-      }
-      if (fp.n_fast) {
-        if (fast3_ok(fp, a)) {
-          const int c3 = fast3_chunks(fp.n_fast, a.i_hi - a.i_lo);
-          if (eik) launch_fast3<true>(kid, a, fp.n_fast, fp.fast_tiles, c3, s);
-          else launch_fast3<false>(kid, a, fp.n_fast, fp.fast_tiles, c3, s);
-        } else {
-          stage_dispatch(R, eik, kid, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
-        }
-      }
-      if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
+      stage_tiles(fp, kid, a, chunks, R, eik, s);
     } else {
       stage_dispatch(R, eik, kid, a, chunks * all_tiles, nullptr, false, s);
     }
@@ -376,24 +410,7 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
   a.p = p;
   a.out = out;
   if (fp.fast_tiles) {
-    if (fp.n_exact && fp.side) {
-      cudaEventRecord(fp.ev_fork, s);
-      cudaStreamWaitEvent(fp.side, fp.ev_fork, 0);
-      stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, fp.side);
-      cudaEventRecord(fp.ev_join, fp.side);
-    } else if (fp.n_exact) {
-      stage_dispatch(R, eik, stage, a, chunks * fp.n_exact, fp.exact_tiles, false, s);
-    }
-    if (fp.n_fast) {
-      if (fast3_ok(fp, a)) {
-        const int c3 = fast3_chunks(fp.n_fast, a.i_hi - a.i_lo);
-        if (eik) launch_fast3<true>(stage, a, fp.n_fast, fp.fast_tiles, c3, s);
-        else launch_fast3<false>(stage, a, fp.n_fast, fp.fast_tiles, c3, s);
-      } else {
-        stage_dispatch(R, eik, stage, a, chunks * fp.n_fast, fp.fast_tiles, true, s);
-      }
-    }
-    if (fp.n_exact && fp.side) cudaStreamWaitEvent(s, fp.ev_join, 0);
+    stage_tiles(fp, stage, a, chunks, R, eik, s);
   } else {
     stage_dispatch(R, eik, stage, a, chunks * all_tiles, nullptr, false, s);
   }

@@ -45,7 +45,8 @@ struct FusedPlan {
   int* tiles_dev = nullptr;
   const int* fast_tiles = nullptr;
   const int* exact_tiles = nullptr;
-  int n_fast = 0, n_exact = 0;
+  const int* jb_tiles = nullptr;  // k interior, touching a j wall
+  int n_fast = 0, n_exact = 0, n_jb = 0;
   cudaStream_t side = nullptr;  // boundary tiles overlap the interior launch
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int i_lo = 0, i_hi = 0;  // axis-0 plane range updated by the stages (0,0 = all)

@@ -51,6 +51,12 @@ struct F3Args {
   double cr[4];
   double e[7];
   double cc0, cc1, cc2;
+  // fast3 folded coefficients: D_l = sum_m fC[l][m] (p_m - p_-m) = sqrt(cc_l) d_l,
+  // lap = fE0 p_0 + sum_l sum_m fE[l][m] (p_m + p_-m), adv = sum_l D_l^2
+  double fC[3][4];
+  double fE[3][7];
+  double fE0;
+  double fsq[3];
 };
 
 template <int R>

@@ -1,6 +1,7 @@
 // Fast-arithmetic E6 stage kernels (wd_stage_fast.cuh) in their own
 // translation unit: launch helpers used by wd_fused.cu.
 #include <cmath>
+#include <vector>
 
 #include "wd_stage_fast.cuh"
 
@@ -8,27 +9,78 @@ namespace wd {
 
 // fast interior tiles, E6: cp.async-pipelined stage (wd_stage_fast.cuh) with
 // its own i-chunking (grid a multiple of the resident CTA slots)
+// Closure rows of the E6 j derivative (wd_common.cuh:deriv_explicit_at,
+// unit spacing) as a matrix D on a line of n = 24; G = D rows, M = D D.
+// Rows 0-5 (low wall, columns from row 0) and n-6..n-1 (high wall, columns
+// from row n-12) -> c_jbG / c_jbM.
+static bool jb_tables() {
+  const int n = 24;
+  std::vector<double> D(n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double* r = &D[i * n];
+    if (i < 2 || i > n - 3) {
+      // e4_closure rows (wd_common.cuh) expressed on unit vectors
+      if (i == 0) { r[0] = -25.0 / 12; r[1] = 48.0 / 12; r[2] = -36.0 / 12; r[3] = 16.0 / 12; r[4] = -3.0 / 12; }
+      if (i == 1) { r[0] = -3.0 / 12; r[1] = -10.0 / 12; r[2] = 18.0 / 12; r[3] = -6.0 / 12; r[4] = 1.0 / 12; }
+      if (i == n - 1) { r[n - 1] = 25.0 / 12; r[n - 2] = -48.0 / 12; r[n - 3] = 36.0 / 12; r[n - 4] = -16.0 / 12; r[n - 5] = 3.0 / 12; }
+      if (i == n - 2) { r[n - 1] = 3.0 / 12; r[n - 2] = 10.0 / 12; r[n - 3] = -18.0 / 12; r[n - 4] = 6.0 / 12; r[n - 5] = -1.0 / 12; }
+    } else if (i == 2 || i == n - 3) {
+      r[i + 1] += E4_CA; r[i - 1] -= E4_CA; r[i + 2] += E4_CB; r[i - 2] -= E4_CB;
+    } else {
+      r[i + 1] += E6_CA; r[i - 1] -= E6_CA; r[i + 2] += E6_CB; r[i - 2] -= E6_CB;
+      r[i + 3] += E6_CC; r[i - 3] -= E6_CC;
+    }
+  }
+  double G[12][12] = {}, M[12][12] = {};
+  for (int t = 0; t < 12; ++t) {
+    const int i = t < 6 ? t : n - 12 + t;  // t >= 6: row n-6+(t-6)
+    const int base = t < 6 ? 0 : n - 12;
+    for (int q = 0; q < 12; ++q) {
+      G[t][q] = D[i * n + base + q];
+      double m = 0.0;
+      for (int k = 0; k < n; ++k) m += D[i * n + k] * D[k * n + base + q];
+      M[t][q] = m;
+    }
+  }
+  return cudaMemcpyToSymbol(c_jbG, G, sizeof(G)) == cudaSuccess &&
+         cudaMemcpyToSymbol(c_jbM, M, sizeof(M)) == cudaSuccess;
+}
+
 template <bool EIK>
 bool fast3_prepare() {
+  static const bool tables = jb_tables();
+  if (!tables) return false;
   const int sm = (int)S3Layout<3>::SMEM;
   auto set = [&](const void* f) {
     return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess;
   };
-  return set((const void*)k_f3_fast3<3, EIK, 1>) && set((const void*)k_f3_fast3<3, EIK, 2>) &&
-         set((const void*)k_f3_fast3<3, EIK, 3>) && set((const void*)k_f3_fast3<3, EIK, 4>);
+  return set((const void*)k_f3_fast3<3, EIK, 1, false>) && set((const void*)k_f3_fast3<3, EIK, 2, false>) &&
+         set((const void*)k_f3_fast3<3, EIK, 3, false>) && set((const void*)k_f3_fast3<3, EIK, 4, false>) &&
+         set((const void*)k_f3_fast3<3, EIK, 1, true>) && set((const void*)k_f3_fast3<3, EIK, 2, true>) &&
+         set((const void*)k_f3_fast3<3, EIK, 3, true>) && set((const void*)k_f3_fast3<3, EIK, 4, true>);
 }
 
 template <bool EIK>
-void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s) {
+void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s,
+                  bool jb) {
   const int ni = a.i_hi - a.i_lo;
   a.chunk = (ni + chunks - 1) / chunks;
   const int blocks = chunks * ntiles;
   const size_t sm = S3Layout<3>::SMEM;
+  if (jb) {
+    switch (stage) {
+      case 1: k_f3_fast3<3, EIK, 1, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+      case 2: k_f3_fast3<3, EIK, 2, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+      case 3: k_f3_fast3<3, EIK, 3, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+      default: k_f3_fast3<3, EIK, 4, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+    }
+    return;
+  }
   switch (stage) {
-    case 1: k_f3_fast3<3, EIK, 1><<<blocks, 256, sm, s>>>(a, tiles); break;
-    case 2: k_f3_fast3<3, EIK, 2><<<blocks, 256, sm, s>>>(a, tiles); break;
-    case 3: k_f3_fast3<3, EIK, 3><<<blocks, 256, sm, s>>>(a, tiles); break;
-    default: k_f3_fast3<3, EIK, 4><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 1: k_f3_fast3<3, EIK, 1, false><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 2: k_f3_fast3<3, EIK, 2, false><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 3: k_f3_fast3<3, EIK, 3, false><<<blocks, 256, sm, s>>>(a, tiles); break;
+    default: k_f3_fast3<3, EIK, 4, false><<<blocks, 256, sm, s>>>(a, tiles); break;
   }
 }
 
@@ -56,7 +108,7 @@ int fast3_chunks(int ntiles, int ni) {
 
 template bool fast3_prepare<true>();
 template bool fast3_prepare<false>();
-template void launch_fast3<true>(int, F3Args, int, const int*, int, cudaStream_t);
-template void launch_fast3<false>(int, F3Args, int, const int*, int, cudaStream_t);
+template void launch_fast3<true>(int, F3Args, int, const int*, int, cudaStream_t, bool);
+template void launch_fast3<false>(int, F3Args, int, const int*, int, cudaStream_t, bool);
 
 }  // namespace wd

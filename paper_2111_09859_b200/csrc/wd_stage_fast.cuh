@@ -29,7 +29,14 @@ namespace wd {
 constexpr int S3_TK = F3_TK;       // 32
 constexpr int S3_TJ = F3_TJ;       // 16
 constexpr int S3_PW = S3_TK + 16;  // 48 doubles per plane row (8-wide k halo)
-constexpr int S3_D = 2;            // planes in flight ahead of the computed one
+#ifndef WD_S3_D
+#define WD_S3_D 2
+#endif
+#ifndef WD_S3_PF
+#define WD_S3_PF 0
+#endif
+constexpr int S3_D = WD_S3_D;      // planes in flight ahead of the computed one
+constexpr int S3_PF = WD_S3_PF;    // extra planes of L2 prefetch beyond the ring (0: off)
 constexpr int S3_SLOTS = S3_D + 1;
 
 template <int R>
@@ -67,7 +74,18 @@ __device__ __forceinline__ double s3_div(double a, double b) {
   return fma(fma(-b, q, a), r, q);
 }
 
-template <int R, bool EIK, int STAGE>
+// JB: tiles touching a non-periodic j end (walls).  Rows 0..5 / n1-6..n1-1
+// see the E4/E6 closures (wd_common.cuh:deriv_explicit_at) inside the reach
+// of D_j o D_j; there the j part is the closure-aware composite: the first
+// derivative G p and the two-pass Laplacian M p = D (D p) as 12-point rows
+// precomputed on the host (c_jbG, c_jbM: same discretisation as the exact
+// kernel's U_j = c_1 D_j p, D_j U_j), wall rows pinned; other rows and the
+// k / i parts stay composite.  No exact-kernel CTA shares the SMs (C4: the
+// 2 of 32 j tile rows at y = 0, 1).
+__constant__ double c_jbG[12][12];  // rows 0-5: low wall, 6-11: high wall (cols from base)
+__constant__ double c_jbM[12][12];
+
+template <int R, bool EIK, int STAGE, bool JB>
 __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles) {
   using LY = S3Layout<R>;
   constexpr int H = LY::H;
@@ -123,8 +141,8 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         if (coff[q] != -2) s3_cp16(sl + cdst[q], a.p + (coff[q] >= 0 ? po + coff[q] : 0), coff[q] >= 0);
       const int pl = po + col;
       double* pt = sl + LY::PLANE + own;
-      s3_cp16(pt, a.A + pl, true);
-      if (STAGE > 1) {
+      if (STAGE > 1) {  // stage 1: A = p, read from the plane tile
+        s3_cp16(pt, a.A + pl, true);
         s3_cp16(pt + LY::PT, a.dt + pl, true);
         s3_cp16(pt + 2 * LY::PT, a.acc + pl, true);
       }
@@ -135,6 +153,18 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         else wok = false;  // beyond the last plane: never used, zero fill
       }
       s3_cp16(pt + 3 * LY::PT, a.p + (wok ? pw_off : 0), wok);
+      if (S3_PF > 0 && (tx & 7) == 0 && ip + S3_PF < i1) {  // one line per 8 pairs
+        const int pf = pl + S3_PF * is0;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.p + pf));
+        if (STAGE > 1) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + pf));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.dt + pf));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.acc + pf));
+        }
+        int pwf = pw_off + S3_PF * is0;
+        if (pwf >= wrap0) pwf -= wrap0;
+        if (a.per0 || pw_off + S3_PF * is0 < wrap0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.p + pwf));
+      }
     }
     s3_commit();
   };
@@ -153,18 +183,18 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
 #pragma unroll
   for (int d = 0; d < S3_D; ++d) issue(i0 + d, d);
 
-  // slot of plane ib + u = (sb + u) mod SLOTS; NW = 13 = 1 (mod 3)
-  static_assert(S3_SLOTS == 3 && NW % 3 == 1, "slot rotation assumes 3 slots, NW = 1 mod 3");
+  // slot of plane ib + u = (sb + u) mod SLOTS; NW = 13 = 1 (mod SLOTS)
+  static_assert(NW % S3_SLOTS == 1, "slot rotation assumes NW = 1 mod SLOTS");
   int sb = 0;
   for (int ib = i0; ib < i1; ib += NW) {
 #pragma unroll
     for (int u = 0; u < NW; ++u) {
       const int i = ib + u;
       if (i < i1) {
-        int scur = sb + u % 3;
-        scur = scur >= 3 ? scur - 3 : scur;
+        int scur = sb + u % S3_SLOTS;
+        scur = scur >= S3_SLOTS ? scur - S3_SLOTS : scur;
         int snext = scur + S3_D;
-        snext = snext >= 3 ? snext - 3 : snext;
+        snext = snext >= S3_SLOTS ? snext - S3_SLOTS : snext;
         s3_wait<S3_D - 1>();
         __syncthreads();
         issue(i + S3_D, snext);
@@ -181,25 +211,50 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         }
         // j column of the pair, accumulated over symmetric row pairs
         const double* colp = sl + (ty + H) * S3_PW + 8 + 2 * tx;
-        double dj0, dj1, ddj0, ddj1;
-        {
+        double Dj0 = 0.0, Dj1 = 0.0, Lj0 = 0.0, Lj1 = 0.0;
+        bool jwall = false, pin = false;
+        if (JB) {
+          const int j = j0 + ty;
+          const int t = j < 6 ? j : (j >= n1 - 6 ? 6 + j - (n1 - 6) : -1);
+          if (t >= 0) {  // closure rows: 12-point rows from the table
+            jwall = true;
+            pin = (j == 0 && a.wall[2]) || (j == n1 - 1 && a.wall[3]);
+            const int base = t < 6 ? 0 : n1 - 12;  // global row of column 0
+            const double* cb = sl + (base - (j0 - H)) * S3_PW + 8 + 2 * tx;
+            double g0 = 0.0, g1 = 0.0, m0 = 0.0, m1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < 12; ++q) {
+              const double2 v = *reinterpret_cast<const double2*>(cb + q * S3_PW);
+              const double G = c_jbG[t][q], M = c_jbM[t][q];
+              g0 = fma(G, v.x, g0);
+              g1 = fma(G, v.y, g1);
+              m0 = fma(M, v.x, m0);
+              m1 = fma(M, v.y, m1);
+            }
+            Dj0 = a.fsq[1] * g0;
+            Dj1 = a.fsq[1] * g1;
+            Lj0 = a.cc1 * m0;
+            Lj1 = a.cc1 * m1;
+          }
+        }
+        if (!jwall) {
           const double2 c = *reinterpret_cast<const double2*>(colp);
-          ddj0 = a.e[0] * c.x;
-          ddj1 = a.e[0] * c.y;
-          dj0 = dj1 = 0.0;
+          Lj0 = a.fE[1][0] * c.x;
+          Lj1 = a.fE[1][0] * c.y;
 #pragma unroll
           for (int m = 1; m <= H; ++m) {
             const double2 lo = *reinterpret_cast<const double2*>(colp - m * S3_PW);
             const double2 hi = *reinterpret_cast<const double2*>(colp + m * S3_PW);
-            ddj0 = fma(a.e[m], hi.x + lo.x, ddj0);
-            ddj1 = fma(a.e[m], hi.y + lo.y, ddj1);
+            Lj0 = fma(a.fE[1][m], hi.x + lo.x, Lj0);
+            Lj1 = fma(a.fE[1][m], hi.y + lo.y, Lj1);
             if (m <= R) {
-              dj0 = fma(a.cr[m], hi.x - lo.x, dj0);
-              dj1 = fma(a.cr[m], hi.y - lo.y, dj1);
+              Dj0 = fma(a.fC[1][m], hi.x - lo.x, Dj0);
+              Dj1 = fma(a.fC[1][m], hi.y - lo.y, Dj1);
             }
           }
         }
-        const double2 Av = *reinterpret_cast<const double2*>(pt + own);
+        const double2 Av = STAGE == 1 ? *reinterpret_cast<const double2*>(colp)
+                                      : *reinterpret_cast<const double2*>(pt + own);
         double2 dtv2 = make_double2(0.0, 0.0), accv2 = make_double2(0.0, 0.0);
         if (STAGE > 1) {
           dtv2 = *reinterpret_cast<const double2*>(pt + LY::PT + own);
@@ -209,56 +264,54 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double* ck = rk + H + e;  // centre of node e
-          double d2 = a.cr[1] * (ck[1] - ck[-1]);
-          if (R >= 2) d2 = fma(a.cr[2], ck[2] - ck[-2], d2);
-          if (R >= 3) d2 = fma(a.cr[3], ck[3] - ck[-3], d2);
-          double dd2 = a.e[0] * ck[0];
-#pragma unroll
-          for (int m = 1; m <= H; ++m) dd2 = fma(a.e[m], ck[m] + ck[-m], dd2);
           // axis 0 from the modular register window: p(i+m) = pw[(u+m+H) % NW]
           auto w0 = [&](int m) -> double {
             const double2 v = pw[(u + m + H + 2 * NW) % NW];
             return e == 0 ? v.x : v.y;
           };
-          double d0 = a.cr[1] * (w0(1) - w0(-1));
-          if (R >= 2) d0 = fma(a.cr[2], w0(2) - w0(-2), d0);
-          if (R >= 3) d0 = fma(a.cr[3], w0(3) - w0(-3), d0);
-          double dd0 = a.e[0] * w0(0);
+          double Dk = a.fC[2][1] * (ck[1] - ck[-1]);
+          double Di = a.fC[0][1] * (w0(1) - w0(-1));
 #pragma unroll
-          for (int m = 1; m <= H; ++m) dd0 = fma(a.e[m], w0(m) + w0(-m), dd0);
-          const double d1 = e == 0 ? dj0 : dj1;
-          const double dd1 = e == 0 ? ddj0 : ddj1;
+          for (int m = 2; m <= R; ++m) {
+            Dk = fma(a.fC[2][m], ck[m] - ck[-m], Dk);
+            Di = fma(a.fC[0][m], w0(m) - w0(-m), Di);
+          }
           const double pv = w0(0);
-          const double h0 = a.cc0 * d0, h1 = a.cc1 * d1, h2 = a.cc2 * d2;
-          double adv = h0 * d0;
-          adv = fma(h1, d1, adv);
-          adv = fma(h2, d2, adv);
+          const double Dj = e == 0 ? Dj0 : Dj1;
+          double adv = Di * Di;
+          adv = fma(Dj, Dj, adv);
+          adv = fma(Dk, Dk, adv);
           double kv;
           if (EIK) {
             kv = 1.0 - adv;
           } else {
-            double lap = a.cc0 * dd0;
-            lap = fma(a.cc1, dd1, lap);
-            lap = fma(a.cc2, dd2, lap);
+            double lap = fma(a.fE0 - a.fE[1][0], pv, e == 0 ? Lj0 : Lj1);  // j's p_0 term is in Lj
+#pragma unroll
+            for (int m = 1; m <= H; ++m) {
+              lap = fma(a.fE[2][m], ck[m] + ck[-m], lap);
+              lap = fma(a.fE[0][m], w0(m) + w0(-m), lap);
+            }
             kv = fma(a.eps * pv, lap, 1.0) - adv;
           }
           const double Ae = e == 0 ? Av.x : Av.y;
           if (STAGE == 1) {
-            double den = fabs(h0) + fabs(h1) + fabs(h2);
+            double den = a.fsq[0] * fabs(Di);
+            den = fma(a.fsq[1], fabs(Dj), den);
+            den = fma(a.fsq[2], fabs(Dk), den);
             if (!EIK) den = fma(2.0 * (a.eps * pv), a.sumS, den);
             const double dtv = fmin(s3_div(a.cfl, den + 1e-30), a.cflms);
             dtn[e] = dtv;
             ac[e] = kv;
-            o[e] = fma(0.5 * dtv, kv, Ae);
+            o[e] = pin ? 0.0 : fma(0.5 * dtv, kv, Ae);
           } else if (STAGE == 2 || STAGE == 3) {
             const double dte = e == 0 ? dtv2.x : dtv2.y;
             const double acce = e == 0 ? accv2.x : accv2.y;
             ac[e] = fma(2.0, kv, acce);
-            o[e] = fma(STAGE == 3 ? dte : 0.5 * dte, kv, Ae);
+            o[e] = pin ? 0.0 : fma(STAGE == 3 ? dte : 0.5 * dte, kv, Ae);
           } else {
             const double dte = e == 0 ? dtv2.x : dtv2.y;
             const double acce = e == 0 ? accv2.x : accv2.y;
-            o[e] = fma(dte * (1.0 / 6.0), acce + kv, Ae);
+            o[e] = pin ? 0.0 : fma(dte * (1.0 / 6.0), acce + kv, Ae);
           }
         }
         const int idx = i * is0 + col;
@@ -269,7 +322,7 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         pw[u] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
       }
     }
-    sb = sb + 1 == 3 ? 0 : sb + 1;
+    sb = sb + 1 == S3_SLOTS ? 0 : sb + 1;
   }
   s3_wait<0>();
 }
