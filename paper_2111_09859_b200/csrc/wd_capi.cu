@@ -335,6 +335,7 @@ struct wd_ctx {
   double sumS_c = 0, cflms_c = 0, sqrtS_c[3] = {0, 0, 0};
   // workspace
   double* ws = nullptr;
+  double* ws_generic = nullptr;  // lazily allocated (ensure_generic)
   double *p, *k, *acc, *dt, *lap, *tmp, *tmp2, *gam, *phiY;
   double *dphi[3], *U[3], *Uh[3], *nrm[3], *B[3], *F[3], *Ue[3];
   Status* st = nullptr;
@@ -593,6 +594,37 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st) {
   }
 }
 
+// Generic-path workspace (24 fields), allocated the first time a generic
+// kernel sequence is enqueued; the fused path never needs it.
+int ensure_generic(wd_ctx* c) {
+  if (c->ws_generic) return WD_OK;
+  const long long N = c->g.N;
+  if (cudaMalloc(&c->ws_generic, (size_t)24 * N * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(WD_ERR_CUDA, "generic workspace allocation failed (" +
+                                 std::to_string(24.0 * N * 8 / 1e9) + " GB)");
+  }
+  double* w = c->ws_generic;
+  auto take = [&]() {
+    double* r = w;
+    w += N;
+    return r;
+  };
+  c->lap = take();
+  c->gam = take();
+  take();
+  for (int a = 0; a < 3; ++a) {
+    c->dphi[a] = take();
+    c->U[a] = take();
+    c->Uh[a] = take();
+    c->nrm[a] = take();
+    c->B[a] = take();
+    c->F[a] = take();
+    c->Ue[a] = take();
+  }
+  return WD_OK;
+}
+
 void enqueue_step(wd_ctx* c, const double* A, double* B) {
   if (c->fused.active) {
     fused_step(c->fused, A, B, c->st, c->hist, c->stream);
@@ -729,37 +761,23 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
       }
     }
   }
-  // workspace
-  const int nfields = 10 + 7 * 3;
-  if (cudaMalloc(&c->ws, (size_t)nfields * g.N * sizeof(double)) != cudaSuccess) {
+  // workspace: the 7 fields every path uses; the generic path's 24 more
+  // (derivatives, U, U_hat, ...) are allocated on first use (ensure_generic)
+  const int ncore = 7;
+  if (cudaMalloc(&c->ws, (size_t)ncore * g.N * sizeof(double)) != cudaSuccess) {
     wd_destroy(c);
     return fail(WD_ERR_CUDA, "workspace allocation failed (" +
-                                 std::to_string((double)nfields * g.N * 8 / 1e9) + " GB)");
+                                 std::to_string((double)ncore * g.N * 8 / 1e9) + " GB)");
   }
-  double* w = c->ws;
-  auto take = [&]() {
-    double* r = w;
-    w += g.N;
-    return r;
-  };
-  c->p = take();
-  c->k = take();
-  c->acc = take();
-  c->dt = take();
-  c->lap = take();
-  c->tmp = take();
-  c->tmp2 = take();
-  c->gam = take();
-  c->phiY = take();
-  take();
-  for (int a = 0; a < 3; ++a) {
-    c->dphi[a] = take();
-    c->U[a] = take();
-    c->Uh[a] = take();
-    c->nrm[a] = take();
-    c->B[a] = take();
-    c->F[a] = take();
-    c->Ue[a] = take();
+  {
+    double* w = c->ws;
+    c->p = w;
+    c->k = w + g.N;
+    c->acc = w + 2 * g.N;
+    c->dt = w + 3 * g.N;
+    c->tmp = w + 4 * g.N;
+    c->tmp2 = w + 5 * g.N;
+    c->phiY = w + 6 * g.N;
   }
   if (cudaMalloc(&c->st, 2 * sizeof(Status)) != cudaSuccess ||
       cudaMalloc(&c->hist_scratch, 8 * sizeof(double)) != cudaSuccess ||
@@ -830,6 +848,7 @@ int wd_destroy(wd_ctx* c) {
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
   cudaFree(c->ws);
+  cudaFree(c->ws_generic);
   cudaFree(c->st);
   cudaFree(c->hist_scratch);
   cudaFree(c->flag_dev);
@@ -862,6 +881,10 @@ int wd_bind(wd_ctx* c, double* phi, double* hist) {
 int wd_steps(wd_ctx* c, int k) {
   if (!c || !c->phi) return fail(WD_ERR_INVALID, "context not bound");
   if (k <= 0) return WD_OK;
+  if (!c->fused.active) {
+    const int rc = ensure_generic(c);
+    if (rc) return rc;
+  }
   const int parity = (int)(c->enq & 1);
   auto key = std::make_pair(k, parity);
   auto it = c->graphs.find(key);
@@ -942,6 +965,7 @@ int wd_time_kernel(wd_ctx* c, int kid, int reps, double* avg_ms) {
 
 int wd_tendency(wd_ctx* c, const double* phi, double* k) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  if (const int rc = ensure_generic(c)) return rc;
   CK(cudaDeviceSynchronize());
   enqueue_tendency(c, phi, k, nullptr);
   CK(cudaGetLastError());
@@ -951,6 +975,7 @@ int wd_tendency(wd_ctx* c, const double* phi, double* k) {
 
 int wd_local_timestep(wd_ctx* c, const double* phi, double* dt) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  if (const int rc = ensure_generic(c)) return rc;
   CK(cudaDeviceSynchronize());
   enqueue_timestep(c, phi, dt, nullptr);
   CK(cudaGetLastError());
@@ -969,6 +994,7 @@ int wd_apply_bc(wd_ctx* c, double* phi) {
 
 int wd_rk4_step(wd_ctx* c, const double* phi, const double* dt, double* out, int* diverged) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  if (const int rc = ensure_generic(c)) return rc;
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpyAsync(c->dt, dt, c->g.N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   enqueue_rk4(c, phi, out, nullptr);
@@ -988,6 +1014,7 @@ int wd_rk4_step(wd_ctx* c, const double* phi, const double* dt, double* out, int
 
 int wd_poisson_post(wd_ctx* c, const double* pp, double* phi) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
+  if (const int rc = ensure_generic(c)) return rc;
   CK(cudaDeviceSynchronize());
   const Geom& g = c->g;
   const int csch = c->sd.scheme == WD_UW ? WD_E2 : c->sd.scheme;

@@ -91,13 +91,15 @@ int fast3_chunks(int ntiles, int ni) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const double slots = 2.0 * sms;
+  // time ~ waves x (chunk length + window prologue, a 13-plane read worth
+  // about 3 computed planes); more chunks = shorter tail, more re-reads
   int best = 1;
   double bc = 1e30;
   for (int c = 1; c <= 32; ++c) {
     const int len = (ni + c - 1) / c;
     if (len < 16 && c > 1) break;
-    const double waves = ntiles * (double)c / slots;
-    const double cost = std::ceil(waves) / c * (len + 12.0);
+    const double waves = std::ceil(ntiles * (double)c / slots);
+    const double cost = waves * (len + 3.0);
     if (cost < bc - 1e-9) {
       bc = cost;
       best = c;

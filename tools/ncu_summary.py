@@ -17,8 +17,8 @@ import subprocess
 import sys
 from collections import OrderedDict, defaultdict
 
-BENCH_NAMES = [("k_f3_fast2", "stage"), ("k_f3_fast", "stage"), ("k_f3_stage", "stage"),
-               ("k_filter_sweep", "filter")]
+BENCH_NAMES = [("k_f3_fast3", "stage"), ("k_f3_fast2", "stage"), ("k_f3_fast", "stage"),
+               ("k_f3_stage", "stage"), ("k_filter_sweep", "filter"), ("k_filter_scan", "filter")]
 
 
 def short(name):
@@ -116,14 +116,14 @@ def full(rep, out, traffic_path=None):
                                                   "Gbyte": 1e9}.get(units[hdr.index("dram__bytes_read.sum")], 1)
             wr = g(r, "dram__bytes_write.sum") * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
                                                    "Gbyte": 1e9}.get(units[hdr.index("dram__bytes_write.sum")], 1)
-            m = re.search(r"<(\d+), (\d+), (\d+)>", r[hdr.index("Kernel Name")])
+            m = re.search(r"<(\d+), (\d+), (\d+)", r[hdr.index("Kernel Name")])
             order.append((name, int(m.group(3)) if m and name.startswith("k_f3") else None, rd + wr))
         out_t = defaultdict(float)
         fi = 0
         for name, stage, b in order:
             if stage is not None:
                 out_t[f"stage{stage}"] += b
-            elif name.startswith("k_filter_sweep"):
+            elif name.startswith("k_filter_sweep") or name.startswith("k_filter_scan"):
                 out_t[f"filter_axis{fi}"] = b
                 fi += 1
         json.dump(dict(out_t), open(traffic_path, "w"), indent=1)
