@@ -9,10 +9,11 @@
 //     ring depth rather than by occupancy;
 //   * per plane a slot holds the p tile with a 2R-row j halo and an 8-wide
 //     k halo (16-byte aligned), the pointwise fields A / dt / acc, and the
-//     interior of plane i + 2R + 1, the entry of the axis-0 register window;
-//   * the axis-0 window (13 pairs for E6) lives in registers and is indexed
-//     modulo its length inside a loop unrolled by that length, so it is
-//     never shifted (no register moves per plane);
+//     interior of plane i + 2R, the entry of the axis-0 register windows;
+//   * axis 0 runs as the two-pass D_0 (D_0 p) in registers: a p window
+//     p(i .. i+2R) and a u = sqrt(cc_0) D_0 p window u(i-R .. i+R) (7 pairs
+//     each for E6), indexed modulo 2R+1 inside a loop unrolled by 2R+1, so
+//     they are never shifted (no register moves per plane);
 //   * each thread owns two adjacent k nodes: the k stencils of both come
 //     from 7 16-byte shared loads, the j stencils from 2R + 1.
 // Registers <= 128 with 256 threads -> two CTAs (16 warps) per SM.
@@ -89,7 +90,7 @@ template <int R, bool EIK, int STAGE, bool JB>
 __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles) {
   using LY = S3Layout<R>;
   constexpr int H = LY::H;
-  constexpr int NW = 2 * H + 1;
+  constexpr int NW = H + 1;  // axis-0 windows: p(i .. i+2R), u(i-R .. i+R)
   if (a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double smem[];
   const int tid = threadIdx.x;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         s3_cp16(pt + LY::PT, a.dt + pl, true);
         s3_cp16(pt + 2 * LY::PT, a.acc + pl, true);
       }
-      int pw_off = pl + (H + 1) * is0;
+      int pw_off = pl + H * is0;  // window entry p(ip + 2R)
       bool wok = true;
       if (pw_off >= wrap0) {
         if (a.per0) pw_off -= wrap0;
@@ -169,21 +170,42 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
     s3_commit();
   };
 
-  // ---- prologue: axis-0 window p(i0-H .. i0+H), pipeline fill
-  double2 pw[NW];
+  // ---- prologue: axis 0 runs as two passes in registers (same
+  // discretisation as the composite D o D): u = sqrt(cc_0) D_0 p on a
+  // window u(i-R .. i+R), p on p(i .. i+2R); both indexed modulo NW = 2R+1
+  // inside a loop unrolled by NW, so neither is ever shifted.
+  double2 pw[NW], uw[NW];
+  {
+    double2 pp[2 * H];  // p(i0-H .. i0+H-1)
 #pragma unroll
-  for (int s = 0; s < NW; ++s) {
-    int pos = i0 - H + s;
-    bool ok = true;
-    if (a.per0) pos = wrapm(pos, n0);
-    else ok = pos >= 0 && pos < n0;
-    pw[s] = ok ? *reinterpret_cast<const double2*>(a.p + (long long)pos * s0 + col)
-               : make_double2(0.0, 0.0);
+    for (int s = 0; s < 2 * H; ++s) {
+      int pos = i0 - H + s;
+      bool ok = true;
+      if (a.per0) pos = wrapm(pos, n0);
+      else ok = pos >= 0 && pos < n0;
+      pp[s] = ok ? *reinterpret_cast<const double2*>(a.p + (long long)pos * s0 + col)
+                 : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < H; ++s) pw[s] = pp[H + s];  // p(i0 + s) at slot s
+#pragma unroll
+    for (int s = 0; s < H; ++s) {  // u(i0 - R + s) at slot s, from p(i0-H+s .. i0+s)
+      const int c = R + s;            // pp index of the centre i0 - R + s
+      double2 v;
+      v.x = a.fC[0][1] * (pp[c + 1].x - pp[c - 1].x);
+      v.y = a.fC[0][1] * (pp[c + 1].y - pp[c - 1].y);
+#pragma unroll
+      for (int m = 2; m <= R; ++m) {
+        v.x = fma(a.fC[0][m], pp[c + m].x - pp[c - m].x, v.x);
+        v.y = fma(a.fC[0][m], pp[c + m].y - pp[c - m].y, v.y);
+      }
+      uw[s] = v;
+    }
   }
 #pragma unroll
   for (int d = 0; d < S3_D; ++d) issue(i0 + d, d);
 
-  // slot of plane ib + u = (sb + u) mod SLOTS; NW = 13 = 1 (mod SLOTS)
+  // slot of plane ib + u = (sb + u) mod SLOTS; NW = 7 = 1 (mod SLOTS)
   static_assert(NW % S3_SLOTS == 1, "slot rotation assumes NW = 1 mod SLOTS");
   int sb = 0;
   for (int ib = i0; ib < i1; ib += NW) {
@@ -200,6 +222,20 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         issue(i + S3_D, snext);
         const double* sl = smem + scur * LY::SLOT;
         const double* pt = sl + LY::PLANE;
+        // window entry p(i + 2R) replaces p(i - 1); u(i + R) replaces u(i - R - 1)
+        pw[(u + H) % NW] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
+        {
+          auto P = [&](int m) -> const double2& { return pw[(u + m + 2 * NW) % NW]; };  // p(i+m)
+          double2 v;
+          v.x = a.fC[0][1] * (P(R + 1).x - P(R - 1).x);
+          v.y = a.fC[0][1] * (P(R + 1).y - P(R - 1).y);
+#pragma unroll
+          for (int m = 2; m <= R; ++m) {
+            v.x = fma(a.fC[0][m], P(R + m).x - P(R - m).x, v.x);
+            v.y = fma(a.fC[0][m], P(R + m).y - P(R - m).y, v.y);
+          }
+          uw[(u + H) % NW] = v;  // u(i + R): slot (u + R + R) mod NW
+        }
         // k row of the pair: values k-H .. k+1+H  (cols 8-H+2tx .. 9+H+2tx)
         const double* rowp = sl + (ty + H) * S3_PW + 2 * tx + 8 - H;
         double rk[2 * H + 2];
@@ -264,19 +300,17 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double* ck = rk + H + e;  // centre of node e
-          // axis 0 from the modular register window: p(i+m) = pw[(u+m+H) % NW]
-          auto w0 = [&](int m) -> double {
-            const double2 v = pw[(u + m + H + 2 * NW) % NW];
+          // axis 0 from the modular register windows:
+          // p(i+m) = pw[(u+m) % NW], u(i+m) = uw[(u+m+R) % NW]
+          auto u0 = [&](int m) -> double {
+            const double2 v = uw[(u + m + R + 2 * NW) % NW];
             return e == 0 ? v.x : v.y;
           };
           double Dk = a.fC[2][1] * (ck[1] - ck[-1]);
-          double Di = a.fC[0][1] * (w0(1) - w0(-1));
 #pragma unroll
-          for (int m = 2; m <= R; ++m) {
-            Dk = fma(a.fC[2][m], ck[m] - ck[-m], Dk);
-            Di = fma(a.fC[0][m], w0(m) - w0(-m), Di);
-          }
-          const double pv = w0(0);
+          for (int m = 2; m <= R; ++m) Dk = fma(a.fC[2][m], ck[m] - ck[-m], Dk);
+          const double Di = u0(0);
+          const double pv = e == 0 ? pw[u % NW].x : pw[u % NW].y;
           const double Dj = e == 0 ? Dj0 : Dj1;
           double adv = Di * Di;
           adv = fma(Dj, Dj, adv);
@@ -285,12 +319,12 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
           if (EIK) {
             kv = 1.0 - adv;
           } else {
-            double lap = fma(a.fE0 - a.fE[1][0], pv, e == 0 ? Lj0 : Lj1);  // j's p_0 term is in Lj
+            // p_0 terms of k (composite); j's is in Lj; i is two-pass
+            double lap = fma(a.fE[2][0], pv, e == 0 ? Lj0 : Lj1);
 #pragma unroll
-            for (int m = 1; m <= H; ++m) {
-              lap = fma(a.fE[2][m], ck[m] + ck[-m], lap);
-              lap = fma(a.fE[0][m], w0(m) + w0(-m), lap);
-            }
+            for (int m = 1; m <= H; ++m) lap = fma(a.fE[2][m], ck[m] + ck[-m], lap);
+#pragma unroll
+            for (int m = 1; m <= R; ++m) lap = fma(a.fC[0][m], u0(m) - u0(-m), lap);
             kv = fma(a.eps * pv, lap, 1.0) - adv;
           }
           const double Ae = e == 0 ? Av.x : Av.y;
@@ -318,8 +352,6 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         if (STAGE == 1) __stcs(reinterpret_cast<double2*>(a.dt + idx), make_double2(dtn[0], dtn[1]));
         if (STAGE <= 3) __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
         __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
-        // window entry p(i + H + 1) replaces p(i - H)
-        pw[u] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
       }
     }
     sb = sb + 1 == S3_SLOTS ? 0 : sb + 1;
