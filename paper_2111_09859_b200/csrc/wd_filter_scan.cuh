@@ -102,24 +102,33 @@ __device__ __forceinline__ double fs_rhsh(const double* w, int h, const double* 
 // RED: fused convergence reduction against a.A (separate instantiation, so
 // the plain sweeps carry no predicated reduction code).
 template <bool AX2, int MM, bool RED>
-__global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
+#ifndef WD_SCAN_TG
+#define WD_SCAN_TG 0  // 1: factor tables read from global memory (L1) instead of shared
+#endif
+#ifndef WD_SCAN_MINB
+#define WD_SCAN_MINB 2
+#endif
+__global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) {
   if (a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double fs_smem[];
   const int n = a.T.n, m = a.T.m, per = a.per;
   // tables: T1 (fm, h), T2 (P, g), T4 (Q, z) as double2; T3 rinv
-  const double2* T1 = reinterpret_cast<const double2*>(fs_smem);
+  const double* tb = WD_SCAN_TG ? a.T.tab : fs_smem;
+  const double2* T1 = reinterpret_cast<const double2*>(tb);
   const double2* T2 = T1 + n;
   const double2* T4 = T2 + n;
-  const double* T3 = fs_smem + 6 * n;
-  double* shc = fs_smem + 7 * n;  // FilterCoef (dynamic h: generic path)
-  double* tile = fs_smem + ((7 * n + 36 + 3) & ~3);  // 32-byte aligned (16-byte cp.async)
+  const double* T3 = tb + 6 * n;
+  constexpr int tabn = WD_SCAN_TG ? 0 : 1;  // tables in shared memory?
+  double* shc = fs_smem + tabn * 7 * n;  // FilterCoef (dynamic h: generic path)
+  double* tile = fs_smem + ((tabn * 7 * n + 36 + 3) & ~3);  // 32-byte aligned (16-byte cp.async)
   const int NR = n + 2 * FS_G;
   const int LS = NR | 1;  // AX2 line stride (odd)
   const int tsz = AX2 ? FS_L * LS : NR * FS_L;
   double* Yend = tile + tsz;
   double* Xst = Yend + FS_T;
   double* Hs = Xst + FS_T;
-  for (int t = threadIdx.x; t < 7 * n; t += FS_T) fs_smem[t] = a.T.tab[t];
+  if (!WD_SCAN_TG)
+    for (int t = threadIdx.x; t < 7 * n; t += FS_T) fs_smem[t] = a.T.tab[t];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < 36; ++k) shc[k] = a.fc.hc[k];
@@ -445,7 +454,8 @@ __global__ void __launch_bounds__(FS_T, 2) k_filter_scan(ScanArgs a) {
 inline size_t scan_smem(int n) {
   const int NR = n + 2 * FS_G;
   const size_t tile = (size_t)FS_L * (size_t)(NR | 1);  // >= NR * FS_L
-  return ((((size_t)7 * n + 36 + 3) & ~(size_t)3) + tile + 3 * FS_T) * sizeof(double);
+  return ((((size_t)(WD_SCAN_TG ? 0 : 7) * n + 36 + 3) & ~(size_t)3) + tile + 3 * FS_T) *
+         sizeof(double);
 }
 
 }  // namespace wd

@@ -8,10 +8,12 @@ CS=$ROOT/paper_2111_09859_b200/csrc
 OUT=$ROOT/paper_2111_09859_b200/variants
 mkdir -p "$OUT"
 name=$1; shift
-make -C "$CS" -j4 wd_capi.o wd_fused.o >/dev/null
-nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false \
-  -Xcompiler -fPIC,-O2 -Xptxas -v --expt-relaxed-constexpr "$@" -c "$CS/wd_stage_fast.cu" \
-  -o "$OUT/$name.o" 2> "$OUT/$name.ptxas.log"
-nvcc -gencode arch=compute_100a,code=sm_100a -shared --cudart=static -o "$OUT/libwd_$name.so" \
-  "$CS/wd_capi.o" "$CS/wd_fused.o" "$OUT/$name.o"
-grep -A2 "k_f3_fast3ILi3ELb0ELi2" "$OUT/$name.ptxas.log" | grep -E "registers|spill" | tr '\n' ' '; echo
+# which translation unit the defines apply to: TU=wd_stage_fast (default) or wd_fused
+TU=${TU:-wd_stage_fast}
+make -C "$CS" -j4 wd_capi.o wd_fused.o wd_stage_fast.o >/dev/null
+FL="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -Xcompiler -fPIC,-O2 -Xptxas -v --expt-relaxed-constexpr"
+nvcc $FL "$@" -c "$CS/$TU.cu" -o "$OUT/$name.o" 2> "$OUT/$name.ptxas.log"
+OBJS="$CS/wd_capi.o $OUT/$name.o"
+[ "$TU" = wd_stage_fast ] && OBJS="$OBJS $CS/wd_fused.o" || OBJS="$OBJS $CS/wd_stage_fast.o"
+nvcc -gencode arch=compute_100a,code=sm_100a -shared --cudart=static -o "$OUT/libwd_$name.so" $OBJS
+grep -E "registers|spill" "$OUT/$name.ptxas.log" | sort | uniq -c | sort -rn | head -3
