@@ -10,6 +10,7 @@
 #include "wd_filter_scan.cuh"
 
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 namespace wd {
@@ -177,6 +178,13 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
     fp.use_scan = 1;
     for (int a = 0; a < 3; ++a)
       if (in.scan[a].n != in.g.n[a]) fp.use_scan = 0;
+  }
+  fp.filt_order[0] = 0;
+  fp.filt_order[1] = 1;
+  fp.filt_order[2] = 2;
+  if (const char* o = getenv("WD_FILTER_ORDER")) {  // experiments: e.g. "201"
+    if (sd.arith == 1 && strlen(o) == 3)
+      for (int a = 0; a < 3; ++a) fp.filt_order[a] = o[a] - '0';
   }
   fp.n_fast = fp.n_exact = 0;
   if (sd.arith == 1) {
@@ -368,12 +376,15 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
       stage_dispatch(R, eik, kid, a, chunks * all_tiles, nullptr, false, s);
     }
   } else if (kid >= 5 && kid <= 7) {
-    const int ax = kid - 5;
+    // position kid-5 in the sweep sequence -> axis (fast arithmetic may use
+    // another axis order: the 1-D filters commute up to round-off)
+    const int pos = kid - 5;
+    const int ax = fp.filt_order[pos];
     const double* srcs[3] = {bk, tmp, bp};
     double* dsts[3] = {tmp, bp, B};
     SweepArgs w;
-    w.in = srcs[ax];
-    w.out = dsts[ax];
+    w.in = srcs[pos];
+    w.out = dsts[pos];
     w.n = g.n[ax];
     w.axis = ax;
     w.n0 = g.n[0];
@@ -390,7 +401,7 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
     w.h = T.h;
     w.denom = T.denom;
     w.fc = in.fcoef;
-    w.A = ax == 2 ? A : nullptr;
+    w.A = pos == 2 ? A : nullptr;
     w.st = st;
     if (fp.use_scan) launch_scan(w, in.scan[ax], s);
     else launch_sweep(w, s);

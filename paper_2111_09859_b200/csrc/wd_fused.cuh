@@ -52,6 +52,7 @@ struct FusedPlan {
   int i_lo = 0, i_hi = 0;  // axis-0 plane range updated by the stages (0,0 = all)
   int use_scan = 0;        // fast arithmetic: segmented-scan filter sweeps
   int use_fast3 = 0;       // fast arithmetic, E6: cp.async-pipelined stage kernel
+  int filt_order[3] = {0, 1, 2};  // axis of each filter sweep (reference order 0, 1, 2)
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).
