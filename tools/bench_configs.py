@@ -1,0 +1,139 @@
+#!/usr/bin/env python
+"""Per-configuration GPU measurement of every BASELINE config (the parity
+cases that are not the bench.py headline): device time per pseudo-step
+(CUDA events on the solver stream, after warm-up), GLUPS, and the step's
+fraction of the HBM roofline with SURVEY sec. 8(d)'s algorithmic bytes per
+update (21 stage words + 2 per filtered axis + 1 convergence read + 4 d^2
+metric words on curvilinear grids).  C1 is additionally solved to its
+tolerance (18,440 iterations in the reference) through solve_steady, so its
+time-to-converge is measured, not extrapolated.
+
+  python tools/bench_configs.py [--cases c1,c2,c3,c5,c5p] [--steps 20] [--out FILE]
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+def cases():
+    import paper_2111_09859_b200 as W
+    from profile_step import case
+    out = {}
+    out["c1"] = case("c1", 0) + ("2-D flat plate 201x101, HJ E4 + F0.49",)
+    out["c2"] = case("c2", 0) + ("2-D annulus O-grid 257x129, HJ-curvature C6 + F0.495",)
+    out["c3"] = case("c3", 0) + ("2-D sinusoidal bump 1025x513, HJ E6 + F0.49",)
+    g, f, s, fc, flt = case("c3", 0)
+    out["c3lad"] = (g, f, "E6", W.FormulationConfig(kind="hj_lad"), flt,
+                    "2-D sinusoidal bump 1025x513, HJ-LAD E6 + F0.49")
+    out["c3eik"] = (g, f, "E6", W.FormulationConfig(kind="eikonal"), flt,
+                    "2-D sinusoidal bump 1025x513, Eikonal E6 + F0.49")
+    out["c5"] = case("c5", 0) + ("3-D cylinder O-grid 1024x512x256, HJ-curvature C6 + F0.48",)
+    g, f, s, fc, flt = out["c5"][:5]
+    out["c5p"] = (g, f, "C6", W.FormulationConfig(kind="poisson"), flt,
+                  "3-D cylinder O-grid 1024x512x256, Poisson C6 + F0.48")
+    out["c4exact"] = case("c4", 512) + ("3-D channel 512^3, HJ E6 + F0.49 (exact arithmetic)",)
+    return out
+
+
+def words(nd, filt, uniform):
+    return 21 + (2 * nd if filt else 0) + 1 + (0 if uniform else 4 * nd * nd)
+
+
+def measure(name, spec, K, Wm, arith, peak):
+    import torch
+    from paper_2111_09859_b200 import _context, _native as nat
+    grid, faces, scheme, fc, filt, label = spec
+    ctx = _context.NativeSolver(grid, faces, None, scheme, fc, filt, 0.5, 1e-15, 10**9,
+                                arith=arith)
+    dims = tuple(grid.dims)
+    N = int(np.prod(dims))
+    phi = torch.zeros(dims, dtype=torch.float64, device="cuda")
+    hist = torch.zeros(K + Wm + 8, dtype=torch.float64, device="cuda")
+    nat.check(ctx.lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
+    stream = ctx.stream()
+    nat.check(ctx.lib.wd_steps(ctx.ptr, Wm))
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    nat.check(ctx.lib.wd_steps(ctx.ptr, K))
+    e1.record(stream)
+    e1.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3
+    st = nat.Status()
+    nat.check(ctx.lib.wd_read_status(ctx.ptr, ctypes.byref(st)))
+    fused = ctx.fused
+    ctx.close()
+    del phi, hist
+    torch.cuda.empty_cache()
+    w = words(grid.ndim, filt is not None, grid.is_uniform)
+    ms = secs / K * 1e3
+    ach = w * 8 * N / (secs / K) / 1e9
+    return {"case": name, "label": label, "dims": list(dims), "nodes": N, "arith": arith,
+            "path": "fused" if fused else "generic", "steps": K, "warmup": Wm,
+            "state": int(st.state), "ms_per_step": round(ms, 4),
+            "glups": round(N * K / secs / 1e9, 4), "words_per_update": w,
+            "step_roofline_frac": round(ach / peak, 4), "achieved_gbs": round(ach, 1)}
+
+
+def converge_c1(spec):
+    """Full C1 solve to tol 1e-8 through the public API (device-resident loop)."""
+    import torch
+    import paper_2111_09859_b200 as W
+    grid, faces, scheme, fc, filt, label = spec
+    cfg = W.SolveConfig(formulation=fc, scheme=scheme, filter_config=filt, cfl=0.5, tol=1e-8,
+                        max_iters=30000)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = W.solve_steady(grid, W.BoundarySpec(faces), cfg)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    return {"case": "c1", "label": label + ", solved to tol 1e-8", "iters": int(rep.iters),
+            "converged": bool(rep.converged), "seconds_wall": round(t, 3),
+            "loop_seconds": round(float(rep.wall_seconds[-1]), 3) if len(rep.wall_seconds) else None,
+            "reference_iters": 18440}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="c1,c2,c3,c3lad,c3eik,c5,c5p,c4exact")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    from bench import _peaks
+    peak, kind = _peaks()
+    allc = cases()
+    rows = []
+    for name in args.cases.split(","):
+        spec = allc[name]
+        K = args.steps if spec[0].dims[0] * spec[0].dims[1] > 10**6 else args.steps * 50
+        for arith in ("exact", "fast"):
+            if arith == "fast" and name == "c4exact":
+                continue
+            r = measure(name, spec, K, args.warmup, arith, peak)
+            print(json.dumps(r), flush=True)
+            rows.append(r)
+            if r["path"] == "generic" and arith == "exact":
+                break  # the generic path has one arithmetic
+    if "c1" in args.cases.split(","):
+        r = converge_c1(allc["c1"])
+        print(json.dumps(r), flush=True)
+        rows.append(r)
+    out = {"peak_gbs": peak, "peak_source": kind, "rows": rows}
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
