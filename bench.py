@@ -354,8 +354,9 @@ def run_b200(args, world, rank, local):
     nd = len(dims)
     roof = None
     if kern:
-        kwords = {"stage1": 4, "stage2": 6, "stage3": 6, "stage4": 5, "filter_axis0": 2,
-                  "filter_axis1": 2, "filter_axis2": 3, "change": 2}
+        # algorithmic words per node of each kernel as run (the fast stage
+        # kernels use a low-storage RK4: 3 / 5 / 4 / 5)
+        kwords = {name: lib.wd_kernel_words(ctx.ptr, kid) for kid, name in names.items()}
         dom = max(kern, key=kern.get)
         ach = kwords[dom] * 8 * N / (kern[dom] / 1e3) / 1e9
         traffic = None
@@ -408,7 +409,11 @@ def run_b200(args, world, rank, local):
                        "fused": True if kern else False},
             "roofline": roof,
             "step_roofline": {"achieved": round(step_ach, 1), "peak": peak, "unit": "GB/s",
-                              "frac": round(step_ach / peak, 4), "words_per_update": w_upd},
+                              "frac": round(step_ach / peak, 4), "words_per_update": w_upd,
+                              "model": "SURVEY 8(d) B_alg (21 stage words + 2 per filter "
+                                       "sweep + 1 convergence read)",
+                              "words_moved": (sum(kwords[k] for k in kwords if k != "change")
+                                              if kern else None)},
             "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
             "gpu_launches": K * (12 if kern else 0),
             "clocks": clk, "e2e": e2e,

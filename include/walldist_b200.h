@@ -132,6 +132,11 @@ int wd_fused_active(wd_ctx* ctx);
  * 5..7 filter sweeps, 8 change reduction.  Clobbers the workspace; for
  * benchmarking only.                                                     */
 int wd_time_kernel(wd_ctx* ctx, int kid, int reps, double* avg_ms);
+/* Algorithmic fp64 words per node that kernel `kid` (as above) of the fused
+ * step moves (reads + writes of whole fields, halos excluded); 0 when the
+ * context has no fused path.  The fast stage kernels run a low-storage RK4
+ * (stage words 3 / 5 / 4 / 5 instead of 4 / 6 / 6 / 5).                   */
+int wd_kernel_words(wd_ctx* ctx, int kid);
 
 /* ---- operator-level entry points (parity + drop-in operators) -------- */
 /* RK4 step solver.py:183-218 (phi_out = BC(filter(RK4(phi_in))))         */

@@ -14,6 +14,7 @@ from .grid import (BumpParams, CurvilinearGrid, build_annulus, build_bump_grid,
 from .operators import FilterConfig
 from .formulations import FormulationConfig
 from .solver import BoundarySpec, SolveConfig, SolveReport, solve_steady
+from .unsteady import MotionSpec, solve_unsteady
 from ._native import NativeUnavailableError
 
 __all__ = [
@@ -24,9 +25,11 @@ __all__ = [
     "FilterConfig",
     "FormulationConfig",
     "BoundarySpec",
+    "MotionSpec",
     "SolveConfig",
     "SolveReport",
     "solve_steady",
+    "solve_unsteady",
     "BumpParams",
     "build_channel3d",
     "build_annulus",

@@ -111,6 +111,7 @@ SIGNATURES = {
     "wd_linf_delta": (_I, [_P, _P, _P, ctypes.c_longlong, _DP, _P]),
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
+    "wd_kernel_words": (_I, [_P, _I]),
     "wd_dist_configure": (_I, [_P, _I, _I]),
     "wd_dist_stage": (_I, [_P, _I, _P, _P, _P]),
     "wd_dist_filter": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _P]),

@@ -963,6 +963,14 @@ int wd_time_kernel(wd_ctx* c, int kid, int reps, double* avg_ms) {
   return WD_OK;
 }
 
+int wd_kernel_words(wd_ctx* c, int kid) {
+  if (!c || !c->fused.active || kid < 1 || kid > 8) return 0;
+  // stages 1-4, filters along axes (sweep order) 0, 1, 2 (+ reduction), change
+  static const int classic[9] = {0, 4, 6, 6, 5, 2, 2, 3, 2};
+  static const int low[9] = {0, 3, 5, 4, 5, 2, 2, 3, 2};
+  return (c->fused.use_fast3 && fast3_lowstorage()) ? low[kid] : classic[kid];
+}
+
 int wd_tendency(wd_ctx* c, const double* phi, double* k) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
   if (const int rc = ensure_generic(c)) return rc;

@@ -57,6 +57,8 @@ struct FusedPlan {
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).
 void fused_plan(FusedPlan& fp, const FusedInputs& in);
+// 1 when the fast E6 stage kernels run the low-storage RK4 (wd_stage_fast.cuh)
+int fast3_lowstorage();
 // One pseudo-step A -> B incl. change reduction and stop test.
 void fused_step(const FusedPlan& fp, const double* A, double* B, Status* st, double* hist,
                 cudaStream_t s);

@@ -108,6 +108,8 @@ int fast3_chunks(int ntiles, int ni) {
   return best;
 }
 
+int fast3_lowstorage() { return S3_LS ? 1 : 0; }
+
 template bool fast3_prepare<true>();
 template bool fast3_prepare<false>();
 template void launch_fast3<true>(int, F3Args, int, const int*, int, cudaStream_t, bool);

@@ -33,11 +33,25 @@ constexpr int S3_PW = S3_TK + 16;  // 48 doubles per plane row (8-wide k halo)
 #ifndef WD_S3_D
 #define WD_S3_D 2
 #endif
-#ifndef WD_S3_PF
-#define WD_S3_PF 0
+#ifndef WD_S3_REG
+#define WD_S3_REG 0
+#endif
+#ifndef WD_S3_LS
+#define WD_S3_LS 1
 #endif
 constexpr int S3_D = WD_S3_D;      // planes in flight ahead of the computed one
-constexpr int S3_PF = WD_S3_PF;    // extra planes of L2 prefetch beyond the ring (0: off)
+// pointwise fields (A, dt, acc, axis-0 window entry) straight to registers,
+// one plane ahead, instead of through shared memory (saves shared-memory
+// bandwidth; measured slower: 7.27 vs 6.42 ms per step, one plane of
+// register prefetch does not cover the HBM latency -> off)
+constexpr bool S3_REG = WD_S3_REG != 0;
+// low-storage RK4 (fast mode): k1 and k3 are recovered from the stage
+// fields, k1 = (p1 - A) * 2 / dt, k3 = (p3 - A) / dt, so acc = k1 + 2 k2 is
+// written once (stage 2) and read once (stage 4): 17 state words per step
+// instead of 21 (stage 1: p -> p1, dt; 2: p1, A, dt -> p2, acc;
+// 3: p2, A, dt -> p3; 4: p3, A, dt, acc -> out).  Round-off level change:
+// the recovered k enters the update multiplied by dt again (<= 1 ulp of A).
+constexpr bool S3_LS = WD_S3_LS != 0;
 constexpr int S3_SLOTS = S3_D + 1;
 
 template <int R>
@@ -46,7 +60,7 @@ struct S3Layout {
   static constexpr int PH = S3_TJ + 2 * H;          // plane rows
   static constexpr int PLANE = PH * S3_PW;          // doubles per plane slot
   static constexpr int PT = S3_TJ * S3_TK;          // 512 doubles per pointwise tile
-  static constexpr int SLOT = PLANE + 4 * PT;       // plane + A + dt + acc + window entry
+  static constexpr int SLOT = PLANE + (S3_REG ? 0 : 4 * PT);  // plane (+ A, dt, acc, window entry)
   static constexpr int CHUNKS = PH * (S3_PW / 2);   // 16-byte chunks of a plane slot
   static constexpr int CPT = (CHUNKS + 255) / 256;  // chunks per thread
   static constexpr size_t SMEM = (size_t)S3_SLOTS * SLOT * sizeof(double);
@@ -73,6 +87,21 @@ __device__ __forceinline__ double s3_div(double a, double b) {
   r = fma(r, e, r);
   const double q = a * r;
   return fma(fma(-b, q, a), r, q);
+}
+
+__device__ __forceinline__ double s3_rcp(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double2 s3_ldcs2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 s3_ldcg2(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
 }
 
 // JB: tiles touching a non-periodic j end (walls).  Rows 0..5 / n1-6..n1-1
@@ -133,6 +162,7 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
   const int wrap0 = n0 * is0;
   // loads of plane ip into slot `slot`; the axis-0 window entry is plane
   // ip + H + 1 (periodic axis 0)
+  constexpr bool NEED_ACC = S3_LS ? STAGE == 4 : STAGE > 1;  // acc read by this stage
   auto issue = [&](int ip, int slot) {
     double* sl = smem + slot * LY::SLOT;
     if (ip < i1) {
@@ -141,33 +171,43 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
       for (int q = 0; q < LY::CPT; ++q)
         if (coff[q] != -2) s3_cp16(sl + cdst[q], a.p + (coff[q] >= 0 ? po + coff[q] : 0), coff[q] >= 0);
       const int pl = po + col;
-      double* pt = sl + LY::PLANE + own;
-      if (STAGE > 1) {  // stage 1: A = p, read from the plane tile
-        s3_cp16(pt, a.A + pl, true);
-        s3_cp16(pt + LY::PT, a.dt + pl, true);
-        s3_cp16(pt + 2 * LY::PT, a.acc + pl, true);
-      }
-      int pw_off = pl + H * is0;  // window entry p(ip + 2R)
-      bool wok = true;
-      if (pw_off >= wrap0) {
-        if (a.per0) pw_off -= wrap0;
-        else wok = false;  // beyond the last plane: never used, zero fill
-      }
-      s3_cp16(pt + 3 * LY::PT, a.p + (wok ? pw_off : 0), wok);
-      if (S3_PF > 0 && (tx & 7) == 0 && ip + S3_PF < i1) {  // one line per 8 pairs
-        const int pf = pl + S3_PF * is0;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.p + pf));
-        if (STAGE > 1) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + pf));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.dt + pf));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.acc + pf));
+      if (!S3_REG) {
+        double* pt = sl + LY::PLANE + own;
+        if (STAGE > 1) {  // stage 1: A = p, read from the plane tile
+          s3_cp16(pt, a.A + pl, true);
+          s3_cp16(pt + LY::PT, a.dt + pl, true);
+          if (NEED_ACC) s3_cp16(pt + 2 * LY::PT, a.acc + pl, true);
         }
-        int pwf = pw_off + S3_PF * is0;
-        if (pwf >= wrap0) pwf -= wrap0;
-        if (a.per0 || pw_off + S3_PF * is0 < wrap0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.p + pwf));
+        int pw_off = pl + H * is0;  // window entry p(ip + 2R)
+        bool wok = true;
+        if (pw_off >= wrap0) {
+          if (a.per0) pw_off -= wrap0;
+          else wok = false;  // beyond the last plane: never used, zero fill
+        }
+        s3_cp16(pt + 3 * LY::PT, a.p + (wok ? pw_off : 0), wok);
       }
     }
     s3_commit();
+  };
+  // S3_REG: pointwise values of plane ip -> registers (A, dt: stages 2-4;
+  // acc: stage 4 (low storage) or 2-4; window entry p(ip + 2R): all stages)
+  double2 nA = make_double2(0.0, 0.0), ndt = nA, nacc = nA, nw = nA;
+  auto pref = [&](int ip) {
+    if (S3_REG && ip < i1) {
+      const int pl = ip * is0 + col;
+      if (STAGE > 1) {
+        nA = s3_ldcs2(a.A + pl);
+        ndt = s3_ldcs2(a.dt + pl);
+      }
+      if (NEED_ACC) nacc = s3_ldcs2(a.acc + pl);
+      int pw_off = pl + H * is0;
+      bool wok = true;
+      if (pw_off >= wrap0) {
+        if (a.per0) pw_off -= wrap0;
+        else wok = false;
+      }
+      nw = wok ? s3_ldcg2(a.p + pw_off) : make_double2(0.0, 0.0);
+    }
   };
 
   // ---- prologue: axis 0 runs as two passes in registers (same
@@ -204,6 +244,7 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
   }
 #pragma unroll
   for (int d = 0; d < S3_D; ++d) issue(i0 + d, d);
+  pref(i0);
 
   // slot of plane ib + u = (sb + u) mod SLOTS; NW = 7 = 1 (mod SLOTS)
   static_assert(NW % S3_SLOTS == 1, "slot rotation assumes NW = 1 mod SLOTS");
@@ -222,8 +263,14 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         issue(i + S3_D, snext);
         const double* sl = smem + scur * LY::SLOT;
         const double* pt = sl + LY::PLANE;
+        double2 cA = nA, cdt = ndt, cacc = nacc;
         // window entry p(i + 2R) replaces p(i - 1); u(i + R) replaces u(i - R - 1)
-        pw[(u + H) % NW] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
+        if (S3_REG) {
+          pw[(u + H) % NW] = nw;
+          pref(i + 1);
+        } else {
+          pw[(u + H) % NW] = *reinterpret_cast<const double2*>(pt + 3 * LY::PT + own);
+        }
         {
           auto P = [&](int m) -> const double2& { return pw[(u + m + 2 * NW) % NW]; };  // p(i+m)
           double2 v;
@@ -290,11 +337,11 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
           }
         }
         const double2 Av = STAGE == 1 ? *reinterpret_cast<const double2*>(colp)
-                                      : *reinterpret_cast<const double2*>(pt + own);
+                                      : (S3_REG ? cA : *reinterpret_cast<const double2*>(pt + own));
         double2 dtv2 = make_double2(0.0, 0.0), accv2 = make_double2(0.0, 0.0);
         if (STAGE > 1) {
-          dtv2 = *reinterpret_cast<const double2*>(pt + LY::PT + own);
-          accv2 = *reinterpret_cast<const double2*>(pt + 2 * LY::PT + own);
+          dtv2 = S3_REG ? cdt : *reinterpret_cast<const double2*>(pt + LY::PT + own);
+          if (NEED_ACC) accv2 = S3_REG ? cacc : *reinterpret_cast<const double2*>(pt + 2 * LY::PT + own);
         }
         double o[2], ac[2], dtn[2];
 #pragma unroll
@@ -337,11 +384,24 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
             dtn[e] = dtv;
             ac[e] = kv;
             o[e] = pin ? 0.0 : fma(0.5 * dtv, kv, Ae);
+          } else if (S3_LS && STAGE == 2) {  // k1 = (p1 - A) * 2 / dt
+            const double dte = e == 0 ? dtv2.x : dtv2.y;
+            const double k1 = (pv - Ae) * (2.0 * s3_rcp(dte));
+            ac[e] = fma(2.0, kv, k1);
+            o[e] = pin ? 0.0 : fma(0.5 * dte, kv, Ae);
+          } else if (S3_LS && STAGE == 3) {
+            const double dte = e == 0 ? dtv2.x : dtv2.y;
+            o[e] = pin ? 0.0 : fma(dte, kv, Ae);
           } else if (STAGE == 2 || STAGE == 3) {
             const double dte = e == 0 ? dtv2.x : dtv2.y;
             const double acce = e == 0 ? accv2.x : accv2.y;
             ac[e] = fma(2.0, kv, acce);
             o[e] = pin ? 0.0 : fma(STAGE == 3 ? dte : 0.5 * dte, kv, Ae);
+          } else if (S3_LS) {  // k3 = (p3 - A) / dt
+            const double dte = e == 0 ? dtv2.x : dtv2.y;
+            const double acce = e == 0 ? accv2.x : accv2.y;
+            const double k3 = (pv - Ae) * s3_rcp(dte);
+            o[e] = pin ? 0.0 : fma(dte * (1.0 / 6.0), fma(2.0, k3, acce) + kv, Ae);
           } else {
             const double dte = e == 0 ? dtv2.x : dtv2.y;
             const double acce = e == 0 ? accv2.x : accv2.y;
@@ -350,7 +410,8 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         }
         const int idx = i * is0 + col;
         if (STAGE == 1) __stcs(reinterpret_cast<double2*>(a.dt + idx), make_double2(dtn[0], dtn[1]));
-        if (STAGE <= 3) __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
+        if (S3_LS ? STAGE == 2 : STAGE <= 3)
+          __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
         __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
       }
     }

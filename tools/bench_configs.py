@@ -116,7 +116,7 @@ def main():
     rows = []
     for name in args.cases.split(","):
         spec = allc[name]
-        K = args.steps if spec[0].dims[0] * spec[0].dims[1] > 10**6 else args.steps * 50
+        K = args.steps if int(np.prod(spec[0].dims)) > 10**6 else args.steps * 50
         for arith in ("exact", "fast"):
             if arith == "fast" and name == "c4exact":
                 continue
