@@ -386,6 +386,10 @@ void line_solve_prepare() {
                        (int)kLineSolveMaxSmem);
   cudaFuncSetAttribute(k_line_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kLineSolveMaxSmem);
+  cudaFuncSetAttribute(k_line_solve_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
+  cudaFuncSetAttribute(k_line_solve_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
   done = true;
 }
 template <int JOB>
@@ -400,6 +404,12 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
                                                                 scheme, fc, st);
   const long long warps = (L + 31) / 32;
   const int blocks = (int)std::min<long long>((warps + LS_WARPS - 1) / LS_WARPS, 148LL * 8);
+  if (g.s[axis] == 1 && axis == g.nd - 1 && line_solve_t_smem(n) <= kLineSolveMaxSmem) {
+    // contiguous lines: transposed cp.async staging (coalesced)
+    k_line_solve_t<JOB><<<blocks, LS_WARPS * 32, line_solve_t_smem(n), s>>>(
+        in, scratch, out, g, n, T, e, pin, use_geom_pin, st);
+    return;
+  }
   k_line_solve<JOB><<<blocks, LS_WARPS * 32, line_solve_smem(n), s>>>(
       in, scratch, out, g, axis, n, g.s[axis], T, e, pin, use_geom_pin, st);
 }
@@ -476,8 +486,12 @@ void launch_gamma_lad(wd_ctx* c, const double* p, const Status* st) {
                                                                    c->sd.epsilon, c->sd.lad_c, st);
 }
 
-// tendency(p) -> k   (formulations.py:232-252)
-void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st) {
+// tendency(p) -> k   (formulations.py:232-252).  `fresh`: dphi / U / Uh
+// (and gamma for LAD) already hold the values for this p -- the time step of
+// the same pseudo-iteration computed them from the same field with the same
+// kernels, so recomputing would reproduce them bit for bit.
+void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
+                      bool fresh = false) {
   const int kind = c->sd.kind, scheme = c->sd.scheme, nd = c->g.nd;
   const int csch = scheme == WD_UW ? WD_E2 : scheme;
   ResidualArgs a;
@@ -502,8 +516,10 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st) {
     launch_assemble(c, c->dphi, c->U, nullptr, st);
     launch_divergence(c, c->U, csch, c->lap, st);
   } else {
-    launch_dphi(c, p, st);
-    launch_assemble(c, c->dphi, c->U, c->Uh, st);
+    if (!fresh) {
+      launch_dphi(c, p, st);
+      launch_assemble(c, c->dphi, c->U, c->Uh, st);
+    }
     if (kind != WD_EIKONAL) {
       double* const* Ul = c->U;
       if (scheme == WD_UW) {
@@ -514,7 +530,7 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st) {
         for (int l = 0; l < 3; ++l) a.U.p[l] = c->Ue[l];
       }
       launch_divergence(c, Ul, csch, c->lap, st);
-      if (kind == WD_HJ_LAD) launch_gamma_lad(c, p, st);
+      if (kind == WD_HJ_LAD && !fresh) launch_gamma_lad(c, p, st);
       if (kind == WD_HJ_CURVATURE) {
         Vec3 uv;
         MVec3 nv;
@@ -576,10 +592,13 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
 }
 
 // one RK4 step A -> B given dt already in c->dt (solver.py:183-212)
-void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st) {
+void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
+                 bool dt_fresh = false) {
   const Geom& g = c->g;
   const int nb = nblocks(g.N, kThreads);
-  enqueue_tendency(c, A, c->acc, st);
+  // stage 1 evaluates the tendency at A, where enqueue_timestep just left
+  // dphi / U / Uh (/ gamma) -- except for Poisson, whose time step is static
+  enqueue_tendency(c, A, c->acc, st, dt_fresh && c->sd.kind != WD_POISSON);
   k_rk_stage<<<nb, kThreads, 0, c->stream>>>(1, A, c->dt, c->acc, c->acc, c->p, g, st);
   enqueue_tendency(c, c->p, c->k, st);
   k_rk_stage<<<nb, kThreads, 0, c->stream>>>(2, A, c->dt, c->k, c->acc, c->p, g, st);
@@ -631,7 +650,7 @@ void enqueue_step(wd_ctx* c, const double* A, double* B) {
     return;
   }
   enqueue_timestep(c, A, c->dt, c->st);
-  enqueue_rk4(c, A, B, c->st);
+  enqueue_rk4(c, A, B, c->st, true);
   k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
                                                                    c->g.N);
   k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));

@@ -31,8 +31,19 @@
 
 namespace wd {
 
-constexpr int LS_WARPS = 4;  // warps per CTA of k_line_solve
-constexpr int LS_U = 8;      // rows per unrolled group
+#ifndef WD_LS_U
+#define WD_LS_U 8
+#endif
+#ifndef WD_LS_MINB
+#define WD_LS_MINB 1
+#endif
+#ifndef WD_LT_EPI
+#define WD_LT_EPI 1
+#endif
+constexpr int LS_WARPS = 4;        // warps per CTA of k_line_solve
+constexpr int LS_U = WD_LS_U;      // rows per unrolled group
+constexpr int LS_MINB = WD_LS_MINB;  // resident CTAs per SM asked of ptxas
+constexpr bool LT_EPI = WD_LT_EPI != 0;  // k_line_solve_t: epilogue operands via cp.async tiles
 
 __device__ __forceinline__ double ls_div(double s, double d, double r) {
   const double q0 = s * r;
@@ -50,8 +61,25 @@ static __global__ void k_line_rhs(const double* __restrict__ in, double* __restr
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < ag.N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = ag.coord(idx);
-    Line w{in + (idx - (long long)i * sa), sa, n, per, off};
     double r;
+    constexpr int H = JOB == 0 ? 2 : 5;  // stencil reach
+    if (i >= H && i < n - H) {
+      // interior row (no wrap, no closure, full order): the same
+      // expressions as compact_rhs_at / the h = 5 filter row
+      const double* q = in + idx;
+      if (JOB == 0) {
+        if (scheme == WD_C4) r = C4_CA * (q[sa] - q[-sa]);
+        else r = C6_CA * (q[sa] - q[-sa]) + C6_CB * (q[2 * sa] - q[-2 * sa]);
+      } else {
+        const double* c = fc.hc + 30;
+        r = c[0] * q[0];
+#pragma unroll
+        for (int k = 1; k <= 5; ++k) r = r + c[k] * (q[k * sa] + q[-k * sa]);
+      }
+      rhs[idx] = r;
+      continue;
+    }
+    Line w{in + (idx - (long long)i * sa), sa, n, per, off};
     if (JOB == 0) {
       r = compact_rhs_at(w, i, n, scheme, per);
     } else {
@@ -69,7 +97,7 @@ static __global__ void k_line_rhs(const double* __restrict__ in, double* __restr
 }
 
 template <int JOB>
-static __global__ void __launch_bounds__(LS_WARPS * 32)
+static __global__ void __launch_bounds__(LS_WARPS * 32, LS_MINB)
     k_line_solve(const double* __restrict__ in, double* y, double* out, Geom g, int axis,
                  int n, long long sa, TriDev T, Epi epi, const uint8_t* pin, int use_geom_pin,
                  const Status* st) {
@@ -287,5 +315,232 @@ __host__ __forceinline__ size_t line_solve_smem(int n) {
   return (size_t)8 * n * sizeof(double) + (size_t)((n + LS_U - 1) / LS_U) * sizeof(int);
 }
 constexpr size_t kLineSolveMaxSmem = 200 * 1024;
+
+// Contiguous lines (the last axis, stride 1): the same recurrences, with every
+// global access transposed through per-warp shared tiles of 32 rows x 32
+// lines.  With lane = line and stride-1 lines, a direct access by the warp
+// touches 32 scattered sectors per row (8 of 32 bytes used, partial-sector
+// stores); staged, each tile row is one 256-byte run of one line.  Tiles are
+// filled with cp.async (no registers, the next chunk's rows in flight while
+// the current chunk's recurrence runs): y double-buffered, and the epilogue
+// operands (acc, c) of the back substitution issued one chunk ahead.  The
+// right-hand side stays in k_line_rhs: evaluated inside this latency-bound
+// chain (one resident CTA per SM) it made every axis slower (measured).
+// Arithmetic and its order are those of k_line_solve (bitwise equal).
+constexpr int LT_P = 33;                     // padded tile row (doubles)
+constexpr int LT_TILE = 32 * LT_P;           // doubles per tile
+constexpr int LT_WARP = (LT_EPI ? 4 : 2) * LT_TILE + 64;  // y[2], (acc, c), fcor[32], line pin[32]
+
+__host__ __forceinline__ size_t line_solve_t_smem(int n) {
+  return line_solve_smem(n) + (size_t)LS_WARPS * LT_WARP * sizeof(double) + 16;
+}
+
+__device__ __forceinline__ void lt_cp8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void lt_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void lt_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int JOB>
+static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
+    k_line_solve_t(const double* __restrict__ in, double* y, double* out, Geom g, int n, TriDev T,
+                   Epi epi, const uint8_t* pin, int use_geom_pin, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  extern __shared__ double ls_f[];
+  const long long L = g.N / n;
+  const int axis = g.nd - 1;
+  double* sfact = ls_f;
+  double* sswap = sfact + n;
+  double* sdu = sswap + n;
+  double* sdu2 = sdu + n;
+  double* sd = sdu2 + n;
+  double* srinv = sd + n;
+  double* sz = srinv + n;
+  double* sh = sz + n;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    sfact[t] = t < n - 1 ? T.fact[t] : 0.0;
+    sswap[t] = t < n - 1 ? T.swap[t] : 0.0;
+    sdu[t] = t < n - 1 ? T.du[t] : 0.0;
+    sdu2[t] = t < n - 2 ? T.du2[t] : 0.0;
+    sd[t] = T.d[t];
+    srinv[t] = T.rinv[t];
+    sz[t] = T.cyclic ? T.z[t] : 0.0;
+    sh[t] = T.cyclic ? T.h[t] : 0.0;
+  }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* wbase = sh + n + 2 + wib * LT_WARP;
+  double* ta = wbase + 2 * LT_TILE;
+  double* tc = wbase + 3 * LT_TILE;
+  double* sfc = wbase + (LT_EPI ? 4 : 2) * LT_TILE;
+  double* slp = sfc + 32;
+  __syncthreads();
+  const bool need_acc = JOB == 0 && epi.mode == 2;
+  const bool need_c = JOB == 0 && epi.mode != 0 && epi.cfield != nullptr;
+  const bool pin_lo = JOB == 1 && use_geom_pin && pick(g.face, 2 * axis) == WD_FACE_WALL;
+  const bool pin_hi = JOB == 1 && use_geom_pin && pick(g.face, 2 * axis + 1) == WD_FACE_WALL;
+  const long long nwarps = (long long)gridDim.x * LS_WARPS;
+  for (long long grp = (long long)blockIdx.x * LS_WARPS + wib; grp * 32 < L; grp += nwarps) {
+    const long long q0 = grp * 32;
+    const int nl = (int)min(32LL, L - q0);
+    const long long b0 = q0 * n;  // line j starts at b0 + j n
+    double* yb = y + b0;
+    const bool act = lane < nl;
+    // rows [r, r + cnt) of the block's lines -> tile[row - r][line]
+    auto fetch = [&](double* tile, const double* src, int r, int cnt) {
+      if (lane < cnt) {
+        const double* s0 = src + b0 + r + lane;
+#pragma unroll 8
+        for (int j = 0; j < nl; ++j) lt_cp8(tile + lane * LT_P + j, s0 + (long long)j * n);
+      }
+    };
+    if (JOB == 1 && use_geom_pin) {
+      bool lp = false;
+      if (act) {
+        int c[kMaxDim];
+        node_coords(g, b0 + (long long)lane * n, c);
+#pragma unroll
+        for (int b = 0; b < kMaxDim; ++b) {
+          if (b >= g.nd || b == axis) continue;
+          if (c[b] == 0 && g.face[2 * b] == WD_FACE_WALL) lp = true;
+          if (c[b] == g.n[b] - 1 && g.face[2 * b + 1] == WD_FACE_WALL) lp = true;
+        }
+      }
+      slp[lane] = lp ? 1.0 : 0.0;
+    }
+    // ---------------- forward elimination: chunk k = steps [r0, r0 + cnt),
+    // b = rhs rows r0 + 1 .. r0 + cnt in tile slots 0 .. cnt-1, y rows
+    // r0 .. r0 + cnt - 1 left in the same slots
+    double carry = act ? yb[(long long)lane * n] : 0.0;
+    double hs = 0.0;
+    if (T.cyclic) hs = hs + sh[0] * carry;
+    fetch(wbase, y, 1, min(32, n - 1));
+    lt_commit();
+    for (int r0 = 0, k = 0; r0 < n - 1; r0 += 32, ++k) {
+      const int cnt = min(32, n - 1 - r0);
+      double* cur = wbase + (k & 1) * LT_TILE;
+      lt_wait<0>();
+      __syncwarp();
+      if (r0 + 32 < n - 1)
+        fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0 + 33, min(32, n - 1 - (r0 + 32)));
+      lt_commit();
+      auto step = [&](int t) {
+        const int i = r0 + t;
+        const double b = cur[t * LT_P + lane];
+        const double f = sfact[i];
+        double yv;
+        if (sswap[i] != 0.0) {
+          yv = b;
+          carry = carry - f * b;
+        } else {
+          yv = carry;
+          carry = b - f * carry;
+        }
+        if (T.cyclic) hs = hs + sh[i + 1] * b;
+        cur[t * LT_P + lane] = yv;
+      };
+      if (cnt == 32) {
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) step(t);
+      } else {
+        for (int t = 0; t < cnt; ++t) step(t);
+      }
+      __syncwarp();
+      if (lane < cnt) {
+        double* d0 = yb + r0 + lane;
+#pragma unroll 8
+        for (int j = 0; j < nl; ++j) d0[(long long)j * n] = cur[lane * LT_P + j];
+      }
+      __syncwarp();
+    }
+    lt_wait<0>();
+    if (act) yb[(long long)lane * n + n - 1] = carry;
+    sfc[lane] = T.cyclic ? hs / T.denom : 0.0;
+    __syncwarp();
+    // ---------------- back substitution, chunks [r0, rt) going down.  Copy
+    // groups in flight: y of the next chunk (double buffer) and the epilogue
+    // operands of the current one, so wait_group 1 releases the older.
+    double x1 = 0.0, x2 = 0.0;
+    auto fetch_epi = [&](int r0, int cnt) {
+      if (LT_EPI && need_acc) fetch(ta, epi.acc, r0, cnt);
+      if (LT_EPI && need_c) fetch(tc, epi.cfield, r0, cnt);
+    };
+    {
+      const int r0 = max(0, n - 32);
+      fetch(wbase, y, r0, n - r0);
+      lt_commit();
+      fetch_epi(r0, n - r0);
+      lt_commit();
+    }
+    for (int rt = n, k = 0; rt > 0; rt -= 32, ++k) {
+      const int r0 = max(0, rt - 32);
+      const int cnt = rt - r0;
+      double* cur = wbase + (k & 1) * LT_TILE;
+      lt_wait<1>();  // y of this chunk
+      __syncwarp();
+      if (r0 > 0) {
+        const int r0n = max(0, r0 - 32);
+        fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0n, r0 - r0n);
+      }
+      lt_commit();
+      for (int r = rt - 1; r >= r0; --r) {
+        const int t = r - r0;
+        const double yv = cur[t * LT_P + lane];
+        double x;
+        if (r == n - 1) {
+          x = ls_div(yv, sd[n - 1], srinv[n - 1]);
+        } else if (r == n - 2) {
+          x = ls_div(yv - sdu[n - 2] * x1, sd[n - 2], srinv[n - 2]);
+        } else {
+          x = ls_div((yv - sdu[r] * x1) - sdu2[r] * x2, sd[r], srinv[r]);
+        }
+        x2 = x1;
+        x1 = x;
+        cur[t * LT_P + lane] = x;
+      }
+      lt_wait<1>();  // epilogue operands of this chunk
+      __syncwarp();
+      if (lane < cnt) {
+        const int r = r0 + lane;
+        const long long i0 = b0 + r;
+#pragma unroll 4
+        for (int j = 0; j < nl; ++j) {
+          const int tj = lane * LT_P + j;
+          const double x = cur[tj];
+          const double xv = T.cyclic ? x - sfc[j] * sz[r] : x;
+          const long long idx = i0 + (long long)j * n;
+          if (JOB == 0) {
+            double o = xv;
+            if (epi.mode != 0) {
+              const double cv = need_c ? (LT_EPI ? tc[tj] : epi.cfield[idx]) : epi.cscal;
+              const double tt = cv * xv;
+              o = epi.mode == 1 ? tt : (need_acc ? (LT_EPI ? ta[tj] : epi.acc[idx]) : 0.0) + tt;
+            }
+            out[idx] = o;
+          } else {
+            bool p;
+            if (use_geom_pin)
+              p = slp[j] != 0.0 || (r == 0 && pin_lo) || (r == n - 1 && pin_hi) ||
+                  (g.mask != nullptr && g.mask[idx] != 0);
+            else
+              p = pin != nullptr && pin[idx] != 0;
+            out[idx] = p ? in[idx] : xv;
+          }
+        }
+      }
+      __syncwarp();
+      if (r0 > 0) {
+        const int r0n = max(0, r0 - 32);
+        fetch_epi(r0n, r0 - r0n);
+      }
+      lt_commit();
+    }
+    lt_wait<0>();
+    __syncwarp();
+  }
+}
 
 }  // namespace wd
