@@ -399,9 +399,14 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
                        const Status* st, cudaStream_t s) {
   const int n = g.n[axis];
   const long long L = g.N / n;
-  k_line_rhs<JOB><<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, scratch, axis_geom(g, axis),
-                                                                per, off,
-                                                                scheme, fc, st);
+  if (g.s[axis] >= 32 && !getenv("WD_NO_RHS_SEG")) {
+    const long long segs = L * ((n + RS_ROWS - 1) / RS_ROWS);
+    k_line_rhs_seg<JOB><<<nblocks(segs, kThreads), kThreads, 0, s>>>(
+        in, scratch, g.N, g.s[axis], n, per, off, scheme, fc, st);
+  } else {
+    k_line_rhs<JOB><<<nblocks(g.N, kThreads), kThreads, 0, s>>>(in, scratch, axis_geom(g, axis),
+                                                                  per, off, scheme, fc, st);
+  }
   const long long warps = (L + 31) / 32;
   const int blocks = (int)std::min<long long>((warps + LS_WARPS - 1) / LS_WARPS, 148LL * 8);
   if (g.s[axis] == 1 && axis == g.nd - 1 && line_solve_t_smem(n) <= kLineSolveMaxSmem) {

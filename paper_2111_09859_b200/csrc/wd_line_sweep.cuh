@@ -96,6 +96,87 @@ static __global__ void k_line_rhs(const double* __restrict__ in, double* __restr
   }
 }
 
+// Strided axes: one thread per segment of RS consecutive rows of a line, the
+// input window (RS + 2H rows) loaded once into registers, so every input
+// row is read ~(RS + 2H) / RS times instead of 2H + 1 (the per-node kernel
+// above read the axis-0 field 3.3x from DRAM at 1024x512x256, ncu).
+// Threads with consecutive ids own consecutive lines (coalesced rows).
+// Same expressions as k_line_rhs (bitwise equal).
+constexpr int RS_ROWS = 16;
+
+template <int JOB>
+static __global__ void k_line_rhs_seg(const double* __restrict__ in, double* __restrict__ rhs,
+                                      long long N, long long sa, int n, int per, double off,
+                                      int scheme, FilterCoef fc, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  constexpr int H = JOB == 0 ? 2 : 5;
+  const int nseg = (n + RS_ROWS - 1) / RS_ROWS;
+  const long long total = (N / n) * nseg;
+  const bool small = N <= 0xffffffffLL;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long u, rest;
+    int seg;
+    if (small) {
+      const unsigned ut = (unsigned)t, usa = (unsigned)sa;
+      const unsigned r32 = ut / usa;
+      u = ut - r32 * usa;
+      const unsigned o32 = r32 / (unsigned)nseg;
+      seg = (int)(r32 - o32 * (unsigned)nseg);
+      rest = o32;
+    } else {
+      u = t % sa;
+      const long long r64 = t / sa;
+      seg = (int)(r64 % nseg);
+      rest = r64 / nseg;
+    }
+    const long long base = rest * (long long)n * sa + u;  // row 0 of the line
+    const int i0 = seg * RS_ROWS;
+    if (i0 >= H && i0 + RS_ROWS + H <= n) {
+      double v[RS_ROWS + 2 * H];
+      const double* q = in + base + (long long)(i0 - H) * sa;
+#pragma unroll
+      for (int k = 0; k < RS_ROWS + 2 * H; ++k) v[k] = q[k * sa];
+      double* o = rhs + base + (long long)i0 * sa;
+#pragma unroll
+      for (int r = 0; r < RS_ROWS; ++r) {
+        const double* c = v + r + H;
+        double x;
+        if (JOB == 0) {
+          if (scheme == WD_C4) x = C4_CA * (c[1] - c[-1]);
+          else x = C6_CA * (c[1] - c[-1]) + C6_CB * (c[2] - c[-2]);
+        } else {
+          const double* hc = fc.hc + 30;
+          x = hc[0] * c[0];
+#pragma unroll
+          for (int k = 1; k <= 5; ++k) x = x + hc[k] * (c[k] + c[-k]);
+        }
+        o[r * sa] = x;
+      }
+      continue;
+    }
+    const Line w{in + base, sa, n, per, off};
+    for (int r = 0; r < RS_ROWS; ++r) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      double x;
+      if (JOB == 0) {
+        x = compact_rhs_at(w, i, n, scheme, per);
+      } else {
+        const int h = per ? 5 : ((i == 0 || i == n - 1) ? 0 : min(min(i, n - 1 - i), 5));
+        if (h == 0) {
+          x = w(i);
+        } else {
+          const double* c = fc.hc + h * 6;
+          x = c[0] * w(i);
+          for (int k = 1; k <= h; ++k) x = x + c[k] * (w(i + k) + w(i - k));
+        }
+      }
+      rhs[base + (long long)i * sa] = x;
+    }
+  }
+}
+
 template <int JOB>
 static __global__ void __launch_bounds__(LS_WARPS * 32, LS_MINB)
     k_line_solve(const double* __restrict__ in, double* y, double* out, Geom g, int axis,
@@ -328,7 +409,11 @@ constexpr size_t kLineSolveMaxSmem = 200 * 1024;
 // chain (one resident CTA per SM) it made every axis slower (measured).
 // Arithmetic and its order are those of k_line_solve (bitwise equal).
 constexpr int LT_P = 33;                     // padded tile row (doubles)
-constexpr int LT_TILE = 32 * LT_P;           // doubles per tile
+#ifndef WD_LT_R
+#define WD_LT_R 32
+#endif
+constexpr int LT_R = WD_LT_R;                // rows per chunk (<= 32)
+constexpr int LT_TILE = LT_R * LT_P;         // doubles per tile
 constexpr int LT_WARP = (LT_EPI ? 4 : 2) * LT_TILE + 64;  // y[2], (acc, c), fcor[32], line pin[32]
 
 __host__ __forceinline__ size_t line_solve_t_smem(int n) {
@@ -417,15 +502,15 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
     double carry = act ? yb[(long long)lane * n] : 0.0;
     double hs = 0.0;
     if (T.cyclic) hs = hs + sh[0] * carry;
-    fetch(wbase, y, 1, min(32, n - 1));
+    fetch(wbase, y, 1, min(LT_R, n - 1));
     lt_commit();
-    for (int r0 = 0, k = 0; r0 < n - 1; r0 += 32, ++k) {
-      const int cnt = min(32, n - 1 - r0);
+    for (int r0 = 0, k = 0; r0 < n - 1; r0 += LT_R, ++k) {
+      const int cnt = min(LT_R, n - 1 - r0);
       double* cur = wbase + (k & 1) * LT_TILE;
       lt_wait<0>();
       __syncwarp();
-      if (r0 + 32 < n - 1)
-        fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0 + 33, min(32, n - 1 - (r0 + 32)));
+      if (r0 + LT_R < n - 1)
+        fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0 + LT_R + 1, min(LT_R, n - 1 - (r0 + LT_R)));
       lt_commit();
       auto step = [&](int t) {
         const int i = r0 + t;
@@ -442,9 +527,9 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
         if (T.cyclic) hs = hs + sh[i + 1] * b;
         cur[t * LT_P + lane] = yv;
       };
-      if (cnt == 32) {
+      if (cnt == LT_R) {
 #pragma unroll 8
-        for (int t = 0; t < 32; ++t) step(t);
+        for (int t = 0; t < LT_R; ++t) step(t);
       } else {
         for (int t = 0; t < cnt; ++t) step(t);
       }
@@ -469,20 +554,20 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
       if (LT_EPI && need_c) fetch(tc, epi.cfield, r0, cnt);
     };
     {
-      const int r0 = max(0, n - 32);
+      const int r0 = max(0, n - LT_R);
       fetch(wbase, y, r0, n - r0);
       lt_commit();
       fetch_epi(r0, n - r0);
       lt_commit();
     }
-    for (int rt = n, k = 0; rt > 0; rt -= 32, ++k) {
-      const int r0 = max(0, rt - 32);
+    for (int rt = n, k = 0; rt > 0; rt -= LT_R, ++k) {
+      const int r0 = max(0, rt - LT_R);
       const int cnt = rt - r0;
       double* cur = wbase + (k & 1) * LT_TILE;
       lt_wait<1>();  // y of this chunk
       __syncwarp();
       if (r0 > 0) {
-        const int r0n = max(0, r0 - 32);
+        const int r0n = max(0, r0 - LT_R);
         fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0n, r0 - r0n);
       }
       lt_commit();
@@ -533,7 +618,7 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
       }
       __syncwarp();
       if (r0 > 0) {
-        const int r0n = max(0, r0 - 32);
+        const int r0n = max(0, r0 - LT_R);
         fetch_epi(r0n, r0 - r0n);
       }
       lt_commit();
