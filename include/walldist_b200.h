@@ -175,6 +175,20 @@ int wd_compute_metrics(const double* coords_dev, double* metrics_dev, double* ja
 int wd_linf_delta(const double* a_dev, const double* b_dev, const unsigned char* mask_dev,
                   long long n, double* out_host, void* stream);
 
+/* ---- validation (reference metrics.py) ---------------- */
+/* metrics.py:20-34 sampled_wall_distance: out[i] = min_m |p_i - w_m|,
+ * points (n, d) and wall samples (m, d) row-major, d <= 3; bit-identical
+ * to the reference's numpy evaluation.                                   */
+int wd_sampled_wall_distance(const double* points_dev, long long n, const double* wall_dev,
+                             long long m, int d, double* out_dev, void* stream);
+/* metrics.py:54-66 l2_norm: sqrt(sum (1/J) (phi - exact)^2); jac_dev NULL
+ * -> the constant jac_const.  Deterministic reduction -> *out_host.       */
+int wd_l2_norm(const double* phi_dev, const double* exact_dev, const double* jac_dev,
+               double jac_const, long long n, double* out_host, void* stream);
+/* metrics.py:121-124 gradient_magnitude: |grad phi| = sqrt(sum_m U_m^2)
+ * with the context's (central) scheme and metrics.                       */
+int wd_gradient_magnitude(wd_ctx* ctx, const double* phi_dev, double* out_dev);
+
 /* ---- slab decomposition (EXTENSION; paper_2111_09859_b200/dist.py) ----
  * The context is created for a rank's ghosted slab (nl + 2G, n1, n2) with
  * axis 0 non-periodic; the host exchanges ghost planes between stages and

@@ -109,6 +109,9 @@ SIGNATURES = {
     "wd_solve_tridiagonal": (_I, [_DP, _DP, _DP, _P, _I, _I, _P]),
     "wd_compute_metrics": (_I, [_P, _P, _P, _I, _IP, _I, _IP, _DP, _P]),
     "wd_linf_delta": (_I, [_P, _P, _P, ctypes.c_longlong, _DP, _P]),
+    "wd_sampled_wall_distance": (_I, [_P, ctypes.c_longlong, _P, ctypes.c_longlong, _I, _P, _P]),
+    "wd_l2_norm": (_I, [_P, _P, _P, ctypes.c_double, ctypes.c_longlong, _DP, _P]),
+    "wd_gradient_magnitude": (_I, [_P, _P, _P]),
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
     "wd_kernel_words": (_I, [_P, _I]),

@@ -16,6 +16,7 @@
 #include "wd_kernels.cuh"
 #include "wd_line_sweep.cuh"
 #include "wd_fused.cuh"
+#include "wd_metrics.cuh"
 
 using namespace wd;
 
@@ -1270,6 +1271,52 @@ int wd_linf_delta(const double* a, const double* b, const unsigned char* mask, l
   double v;
   std::memcpy(&v, &h, sizeof(v));
   *out = v;
+  return WD_OK;
+}
+
+int wd_sampled_wall_distance(const double* pts, long long n, const double* wall, long long m,
+                             int d, double* out, void* stream) {
+  if (!pts || !wall || !out || n < 0 || m < 1 || d < 1 || d > 3)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  if (n == 0) return WD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long per_cta = (long long)MP_T * MP_PTS;
+  const int blocks = (int)((n + per_cta - 1) / per_cta);
+  if (d == 1) k_sampled_distance<1><<<blocks, MP_T, 0, s>>>(pts, n, wall, m, out);
+  else if (d == 2) k_sampled_distance<2><<<blocks, MP_T, 0, s>>>(pts, n, wall, m, out);
+  else k_sampled_distance<3><<<blocks, MP_T, 0, s>>>(pts, n, wall, m, out);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_l2_norm(const double* phi, const double* exact, const double* jac, double jac_const,
+               long long n, double* out, void* stream) {
+  if (!phi || !exact || !out || n < 1) return fail(WD_ERR_INVALID, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* dev = nullptr;
+  CK(cudaMallocAsync(&dev, (L2_B + 1) * sizeof(double), s));
+  const int nb = (int)std::min<long long>(L2_B, (n + L2_T - 1) / L2_T);
+  k_l2_partial<<<nb, L2_T, 0, s>>>(phi, exact, jac, jac_const, n, dev + 1);
+  k_l2_final<<<1, L2_T, 0, s>>>(dev + 1, nb, dev);
+  CK(cudaMemcpyAsync(out, dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(dev, s));
+  CK(cudaStreamSynchronize(s));
+  return WD_OK;
+}
+
+int wd_gradient_magnitude(wd_ctx* c, const double* phi, double* out) {
+  if (!c || !phi || !out) return fail(WD_ERR_INVALID, "bad arguments");
+  if (c->sd.scheme == WD_UW) return fail(WD_ERR_INVALID, "gradient_magnitude needs a central scheme");
+  int rc = ensure_generic(c);
+  if (rc != WD_OK) return rc;
+  CK(cudaDeviceSynchronize());
+  launch_dphi(c, phi, nullptr);
+  launch_assemble(c, c->dphi, c->U, c->Uh, nullptr);
+  MVec3 U;
+  for (int a = 0; a < 3; ++a) U.p[a] = c->U[a];
+  k_gradmag<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(U, c->g.N, c->g.nd, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
   return WD_OK;
 }
 

@@ -103,9 +103,39 @@ def converge_c1(spec):
             "reference_iters": 18440}
 
 
+def oracle_rate():
+    """GPU brute-force oracle (metrics.sampled_wall_distance): C3's 1025 x 513
+    bump-grid nodes against a 20,001-sample wall polyline (the reference's
+    BumpParams.wall_polyline default density), fp64, bit-identical to the
+    reference.  Roofline: fp64 issue (no FMA in the distance expression:
+    2 sub + 2 mul + 1 add + 1 min per pair in 2-D)."""
+    import torch
+    import paper_2111_09859_b200 as W
+    from paper_2111_09859_b200 import metrics as M
+    g = W.build_sinusoidal_bump(1025, 513, scheme="E6")
+    pts = torch.from_numpy(np.ascontiguousarray(g.coords.reshape(2, -1).T)).to("cuda")
+    xs = np.linspace(0.0, 4.0, 20001)
+    wall = torch.from_numpy(np.stack([xs, 0.1 * np.sin(2 * np.pi * xs)], axis=1)).to("cuda")
+    M.sampled_wall_distance(pts, wall)
+    torch.cuda.synchronize()
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        M.sampled_wall_distance(pts, wall)
+    torch.cuda.synchronize()
+    secs = (time.perf_counter() - t0) / reps
+    pairs = pts.shape[0] * wall.shape[0]
+    ops = 6.0 * pairs
+    props = torch.cuda.get_device_properties(0)
+    peak = props.multi_processor_count * 64 * 1.965e9  # fp64 lanes x max clock
+    return {"case": "oracle_c3", "label": "sampled_wall_distance: 525,825 nodes x 20,001 wall samples",
+            "ms": round(secs * 1e3, 3), "pairs_per_s": pairs / secs, "fp64_ops_per_s": ops / secs,
+            "fp64_issue_peak": peak, "frac": round(ops / secs / peak, 4)}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", default="c1,c2,c3,c3lad,c3eik,c5,c5p,c4exact")
+    ap.add_argument("--cases", default="c1,c2,c3,c3lad,c3eik,c5,c5p,c4exact,oracle")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=None)
@@ -115,6 +145,8 @@ def main():
     allc = cases()
     rows = []
     for name in args.cases.split(","):
+        if name not in allc:
+            continue
         spec = allc[name]
         K = args.steps if int(np.prod(spec[0].dims)) > 10**6 else args.steps * 50
         for arith in ("exact", "fast"):
@@ -125,6 +157,10 @@ def main():
             rows.append(r)
             if r["path"] == "generic" and arith == "exact":
                 break  # the generic path has one arithmetic
+    if "oracle" in args.cases.split(","):
+        r = oracle_rate()
+        print(json.dumps(r), flush=True)
+        rows.append(r)
     if "c1" in args.cases.split(","):
         r = converge_c1(allc["c1"])
         print(json.dumps(r), flush=True)
