@@ -188,6 +188,11 @@ int wd_l2_norm(const double* phi_dev, const double* exact_dev, const double* jac
 /* metrics.py:121-124 gradient_magnitude: |grad phi| = sqrt(sum_m U_m^2)
  * with the context's (central) scheme and metrics.                       */
 int wd_gradient_magnitude(wd_ctx* ctx, const double* phi_dev, double* out_dev);
+/* levelset.py:169-202 levelset_step: one RK4 step of
+ * d phi_s / dt = source - F |grad phi_s| with zero-gradient (far-field)
+ * faces; the context is created with every face far-field.               */
+int wd_levelset_step(wd_ctx* ctx, const double* phi_dev, double* out_dev, double F, double dt,
+                     double source);
 
 /* ---- slab decomposition (EXTENSION; paper_2111_09859_b200/dist.py) ----
  * The context is created for a rank's ghosted slab (nl + 2G, n1, n2) with

@@ -112,6 +112,7 @@ SIGNATURES = {
     "wd_sampled_wall_distance": (_I, [_P, ctypes.c_longlong, _P, ctypes.c_longlong, _I, _P, _P]),
     "wd_l2_norm": (_I, [_P, _P, _P, ctypes.c_double, ctypes.c_longlong, _DP, _P]),
     "wd_gradient_magnitude": (_I, [_P, _P, _P]),
+    "wd_levelset_step": (_I, [_P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
     "wd_kernel_words": (_I, [_P, _I]),

@@ -1306,7 +1306,6 @@ int wd_l2_norm(const double* phi, const double* exact, const double* jac, double
 
 int wd_gradient_magnitude(wd_ctx* c, const double* phi, double* out) {
   if (!c || !phi || !out) return fail(WD_ERR_INVALID, "bad arguments");
-  if (c->sd.scheme == WD_UW) return fail(WD_ERR_INVALID, "gradient_magnitude needs a central scheme");
   int rc = ensure_generic(c);
   if (rc != WD_OK) return rc;
   CK(cudaDeviceSynchronize());
@@ -1315,6 +1314,38 @@ int wd_gradient_magnitude(wd_ctx* c, const double* phi, double* out) {
   MVec3 U;
   for (int a = 0; a < 3; ++a) U.p[a] = c->U[a];
   k_gradmag<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(U, c->g.N, c->g.nd, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+int wd_levelset_step(wd_ctx* c, const double* p0, double* out, double F, double dt,
+                     double source) {
+  if (!c || !p0 || !out || p0 == out) return fail(WD_ERR_INVALID, "bad arguments");
+  int rc = ensure_generic(c);
+  if (rc != WD_OK) return rc;
+  CK(cudaDeviceSynchronize());
+  const Geom& g = c->g;
+  const int nb = nblocks(g.N, kThreads);
+  MVec3 U;
+  for (int a = 0; a < 3; ++a) U.p[a] = c->U[a];
+  // rate(p) -> k (levelset.py:185-188)
+  auto rate = [&](const double* p, double* k) {
+    launch_dphi(c, p, nullptr);
+    launch_assemble(c, c->dphi, c->U, c->Uh, nullptr);
+    k_ls_rate<<<nb, kThreads, 0, c->stream>>>(U, g.N, g.nd, F, source, k);
+  };
+  // classical RK4 with the Neumann (far-field) BC on every stage
+  // (levelset.py:190-199): the solver's stage kernels with dt as a field
+  k_fill<<<nb, kThreads, 0, c->stream>>>(c->dt, dt, g.N);
+  rate(p0, c->acc);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(1, p0, c->dt, c->acc, c->acc, c->p, g, nullptr);
+  rate(c->p, c->k);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(2, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
+  rate(c->p, c->k);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(3, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
+  rate(c->p, c->k);
+  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, p0, c->dt, c->k, c->acc, out, g, nullptr);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
   return WD_OK;

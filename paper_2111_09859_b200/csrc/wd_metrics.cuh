@@ -108,4 +108,21 @@ __global__ void k_gradmag(MVec3 U, long long N, int nd, double* __restrict__ out
   }
 }
 
+// levelset.py:169-202 rate(p) = source - F |grad p|, |grad p| as above
+__global__ void k_ls_rate(MVec3 U, long long N, int nd, double F, double source,
+                          double* __restrict__ k) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = U.p[0][i] * U.p[0][i];
+    for (int a = 1; a < nd; ++a) s = s + U.p[a][i] * U.p[a][i];
+    k[i] = source - F * sqrt(s);
+  }
+}
+
+__global__ void k_fill(double* __restrict__ out, double v, long long N) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
 }  // namespace wd
