@@ -4,6 +4,15 @@
 #include <vector>
 
 #include "wd_stage_fast.cuh"
+#include "wd_stage_fast4.cuh"
+
+// interior tiles of stage s run k_f3_fast4 (two j rows per thread) when bit
+// s-1 of WD_S4 is set.  A/B (same box, 512^3): stages 3 / 4 faster with
+// fast4 (0.94 -> 0.84 / 1.04 -> 1.02 ms), stages 1 / 2 slower (1.00 -> 1.05,
+// 1.01 -> 1.06 ms: dt quotient / k1 reciprocal at 8 warps per SM).
+#ifndef WD_S4
+#define WD_S4 12
+#endif
 
 namespace wd {
 
@@ -54,6 +63,9 @@ bool fast3_prepare() {
   auto set = [&](const void* f) {
     return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess;
   };
+  if (WD_S4 != 0 && !(set((const void*)k_f3_fast4<3, EIK, 1>) && set((const void*)k_f3_fast4<3, EIK, 2>) &&
+                 set((const void*)k_f3_fast4<3, EIK, 3>) && set((const void*)k_f3_fast4<3, EIK, 4>)))
+    return false;
   return set((const void*)k_f3_fast3<3, EIK, 1, false>) && set((const void*)k_f3_fast3<3, EIK, 2, false>) &&
          set((const void*)k_f3_fast3<3, EIK, 3, false>) && set((const void*)k_f3_fast3<3, EIK, 4, false>) &&
          set((const void*)k_f3_fast3<3, EIK, 1, true>) && set((const void*)k_f3_fast3<3, EIK, 2, true>) &&
@@ -73,6 +85,15 @@ void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks,
       case 2: k_f3_fast3<3, EIK, 2, true><<<blocks, 256, sm, s>>>(a, tiles); break;
       case 3: k_f3_fast3<3, EIK, 3, true><<<blocks, 256, sm, s>>>(a, tiles); break;
       default: k_f3_fast3<3, EIK, 4, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+    }
+    return;
+  }
+  if ((WD_S4 >> (stage - 1)) & 1) {
+    switch (stage) {
+      case 1: k_f3_fast4<3, EIK, 1><<<blocks, 128, sm, s>>>(a, tiles); break;
+      case 2: k_f3_fast4<3, EIK, 2><<<blocks, 128, sm, s>>>(a, tiles); break;
+      case 3: k_f3_fast4<3, EIK, 3><<<blocks, 128, sm, s>>>(a, tiles); break;
+      default: k_f3_fast4<3, EIK, 4><<<blocks, 128, sm, s>>>(a, tiles); break;
     }
     return;
   }
