@@ -15,8 +15,11 @@
 
 namespace wd {
 
+#ifndef WD_S4_MINB
+#define WD_S4_MINB 2
+#endif
 template <int R, bool EIK, int STAGE>
-__global__ void __launch_bounds__(128, 2) k_f3_fast4(F3Args a, const int* tiles) {
+__global__ void __launch_bounds__(128, WD_S4_MINB) k_f3_fast4(F3Args a, const int* tiles) {
   static_assert(S3_LS && !S3_REG, "k_f3_fast4 implements the low-storage, shared-memory variant");
   using LY = S3Layout<R>;
   constexpr int H = LY::H;
