@@ -182,3 +182,14 @@ def int_array(vals):
 
 def double_array(vals):
     return (ctypes.c_double * len(vals))(*[float(v) for v in vals])
+
+
+def to_host(t):
+    """Device tensor -> numpy through page-locked memory (torch's caching
+    host allocator).  A device-to-pageable copy of a 1 GB field runs at
+    ~2 GB/s (the driver stages it); into pinned memory it is a single DMA at
+    PCIe speed (~45 GB/s measured: 470 -> 23 ms at 512^3)."""
+    import torch
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()

@@ -266,7 +266,7 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
         nat.check(lib.wd_finish(ctx.ptr))
         iters = st.iters
         res = hist[:iters].cpu().numpy().copy()
-        report = SolveReport(phi=phi if device_result else phi.cpu().numpy(), iters=iters,
+        report = SolveReport(phi=phi if device_result else nat.to_host(phi), iters=iters,
                              residual_history=res, wall_seconds=np.asarray(seconds[:iters]),
                              converged=st.state == nat.STATE_CONVERGED,
                              l2_history=np.asarray(l2_samples) if l2_samples else None)
@@ -274,7 +274,7 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
             out = ctx.empty()
             nat.check(lib.wd_poisson_post(ctx.ptr, phi.data_ptr(), out.data_ptr()))
             report.phi_prime = report.phi
-            report.phi = out if device_result else out.cpu().numpy()
+            report.phi = out if device_result else nat.to_host(out)
         return report
     finally:
         ctx.close()

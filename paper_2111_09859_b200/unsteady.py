@@ -15,6 +15,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native as nat
 from .errors import BodyOutsideDomainError
 from .solver import (FARFIELD, WALL, _FACE_NAMES, BoundarySpec, SolveConfig, SolveReport,
                      all_wall_faces, solve_steady)
@@ -117,9 +118,9 @@ def solve_unsteady(grid, motion: MotionSpec, config: SolveConfig, n_steps: int,
         bnd = BoundarySpec(faces=dict(faces), solid_mask=motion.body_mask(grid, t))
         rep = solve_steady(grid, bnd, config, phi0=phi, device_result=True)
         phi = rep.phi
-        rep.phi = phi.cpu().numpy()
+        rep.phi = nat.to_host(phi)
         if rep.phi_prime is not None:
-            rep.phi_prime = rep.phi_prime.cpu().numpy()
+            rep.phi_prime = nat.to_host(rep.phi_prime)
         rep.time = t
         reports.append(rep)
     return reports
