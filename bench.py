@@ -244,7 +244,7 @@ def run_b200_dist(args, world, rank, local):
     K, Wm = args.steps, args.warmup
     comm = dist.TorchComm()
     ds = dist.DistributedSolve(dims, sp, cfg["faces"], cfg["scheme"], fc, filt, 0.5, 1e-15,
-                               K + Wm + 8, args.arith, comm, [rank])
+                               K + Wm + 8, args.arith, comm, [rank], filter0=args.filter0)
     nl = dims[0] // world
     ds.set_state([torch.zeros((nl, dims[1], dims[2]), dtype=torch.float64, device="cuda")])
     for _ in range(Wm):
@@ -279,6 +279,7 @@ def run_b200_dist(args, world, rank, local):
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "dims": list(dims), "arith": args.arith,
                        "global_nodes": N, "parallelism": f"slab{world}",
+                       "axis0_filter": ds.filter0,
                        "l2": "inputs larger than L2"},
             "roofline": None,
             "step_roofline": {"achieved_per_gpu": round(step_ach, 1), "peak": peak, "unit": "GB/s",
@@ -446,6 +447,8 @@ def main():
                          "within 1e-10); exact: bit-identical to the reference algorithm")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-mode side run")
     ap.add_argument("--dist", action="store_true", help="slab-decomposed path even at N=1")
+    ap.add_argument("--filter0", default=None, choices=["partitioned", "transpose"],
+                    help="decomposed axis-0 filter (default: partitioned in fast arithmetic)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

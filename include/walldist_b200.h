@@ -214,6 +214,16 @@ int wd_dist_pack(const double* slab_dev, double* buf_dev, int nl, int n1, int n2
 int wd_dist_unpack(const double* buf_dev, double* slab_dev, int nl, int n1, int n2, int P,
                    void* stream);
 /* status maxima -> dev3 (int64 x3) for all_reduce(max); then finalize    */
+/* Partitioned axis-0 filter (fast arithmetic; wd_dist_filter0.cuh): the
+ * rank's rows [rank nl, (rank+1) nl) of the n0-long periodic lines, three
+ * phases around two all_gathers of per-line carries.  in: ghosted slab
+ * (nl + 2G, n1, n2), G >= 5 ghosts filled; out: interior (nl, n1, n2).
+ * phase 1 writes mine[2][n1 n2] (Y_blk, h.rhs); phase 2 reads xa =
+ * gathered phase-1 slots [P][2][n1 n2], writes out (x') and mine[n1 n2]
+ * (X_blk); phase 3 reads xa and xb = gathered phase-2 slots [P][n1 n2].   */
+int wd_dist_filter0(wd_ctx* ctx, int phase, const double* in_dev, double* out_dev, int n0,
+                    int n1, int n2, int G, int P, int rank, const double* xa_dev,
+                    const double* xb_dev, double* mine_dev);
 int wd_dist_stats(wd_ctx* ctx, long long* dev3);
 int wd_dist_finalize(wd_ctx* ctx, const long long* dev3);
 

@@ -121,6 +121,7 @@ SIGNATURES = {
     "wd_dist_filter": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _P]),
     "wd_dist_pack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "wd_dist_unpack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "wd_dist_filter0": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "wd_dist_stats": (_I, [_P, _P]),
     "wd_dist_finalize": (_I, [_P, _P]),
 }

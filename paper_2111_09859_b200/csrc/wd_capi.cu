@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -17,6 +18,7 @@
 #include "wd_line_sweep.cuh"
 #include "wd_fused.cuh"
 #include "wd_metrics.cuh"
+#include "wd_dist_filter0.cuh"
 
 using namespace wd;
 
@@ -351,6 +353,8 @@ struct wd_ctx {
   FusedPlan fused;    // specialised kernels (wd_fused.cuh), if applicable
   // distributed path: filter factors for arbitrary (length, periodic)
   std::map<std::pair<int, int>, std::pair<HostFactor, double*>> dfilt;
+  // partitioned axis-0 filter tables per (n0, P, rank) (wd_dist_filter0.cuh)
+  std::map<std::tuple<int, int, int>, std::pair<D0Tables, double*>> d0tab;
 };
 
 namespace {
@@ -870,6 +874,7 @@ int wd_destroy(wd_ctx* c) {
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   fused_release(c->fused);
   for (auto& kv : c->dfilt) cudaFree(kv.second.second);
+  for (auto& kv : c->d0tab) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
   cudaFree(c->ws);
@@ -1458,6 +1463,78 @@ int wd_dist_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, i
   }
   fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream,
                    SD.n ? &SD : nullptr);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+int wd_dist_filter0(wd_ctx* c, int phase, const double* in, double* out, int n0, int n1, int n2,
+                    int G, int P, int rank, const double* xa, const double* xb, double* mine) {
+  if (!c || !c->fused.active || !c->sd.use_filter || phase < 1 || phase > 3 || P < 1 ||
+      rank < 0 || rank >= P || n0 % P || !in || !out || !mine)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  const int nl = n0 / P;
+  if (G < 5) return fail(WD_ERR_INVALID, "the axis-0 filter needs 5 ghost planes");
+  auto key = std::make_tuple(n0, P, rank);
+  auto it = c->d0tab.find(key);
+  if (it == c->d0tab.end()) {
+    HostFactor F;
+    int rc = filter_factor(c->sd.alpha_f, n0, 1, F);
+    if (rc) return rc;
+    for (double sw : F.swap)
+      if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
+    // global rows (the scan_pack conventions): fm, 1/d, g, h, z
+    std::vector<double> fm(n0), ri(n0), g(n0), h(n0), z(n0);
+    for (int r = 0; r < n0; ++r) {
+      fm[r] = r > 0 ? F.fact[r - 1] : 0.0;
+      ri[r] = 1.0 / F.d[r];
+      g[r] = r < n0 - 1 ? F.du[r] * ri[r] : 0.0;
+      h[r] = F.cyclic ? F.h[r] : 0.0;
+      z[r] = F.cyclic ? F.z[r] : 0.0;
+    }
+    std::vector<double> tab((size_t)6 * nl + 2 * P);
+    const int lo = rank * nl;
+    for (int r = 0; r < nl; ++r) {
+      tab[r] = fm[lo + r];
+      tab[nl + r] = ri[lo + r];
+      tab[2 * nl + r] = g[lo + r];
+      tab[3 * nl + r] = h[lo + r];
+      tab[4 * nl + r] = z[lo + r];
+    }
+    double qp = 1.0;  // Qpref_r = prod_{t = r}^{hi - 1} (-g_t)
+    for (int r = nl - 1; r >= 0; --r) {
+      qp *= -g[lo + r];
+      tab[5 * nl + r] = qp;
+    }
+    for (int q = 0; q < P; ++q) {
+      double pb = 1.0, qb = 1.0;
+      for (int r = q * nl; r < (q + 1) * nl; ++r) {
+        pb *= -fm[r];
+        qb *= -g[r];
+      }
+      tab[6 * nl + 2 * q] = pb;
+      tab[6 * nl + 2 * q + 1] = qb;
+    }
+    double* dev = nullptr;
+    CK(cudaMalloc(&dev, tab.size() * sizeof(double)));
+    CK(cudaMemcpy(dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    D0Tables T;
+    T.row = dev;
+    T.blk = dev + 6 * nl;
+    T.P = P;
+    T.rank = rank;
+    T.nl = nl;
+    T.denom = F.cyclic ? F.denom : 0.0;
+    it = c->d0tab.emplace(key, std::make_pair(T, dev)).first;
+  }
+  const D0Tables& T = it->second.first;
+  const long long lines = (long long)n1 * n2;
+  const int blocks = nblocks(lines, 128);
+  if (phase == 1)
+    k_dist_filter0<1><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
+  else if (phase == 2)
+    k_dist_filter0<2><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
+  else
+    k_dist_filter0<3><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
   CK(cudaGetLastError());
   return WD_OK;
 }

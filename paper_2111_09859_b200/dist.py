@@ -8,14 +8,22 @@ One pseudo-step:
 * before each RK stage, exchange the stage input's ghost planes with both
   ring neighbours (``send/recv``, NCCL over NVLink);
 * run the fused stage kernel on the slab interior (``wd_dist_stage``);
-* filter axis 0 exactly on full x-lines: pack the slab into P chunks,
-  ``all_to_all`` to pencils ``(n0, n1/P, n2)``, sweep, ``all_to_all`` back;
+* filter axis 0 on full x-lines.  Exact arithmetic: pack the slab into P
+  chunks, ``all_to_all`` to pencils ``(n0, n1/P, n2)``, sweep, ``all_to_all``
+  back (bit-identical to one GPU).  Fast arithmetic (default there): the
+  partitioned solve of ``csrc/wd_dist_filter0.cuh`` -- ghost exchange of the
+  filter input, then per line one forward carry and one backward carry
+  ``all_gather``-ed between three local kernels (2 + 1 doubles per line per
+  rank instead of two transposes of the whole slab: ~6 MB vs ~234 MB per GPU
+  and step at 512^3, P = 8);
 * filter axes 1 and 2 on the slab; the last sweep accumulates the local
   ``max|Δφ|``, ``max|φ|`` and non-finite flag;
 * ``all_reduce(max)`` of those three words, then the stop test.
 
-Every node and every filter line sees exactly the operations of the
-single-GPU path, so the decomposed solve is bit-identical to it (checked by
+With the transposed axis-0 filter every node and every filter line sees
+exactly the operations of the single-GPU path, so the decomposed solve is
+bit-identical to it; the partitioned filter solves the same linear system
+with another association (round-off level; checked by
 ``tests/test_gpu_dist.py`` with P simulated ranks on one GPU).
 """
 from __future__ import annotations
@@ -116,6 +124,14 @@ class TorchComm:
             return
         self.dist.all_to_all_single(o, i, group=self.group)
 
+    def allgather(self, outs, ins):
+        """outs[0] (P * len(ins[0]),) <- every rank's ins[0], rank order."""
+        (o,), (i,) = outs, ins
+        if self.P == 1:
+            o.copy_(i)
+            return
+        self.dist.all_gather_into_tensor(o, i, group=self.group)
+
     def allreduce_max(self, ts):
         (t,) = ts
         if self.P > 1:
@@ -147,6 +163,13 @@ class LocalComm:
             for s in range(P):
                 ov[s].copy_(chunks[s][r])
 
+    def allgather(self, outs, ins):
+        P = self.P
+        for o in outs:
+            ov = o.view(P, -1)
+            for s_ in range(P):
+                ov[s_].copy_(ins[s_])
+
     def allreduce_max(self, ts):
         import torch
         m = torch.stack(list(ts)).max(dim=0).values
@@ -160,7 +183,7 @@ class DistributedSolve:
     local logical rank: 1 under torchrun, P in the simulated mode)."""
 
     def __init__(self, dims, spacing, faces, scheme, formulation, filter_config, cfl, tol,
-                 max_iters, arith, comm, ranks, ref_length=1.0):
+                 max_iters, arith, comm, ranks, ref_length=1.0, filter0=None):
         import torch
         from ._context import NativeSolver
         from .grid import CurvilinearGrid
@@ -209,6 +232,17 @@ class DistributedSolve:
         self.slab1 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
         self.slab2 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
         self.stats = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(R)]
+        # axis-0 filter: "partitioned" (fast arithmetic) or "transpose"
+        self.filter0 = filter0 or ("partitioned" if arith == "fast" else "transpose")
+        if self.filter0 not in ("partitioned", "transpose"):
+            raise ValueError(f"unknown axis-0 filter mode {self.filter0!r}")
+        if self.filter0 == "partitioned" and arith != "fast":
+            raise ValueError("the partitioned axis-0 filter is a fast-arithmetic path")
+        lines = n1 * n2
+        self.mineA = [torch.empty(2 * lines, **f64) for _ in range(R)]
+        self.mineB = [torch.empty(lines, **f64) for _ in range(R)]
+        self.gathA = [torch.empty(P * 2 * lines, **f64) for _ in range(R)]
+        self.gathB = [torch.empty(P * lines, **f64) for _ in range(R)]
         for ctx in self.ctxs:
             h = torch.zeros(max(max_iters, 1), **f64)
             self.hists.append(h)
@@ -257,7 +291,60 @@ class DistributedSolve:
                 nat.check(lib.wd_dist_stage(self.ctxs[r].ptr, s + 1, self.A[r].data_ptr(),
                                             bufs[s][r].data_ptr(), outs[s][r].data_ptr()))
         streams = [self.ctxs[r].lib.wd_get_stream(self.ctxs[r].ptr) for r in range(R)]
-        # axis-0 filter on pencils (n0, n1/P, n2)
+        if self.filter0 == "partitioned":
+            self._filter0_partitioned()
+        else:
+            self._filter0_transpose(streams)
+        for r in range(R):
+            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 1, self.slab1[r].data_ptr(),
+                                         self.slab2[r].data_ptr(), nl, n1, n2,
+                                         int(self.per[1]), None))
+            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 2, self.slab2[r].data_ptr(),
+                                         self._interior(self.B[r]).data_ptr(), nl, n1, n2,
+                                         int(self.per[2]), self._interior(self.A[r]).data_ptr()))
+            nat.check(lib.wd_dist_stats(self.ctxs[r].ptr, self.stats[r].data_ptr()))
+        self._sync()
+        comm.allreduce_max(self.stats)
+        self._sync()
+        for r in range(R):
+            nat.check(lib.wd_dist_finalize(self.ctxs[r].ptr, self.stats[r].data_ptr()))
+        self.A, self.B = self.B, self.A
+
+    def _filter0_partitioned(self):
+        """Axis-0 filter of the stage-4 output Pb -> slab1, rows split over
+        the ranks (wd_dist_filter0: three local phases, two all_gathers)."""
+        lib, comm = self.lib, self.comm
+        n0, n1, n2 = self.dims
+        P = comm.P
+        R = len(self.ctxs)
+        self._sync()
+        comm.halo(self.Pb, self.slabs[0])
+        self._sync()
+
+        def phase(ph, mine):
+            for r in range(R):
+                nat.check(lib.wd_dist_filter0(
+                    self.ctxs[r].ptr, ph, self.Pb[r].data_ptr(), self.slab1[r].data_ptr(), n0,
+                    n1, n2, self.G, P, self.slabs[r].rank, self.gathA[r].data_ptr(),
+                    self.gathB[r].data_ptr(), mine[r].data_ptr()))
+        phase(1, self.mineA)
+        self._sync()
+        comm.allgather(self.gathA, self.mineA)
+        self._sync()
+        phase(2, self.mineB)
+        self._sync()
+        comm.allgather(self.gathB, self.mineB)
+        self._sync()
+        phase(3, self.mineB)
+
+    def _filter0_transpose(self, streams):
+        """Axis-0 filter on pencils (n0, n1/P, n2): pack, all_to_all, sweep,
+        all_to_all back, unpack -> slab1 (bit-identical to one GPU)."""
+        lib, comm = self.lib, self.comm
+        n0, n1, n2 = self.dims
+        P, nl = comm.P, self.nl
+        m1 = n1 // P
+        R = len(self.ctxs)
         for r in range(R):
             x = self._interior(self.Pb[r])
             nat.check(lib.wd_dist_pack(x.data_ptr(), self.send[r].data_ptr(), nl, n1, n2, P,
@@ -274,19 +361,6 @@ class DistributedSolve:
         for r in range(R):
             nat.check(lib.wd_dist_unpack(self.back[r].data_ptr(), self.slab1[r].data_ptr(), nl,
                                          n1, n2, P, streams[r]))
-            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 1, self.slab1[r].data_ptr(),
-                                         self.slab2[r].data_ptr(), nl, n1, n2,
-                                         int(self.per[1]), None))
-            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 2, self.slab2[r].data_ptr(),
-                                         self._interior(self.B[r]).data_ptr(), nl, n1, n2,
-                                         int(self.per[2]), self._interior(self.A[r]).data_ptr()))
-            nat.check(lib.wd_dist_stats(self.ctxs[r].ptr, self.stats[r].data_ptr()))
-        self._sync()
-        comm.allreduce_max(self.stats)
-        self._sync()
-        for r in range(R):
-            nat.check(lib.wd_dist_finalize(self.ctxs[r].ptr, self.stats[r].data_ptr()))
-        self.A, self.B = self.B, self.A
 
     def _sync(self):
         """Simulated ranks use one stream per logical rank: order them

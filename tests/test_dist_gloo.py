@@ -1,7 +1,8 @@
 """The slab decomposition's host-side communication (dist.TorchComm) with
 world_size 2 over gloo on CPU: ghost-plane ring exchange, slab <-> pencil
 all_to_all (the axis-0 filter transpose) and the all_reduce(max) of the
-convergence words reassemble the global field exactly."""
+convergence words reassemble the global field exactly; the all_gather of
+the partitioned axis-0 filter's per-line carries arrives in rank order."""
 import os
 import socket
 
@@ -51,10 +52,15 @@ def _worker(rank, world, port, dims, q):
         comm.alltoall([back], [torch.from_numpy(pencil.ravel().copy())])
         unpacked = back.numpy().reshape(world, nl, m1, n2).transpose(1, 0, 2, 3).reshape(nl, n1, n2)
         ok_back = np.array_equal(unpacked, interior)
+        # per-line carries of the partitioned axis-0 filter: all_gather
+        mine = torch.full((6,), float(rank + 1), dtype=torch.float64)
+        gath = torch.empty(6 * world, dtype=torch.float64)
+        comm.allgather([gath], [mine])
+        ok_gather = gath.view(world, 6)[:, 0].tolist() == [float(r + 1) for r in range(world)]
         stats = torch.tensor([rank * 10 + 3, 7 - rank, rank], dtype=torch.int64)
         comm.allreduce_max([stats])
         ok_red = stats.tolist() == [(world - 1) * 10 + 3, 7, world - 1]
-        q.put((rank, ok_halo, ok_pencil, ok_back, ok_red))
+        q.put((rank, ok_halo, ok_pencil, ok_back, ok_red, ok_gather))
     finally:
         tdist.destroy_process_group()
 

@@ -1,5 +1,7 @@
 """Slab-decomposed solve (dist.py) with P logical ranks on one GPU against
-the single-GPU fused solve: bit-identical state and residual history."""
+the single-GPU fused solve: bit-identical state and residual history with
+the transposed axis-0 filter; round-off-level agreement with the
+partitioned one (fast arithmetic)."""
 import numpy as np
 import pytest
 
@@ -20,8 +22,7 @@ FACES = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "wall",
          "kmin": "periodic", "kmax": "periodic"}
 
 
-@pytest.mark.parametrize("P,arith", [(1, "exact"), (2, "exact"), (4, "exact"), (2, "fast")])
-def test_decomposed_equals_single(P, arith):
+def _run(P, arith, filter0):
     from paper_2111_09859_b200 import dist
     dims = (32, 48, 64)
     sp = (1.0 / 32, 1.0 / 47, 1.0 / 64)
@@ -38,7 +39,7 @@ def test_decomposed_equals_single(P, arith):
     ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
     comm = dist.LocalComm(P)
     ds = dist.DistributedSolve(dims, sp, FACES, "E6", fc, filt, 0.5, 1e-15, steps, arith, comm,
-                               list(range(P)))
+                               list(range(P)), filter0=filter0)
     n = dims[0] // P
     # the single-GPU path applies the BCs to phi0 first; mirror it
     import torch
@@ -49,9 +50,26 @@ def test_decomposed_equals_single(P, arith):
     for _ in range(steps):
         ds.step()
     got = np.concatenate([s.cpu().numpy() for s in ds.state()], axis=0)
-    assert same(ds.history(0), ref.residual_history)
-    assert same(got, ref.phi)
+    hist = ds.history(0)
     ds.close()
+    return got, hist, ref
+
+
+@pytest.mark.parametrize("P,arith", [(1, "exact"), (2, "exact"), (4, "exact"), (2, "fast")])
+def test_decomposed_equals_single(P, arith):
+    got, hist, ref = _run(P, arith, "transpose")
+    assert same(hist, ref.residual_history)
+    assert same(got, ref.phi)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_partitioned_axis0_filter(P):
+    """Fast arithmetic with the axis-0 filter solved across the ranks
+    (two per-line carry all_gathers instead of two slab transposes)."""
+    got, hist, ref = _run(P, "fast", "partitioned")
+    scale = float(np.max(np.abs(ref.phi)))
+    assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale
+    assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
 
 
 def test_slab_checks():
