@@ -414,10 +414,15 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
   }
   const long long warps = (L + 31) / 32;
   const int blocks = (int)std::min<long long>((warps + LS_WARPS - 1) / LS_WARPS, 148LL * 8);
-  if (g.s[axis] == 1 && axis == g.nd - 1 && line_solve_t_smem(n) <= kLineSolveMaxSmem) {
-    // contiguous lines: transposed cp.async staging (coalesced)
+  // contiguous lines: transposed cp.async staging (coalesced); long strided
+  // lines when there are too few of them to fill the GPU (C3's axis-0
+  // filter: 513 lines of 1025, the chain runs from shared memory with the
+  // next chunk in flight: 1.12 -> 1.04 ms per step; short lines (C2) lose)
+  const bool few = warps < 148LL * 2 * LS_WARPS && n >= 512;
+  if (line_solve_t_smem(n) <= kLineSolveMaxSmem &&
+      ((g.s[axis] == 1 && axis == g.nd - 1) || (few && !getenv("WD_NO_TILED_FEW")))) {
     k_line_solve_t<JOB><<<blocks, LS_WARPS * 32, line_solve_t_smem(n), s>>>(
-        in, scratch, out, g, n, T, e, pin, use_geom_pin, st);
+        in, scratch, out, g, axis, n, g.s[axis], T, e, pin, use_geom_pin, st);
     return;
   }
   k_line_solve<JOB><<<blocks, LS_WARPS * 32, line_solve_smem(n), s>>>(

@@ -432,12 +432,13 @@ __device__ __forceinline__ void lt_wait() {
 
 template <int JOB>
 static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
-    k_line_solve_t(const double* __restrict__ in, double* y, double* out, Geom g, int n, TriDev T,
-                   Epi epi, const uint8_t* pin, int use_geom_pin, const Status* st) {
+    k_line_solve_t(const double* __restrict__ in, double* y, double* out, Geom g, int axis, int n,
+                   long long sa, TriDev T, Epi epi, const uint8_t* pin, int use_geom_pin,
+                   const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
   extern __shared__ double ls_f[];
   const long long L = g.N / n;
-  const int axis = g.nd - 1;
+  const bool contig = sa == 1;
   double* sfact = ls_f;
   double* sswap = sfact + n;
   double* sdu = sswap + n;
@@ -471,22 +472,31 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
   for (long long grp = (long long)blockIdx.x * LS_WARPS + wib; grp * 32 < L; grp += nwarps) {
     const long long q0 = grp * 32;
     const int nl = (int)min(32LL, L - q0);
-    const long long b0 = q0 * n;  // line j starts at b0 + j n
-    double* yb = y + b0;
     const bool act = lane < nl;
+    // contiguous lines: line j starts at b0 + j n; strided: this lane's line
+    const long long b0 = contig ? q0 * n : 0;
+    const long long mybase =
+        contig ? b0 + (long long)lane * n : line_base(g, axis, q0 + (act ? lane : 0));
+    double* yb = y + b0;
     // rows [r, r + cnt) of the block's lines -> tile[row - r][line]
     auto fetch = [&](double* tile, const double* src, int r, int cnt) {
-      if (lane < cnt) {
-        const double* s0 = src + b0 + r + lane;
+      if (contig) {
+        if (lane < cnt) {
+          const double* s0 = src + b0 + r + lane;
 #pragma unroll 8
-        for (int j = 0; j < nl; ++j) lt_cp8(tile + lane * LT_P + j, s0 + (long long)j * n);
+          for (int j = 0; j < nl; ++j) lt_cp8(tile + lane * LT_P + j, s0 + (long long)j * n);
+        }
+      } else if (act) {
+        const double* s0 = src + mybase + (long long)r * sa;
+#pragma unroll 8
+        for (int t = 0; t < cnt; ++t) lt_cp8(tile + t * LT_P + lane, s0 + (long long)t * sa);
       }
     };
     if (JOB == 1 && use_geom_pin) {
       bool lp = false;
       if (act) {
         int c[kMaxDim];
-        node_coords(g, b0 + (long long)lane * n, c);
+        node_coords(g, mybase, c);
 #pragma unroll
         for (int b = 0; b < kMaxDim; ++b) {
           if (b >= g.nd || b == axis) continue;
@@ -499,7 +509,7 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
     // ---------------- forward elimination: chunk k = steps [r0, r0 + cnt),
     // b = rhs rows r0 + 1 .. r0 + cnt in tile slots 0 .. cnt-1, y rows
     // r0 .. r0 + cnt - 1 left in the same slots
-    double carry = act ? yb[(long long)lane * n] : 0.0;
+    double carry = act ? y[mybase] : 0.0;
     double hs = 0.0;
     if (T.cyclic) hs = hs + sh[0] * carry;
     fetch(wbase, y, 1, min(LT_R, n - 1));
@@ -534,15 +544,21 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
         for (int t = 0; t < cnt; ++t) step(t);
       }
       __syncwarp();
-      if (lane < cnt) {
-        double* d0 = yb + r0 + lane;
+      if (contig) {
+        if (lane < cnt) {
+          double* d0 = yb + r0 + lane;
 #pragma unroll 8
-        for (int j = 0; j < nl; ++j) d0[(long long)j * n] = cur[lane * LT_P + j];
+          for (int j = 0; j < nl; ++j) d0[(long long)j * n] = cur[lane * LT_P + j];
+        }
+      } else if (act) {
+        double* d0 = y + mybase + (long long)r0 * sa;
+#pragma unroll 8
+        for (int t = 0; t < cnt; ++t) d0[(long long)t * sa] = cur[t * LT_P + lane];
       }
       __syncwarp();
     }
     lt_wait<0>();
-    if (act) yb[(long long)lane * n + n - 1] = carry;
+    if (act) y[mybase + (long long)(n - 1) * sa] = carry;
     sfc[lane] = T.cyclic ? hs / T.denom : 0.0;
     __syncwarp();
     // ---------------- back substitution, chunks [r0, rt) going down.  Copy
@@ -588,33 +604,38 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
       }
       lt_wait<1>();  // epilogue operands of this chunk
       __syncwarp();
-      if (lane < cnt) {
-        const int r = r0 + lane;
-        const long long i0 = b0 + r;
-#pragma unroll 4
-        for (int j = 0; j < nl; ++j) {
-          const int tj = lane * LT_P + j;
-          const double x = cur[tj];
-          const double xv = T.cyclic ? x - sfc[j] * sz[r] : x;
-          const long long idx = i0 + (long long)j * n;
-          if (JOB == 0) {
-            double o = xv;
-            if (epi.mode != 0) {
-              const double cv = need_c ? (LT_EPI ? tc[tj] : epi.cfield[idx]) : epi.cscal;
-              const double tt = cv * xv;
-              o = epi.mode == 1 ? tt : (need_acc ? (LT_EPI ? ta[tj] : epi.acc[idx]) : 0.0) + tt;
-            }
-            out[idx] = o;
-          } else {
-            bool p;
-            if (use_geom_pin)
-              p = slp[j] != 0.0 || (r == 0 && pin_lo) || (r == n - 1 && pin_hi) ||
-                  (g.mask != nullptr && g.mask[idx] != 0);
-            else
-              p = pin != nullptr && pin[idx] != 0;
-            out[idx] = p ? in[idx] : xv;
+      // node (line j, row r) from tile slot tj
+      auto emit = [&](int j, int r, int tj, long long idx) {
+        const double x = cur[tj];
+        const double xv = T.cyclic ? x - sfc[j] * sz[r] : x;
+        if (JOB == 0) {
+          double o = xv;
+          if (epi.mode != 0) {
+            const double cv = need_c ? (LT_EPI ? tc[tj] : epi.cfield[idx]) : epi.cscal;
+            const double tt = cv * xv;
+            o = epi.mode == 1 ? tt : (need_acc ? (LT_EPI ? ta[tj] : epi.acc[idx]) : 0.0) + tt;
           }
+          out[idx] = o;
+        } else {
+          bool p;
+          if (use_geom_pin)
+            p = slp[j] != 0.0 || (r == 0 && pin_lo) || (r == n - 1 && pin_hi) ||
+                (g.mask != nullptr && g.mask[idx] != 0);
+          else
+            p = pin != nullptr && pin[idx] != 0;
+          out[idx] = p ? in[idx] : xv;
         }
+      };
+      if (contig) {
+        if (lane < cnt) {
+          const int r = r0 + lane;
+#pragma unroll 4
+          for (int j = 0; j < nl; ++j) emit(j, r, lane * LT_P + j, b0 + (long long)j * n + r);
+        }
+      } else if (act) {
+#pragma unroll 4
+        for (int t = 0; t < cnt; ++t)
+          emit(lane, r0 + t, t * LT_P + lane, mybase + (long long)(r0 + t) * sa);
       }
       __syncwarp();
       if (r0 > 0) {
