@@ -587,17 +587,26 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
         fetch(wbase + ((k + 1) & 1) * LT_TILE, y, r0n, r0 - r0n);
       }
       lt_commit();
-      for (int r = rt - 1; r >= r0; --r) {
+      int r = rt - 1;
+      if (r == n - 1) {  // the last two rows first, then a branch-free unrolled body
+        const double x = ls_div(cur[(r - r0) * LT_P + lane], sd[n - 1], srinv[n - 1]);
+        x2 = x1;
+        x1 = x;
+        cur[(r - r0) * LT_P + lane] = x;
+        --r;
+      }
+      if (r == n - 2 && r >= r0) {
+        const double x = ls_div(cur[(r - r0) * LT_P + lane] - sdu[n - 2] * x1, sd[n - 2],
+                                srinv[n - 2]);
+        x2 = x1;
+        x1 = x;
+        cur[(r - r0) * LT_P + lane] = x;
+        --r;
+      }
+#pragma unroll 8
+      for (; r >= r0; --r) {
         const int t = r - r0;
-        const double yv = cur[t * LT_P + lane];
-        double x;
-        if (r == n - 1) {
-          x = ls_div(yv, sd[n - 1], srinv[n - 1]);
-        } else if (r == n - 2) {
-          x = ls_div(yv - sdu[n - 2] * x1, sd[n - 2], srinv[n - 2]);
-        } else {
-          x = ls_div((yv - sdu[r] * x1) - sdu2[r] * x2, sd[r], srinv[r]);
-        }
+        const double x = ls_div((cur[t * LT_P + lane] - sdu[r] * x1) - sdu2[r] * x2, sd[r], srinv[r]);
         x2 = x1;
         x1 = x;
         cur[t * LT_P + lane] = x;
