@@ -537,7 +537,20 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
         if (T.cyclic) hs = hs + sh[i + 1] * b;
         cur[t * LT_P + lane] = yv;
       };
-      if (cnt == LT_R) {
+      // no row interchange in the chunk (every row but 1 and n-2 of the
+      // compact matrices): branch-free body, the carry update as in the
+      // no-swap case of step()
+      bool anysw = false;
+      for (int t = 0; t < cnt; ++t) anysw |= sswap[r0 + t] != 0.0;
+      if (cnt == LT_R && !anysw && !T.cyclic) {
+#pragma unroll 8
+        for (int t = 0; t < LT_R; ++t) {
+          const double b = cur[t * LT_P + lane];
+          const double yv = carry;
+          carry = b - sfact[r0 + t] * carry;
+          cur[t * LT_P + lane] = yv;
+        }
+      } else if (cnt == LT_R) {
 #pragma unroll 8
         for (int t = 0; t < LT_R; ++t) step(t);
       } else {
