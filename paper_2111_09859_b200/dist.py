@@ -97,12 +97,17 @@ class TorchComm:
 
     def halo(self, slabs, slab: Slab):
         """Fill the ghost planes of this rank's (nl + 2G, ...) tensor."""
+        self.halo_finish(self.halo_start(slabs, slab), slabs, slab)
+
+    def halo_start(self, slabs, slab: Slab):
+        """Post the ghost-plane exchange; the caller may enqueue work that
+        does not read the ghost planes before halo_finish."""
         (t,) = slabs
         G, nl = slab.G, slab.nl
         if self.P == 1:
             t[:G].copy_(t[nl:nl + G])
             t[nl + G:].copy_(t[G:2 * G])
-            return
+            return None
         d = self.dist
         lo = t.new_empty(t[:G].shape)
         hi = t.new_empty(t[:G].shape)
@@ -112,10 +117,17 @@ class TorchComm:
                d.P2POp(d.irecv, lo, slab.left, self.group),
                d.P2POp(d.isend, t[G:2 * G].contiguous(), slab.left, self.group),
                d.P2POp(d.irecv, hi, slab.right, self.group)]
-        for req in d.batch_isend_irecv(ops):
+        return d.batch_isend_irecv(ops), lo, hi
+
+    def halo_finish(self, handle, slabs, slab: Slab):
+        if handle is None:
+            return
+        (t,) = slabs
+        reqs, lo, hi = handle
+        for req in reqs:
             req.wait()
-        t[:G].copy_(lo)
-        t[nl + G:].copy_(hi)
+        t[:slab.G].copy_(lo)
+        t[slab.nl + slab.G:].copy_(hi)
 
     def alltoall(self, outs, ins):
         (o,), (i,) = outs, ins
@@ -145,6 +157,13 @@ class LocalComm:
 
     def __init__(self, P):
         self.P = P
+
+    def halo_start(self, slabs, slab: Slab):
+        self.halo(slabs, slab)
+        return None
+
+    def halo_finish(self, handle, slabs, slab: Slab):
+        return None
 
     def halo(self, slabs, slab: Slab):
         G, nl = slab.G, slab.nl
@@ -183,7 +202,7 @@ class DistributedSolve:
     local logical rank: 1 under torchrun, P in the simulated mode)."""
 
     def __init__(self, dims, spacing, faces, scheme, formulation, filter_config, cfl, tol,
-                 max_iters, arith, comm, ranks, ref_length=1.0, filter0=None):
+                 max_iters, arith, comm, ranks, ref_length=1.0, filter0=None, overlap=True):
         import torch
         from ._context import NativeSolver
         from .grid import CurvilinearGrid
@@ -232,6 +251,9 @@ class DistributedSolve:
         self.slab1 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
         self.slab2 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
         self.stats = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(R)]
+        # stage kernels on the planes that need no ghost while the ghost
+        # planes are in flight, then the 2 x G boundary planes
+        self.overlap = bool(overlap) and self.nl >= 2 * self.G + 8
         # axis-0 filter: "partitioned" (fast arithmetic) or "transpose"
         self.filter0 = filter0 or ("partitioned" if arith == "fast" else "transpose")
         if self.filter0 not in ("partitioned", "transpose"):
@@ -283,13 +305,30 @@ class DistributedSolve:
         R = len(self.ctxs)
         bufs = [self.A, self.Pa, self.Pb, self.Pa]
         outs = [self.Pa, self.Pb, self.Pa, self.Pb]
+        G = self.G
         for s in range(4):
             self._sync()
-            comm.halo(bufs[s], self.slabs[0])
-            self._sync()
-            for r in range(R):
-                nat.check(lib.wd_dist_stage(self.ctxs[r].ptr, s + 1, self.A[r].data_ptr(),
-                                            bufs[s][r].data_ptr(), outs[s][r].data_ptr()))
+            h = comm.halo_start(bufs[s], self.slabs[0])
+
+            def launch(lo, hi):
+                for r in range(R):
+                    nat.check(lib.wd_dist_configure(self.ctxs[r].ptr, lo, hi))
+                    nat.check(lib.wd_dist_stage(self.ctxs[r].ptr, s + 1, self.A[r].data_ptr(),
+                                                bufs[s][r].data_ptr(), outs[s][r].data_ptr()))
+            if self.overlap:
+                # planes [2G, nl): every stencil reach (<= G planes) stays
+                # inside the rank's own planes
+                launch(2 * G, nl)
+                comm.halo_finish(h, bufs[s], self.slabs[0])
+                self._sync()
+                launch(G, 2 * G)
+                launch(nl, nl + G)
+            else:
+                comm.halo_finish(h, bufs[s], self.slabs[0])
+                self._sync()
+                launch(G, G + nl)
+        for r in range(R):
+            nat.check(lib.wd_dist_configure(self.ctxs[r].ptr, G, G + nl))
         streams = [self.ctxs[r].lib.wd_get_stream(self.ctxs[r].ptr) for r in range(R)]
         if self.filter0 == "partitioned":
             self._filter0_partitioned()
