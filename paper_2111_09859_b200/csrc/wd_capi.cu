@@ -19,6 +19,7 @@
 #include "wd_fused.cuh"
 #include "wd_metrics.cuh"
 #include "wd_dist_filter0.cuh"
+#include "wd_deriv_scan.cuh"
 
 using namespace wd;
 
@@ -181,6 +182,39 @@ int compact_factor(int scheme, int n, int periodic, HostFactor& F) {
   return gtsv_factor(n, lower.data(), diag.data(), upper.data(), F);
 }
 
+// arith="fast": the same compact matrix factored WITHOUT interchanges
+// (Thomas), the swap-free form the scan solve needs (wd_deriv_scan.cuh);
+// periodic axes keep the cyclic factor (already swap-free).
+int compact_factor_fast(int scheme, int n, int periodic, HostFactor& F) {
+  const double alpha = scheme == WD_C4 ? 0.25 : 1.0 / 3.0;
+  if (periodic) return cyclic_factor(alpha, n, F);
+  std::vector<double> lower(n, alpha), diag(n, 1.0), upper(n, alpha);
+  lower[0] = 0.0;
+  upper[0] = 3.0;
+  upper[n - 1] = 0.0;
+  lower[n - 1] = 3.0;
+  if (scheme == WD_C6) {
+    lower[1] = upper[1] = 0.25;
+    lower[n - 2] = upper[n - 2] = 0.25;
+  }
+  F = HostFactor();
+  F.n = n;
+  F.d = diag;
+  F.fact.assign(n, 0.0);
+  F.swap.assign(n, 0.0);
+  F.du.assign(n, 0.0);
+  F.du2.assign(n, 0.0);
+  F.z.assign(n, 0.0);
+  for (int i = 0; i < n - 1; ++i) {
+    if (F.d[i] == 0.0) return fail(WD_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(i + 1));
+    const double f = lower[i + 1] / F.d[i];
+    F.d[i + 1] = F.d[i + 1] - f * upper[i];
+    F.fact[i] = f;
+    F.du[i] = upper[i];
+  }
+  if (F.d[n - 1] == 0.0) return fail(WD_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(n));
+  return WD_OK;
+}
 int filter_factor(double af, int n, int periodic, HostFactor& F) {
   if (periodic) return cyclic_factor(af, n, F);
   std::vector<double> lower(n, af), diag(n, 1.0), upper(n, af);
@@ -264,12 +298,12 @@ void factor_pack(const HostFactor& F, std::vector<double>& out) {
 // Scan form of a swap-free factor for the fast filter (wd_filter_scan.cuh):
 // y_r = rhs_r - fm_r y_{r-1}, x_r = y_r rinv_r - g_r x_{r+1}; per segment of
 // m rows P_r = prod_{k=r0..r} (-fm_k), Q_r = prod_{k=r..r1-1} (-g_k).
-int scan_pack(const HostFactor& F, std::vector<double>& out, int& m) {
+int scan_pack(const HostFactor& F, std::vector<double>& out, int& m, int nseg = FS_S) {
   const int n = F.n;
-  if (n < 12 || n > FS_NMAX) return 0;
+  if (n < 12 || n > nseg * FS_M) return 0;
   for (int i = 0; i < n; ++i)
     if (F.swap[i] != 0.0) return 0;
-  m = (n + FS_S - 1) / FS_S;
+  m = (n + nseg - 1) / nseg;
   // device layout: (fm, h)[n], (P, g)[n], (Q, z)[n] as double2, rinv[n]
   std::vector<double> fm(n), P(n), ri(n), g(n), Q(n), z(n, 0.0), h(n, 0.0);
   for (int r = 0; r < n; ++r) {
@@ -326,11 +360,14 @@ struct wd_ctx {
   wd_solver_desc sd;
   Geom g;
   Metric M;
+  // M[l, m] not identically zero (generic path; see k_metric_nonzero)
+  unsigned char mterm[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};
   cudaStream_t stream = nullptr;
   // factors
   HostFactor hcomp[3], hfilt[3];
   TriDev comp[3], filt[3];
   ScanDev scan[3];
+  ScanDev cscan[3];  // fast compact derivatives (wd_deriv_scan.cuh), per axis
   double* factor_dev = nullptr;
   FilterCoef fcoef;
   // per-node metric sums (curvilinear) or scalars (uniform)
@@ -432,6 +469,28 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
 void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int axis, int scheme,
                   Epi e, const Status* st) {
   const Geom& g = c->g;
+  if ((scheme == WD_C4 || scheme == WD_C6) && c->cscan[axis].tab && scheme == c->sd.scheme) {
+    // arith="fast": segmented-scan solve, epilogue fused (wd_deriv_scan.cuh)
+    DScanArgs a;
+    a.in = in;
+    a.out = out;
+    a.N = g.N;
+    a.sa = g.s[axis];
+    a.per = g.per[axis];
+    a.scheme = scheme;
+    a.T = c->cscan[axis];
+    a.epi = e;
+    a.st = st;
+    const int n = g.n[axis];
+    const long long lines = g.N / n;
+    const int NL = dscan_lines(n);
+    const long long groups = a.sa == 1 ? (lines + NL - 1) / NL
+                                       : (g.N / (n * a.sa)) * ((a.sa + NL - 1) / NL);
+    const int blocks = (int)std::min<long long>(groups, 148LL * 2);
+    const DScanFn fn = dscan_kernel(n, a.sa == 1, a.per != 0, scheme == WD_C6);
+    fn<<<blocks, FS_T, dscan_smem(n, NL), c->stream>>>(a);
+    return;
+  }
   if (scheme == WD_C4 || scheme == WD_C6) {
     const long long L = g.N / g.n[axis];
     double* ys = (e.mode == 0 && out != in) ? out : scratch;
@@ -455,7 +514,7 @@ void launch_divergence(wd_ctx* c, double* const V[3], int csch, double* out, con
   bool first = true;
   for (int m = 0; m < nd; ++m)
     for (int l = 0; l < nd; ++l) {
-      if (c->M.m == nullptr && l != m) continue;  // exact zero terms (uniform)
+      if (c->M.m == nullptr ? l != m : !c->mterm[l * nd + m]) continue;  // exact zero terms
       launch_deriv(c, V[m], out, c->tmp, l, csch, epi_metric(c, l, m, first, out), st);
       first = false;
     }
@@ -470,8 +529,11 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
     Uv.p[a] = U[a];
     Uhv.p[a] = Uh ? Uh[a] : nullptr;
   }
+  unsigned nzm = 0;
+  for (int t = 0; t < c->g.nd * c->g.nd; ++t)
+    if (c->M.m == nullptr || c->mterm[t]) nzm |= 1u << t;
   k_assemble<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv, c->g.N,
-                                                                     c->g.nd, st);
+                                                                     c->g.nd, nzm, st);
 }
 
 // directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
@@ -638,6 +700,22 @@ int ensure_generic(wd_ctx* c) {
     return fail(WD_ERR_CUDA, "generic workspace allocation failed (" +
                                  std::to_string(24.0 * N * 8 / 1e9) + " GB)");
   }
+  if (c->M.m && !getenv("WD_NO_ZERO_SKIP")) {
+    const int nt = c->g.nd * c->g.nd;
+    int* fl = nullptr;
+    int hf[9] = {0};
+    if (cudaMalloc(&fl, nt * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(WD_ERR_CUDA, "metric flag allocation failed");
+    }
+    cudaMemsetAsync(fl, 0, nt * sizeof(int), c->stream);
+    k_metric_nonzero<<<dim3(148 * 2, nt), kThreads, 0, c->stream>>>(c->M.m, c->g.N, fl);
+    cudaMemcpyAsync(hf, fl, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(fl);
+    if (e != cudaSuccess) return fail(WD_ERR_CUDA, std::string("metric scan: ") + cudaGetErrorString(e));
+    for (int t = 0; t < nt; ++t) c->mterm[t] = hf[t] != 0;
+  }
   double* w = c->ws_generic;
   auto take = [&]() {
     double* r = w;
@@ -747,7 +825,9 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   // factors
   std::vector<double> packed, all;
   size_t off_comp[3] = {0, 0, 0}, off_filt[3] = {0, 0, 0}, off_scan[3] = {0, 0, 0};
-  int scan_m[3] = {0, 0, 0};
+  size_t off_cscan[3] = {0, 0, 0};
+  int scan_m[3] = {0, 0, 0}, cscan_m[3] = {0, 0, 0};
+  HostFactor cfast[3];
   for (int a = 0; a < g.nd; ++a) {
     if (sd->scheme == WD_C4 || sd->scheme == WD_C6) {
       rc = compact_factor(sd->scheme, g.n[a], g.per[a], c->hcomp[a]);
@@ -758,6 +838,14 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
       factor_pack(c->hcomp[a], packed);
       off_comp[a] = all.size();
       all.insert(all.end(), packed.begin(), packed.end());
+      if (sd->arith == 1 && !getenv("WD_NO_DSCAN") &&
+          compact_factor_fast(sd->scheme, g.n[a], g.per[a], cfast[a]) == WD_OK &&
+          scan_pack(cfast[a], packed, cscan_m[a], FS_T / dscan_lines(g.n[a]))) {
+        off_cscan[a] = all.size();
+        all.insert(all.end(), packed.begin(), packed.end());
+      } else {
+        cscan_m[a] = 0;
+      }
     }
     if (c->sd.use_filter && g.n[a] >= 3) {
       rc = filter_factor(sd->alpha_f, g.n[a], g.per[a], c->hfilt[a]);
@@ -787,6 +875,12 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
     for (int a = 0; a < g.nd; ++a) {
       if (c->hcomp[a].n) c->comp[a] = factor_view(c->hcomp[a], c->factor_dev + off_comp[a]);
       if (c->hfilt[a].n) c->filt[a] = factor_view(c->hfilt[a], c->factor_dev + off_filt[a]);
+      if (cscan_m[a]) {
+        c->cscan[a].n = cfast[a].n;
+        c->cscan[a].m = cscan_m[a];
+        c->cscan[a].tab = c->factor_dev + off_cscan[a];
+        c->cscan[a].denom = cfast[a].cyclic ? cfast[a].denom : 1.0;
+      }
       if (scan_m[a]) {
         c->scan[a].n = c->hfilt[a].n;
         c->scan[a].m = scan_m[a];

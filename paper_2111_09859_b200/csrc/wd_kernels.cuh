@@ -261,8 +261,11 @@ struct MVec3 {
 
 // U_m = sum_l M[l,m] dphi_l ; Uhat_l = sum_m M[l,m] U_m
 // (formulations.py:87-98, Python sum order).
+// nzm: bit l*nd+m set when M[l,m] is not identically zero (k_metric_nonzero);
+// a skipped term is +-0, which leaves a running sum unchanged (up to the
+// sign of an all-zero sum), so the result equals the full sum.
 static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd,
-                           const Status* st) {
+                                  unsigned nzm, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -272,10 +275,15 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
 #pragma unroll
     for (int m = 0; m < kMaxDim; ++m) {
       if (m >= nd) break;
-      double s = M.get(0, m, idx) * d[0];
+      double s = 0.0;
+      bool any = false;
 #pragma unroll
-      for (int l = 1; l < kMaxDim; ++l)
-        if (l < nd) s = s + M.get(l, m, idx) * d[l];
+      for (int l = 0; l < kMaxDim; ++l)
+        if (l < nd && ((nzm >> (l * nd + m)) & 1u)) {
+          const double t = M.get(l, m, idx) * d[l];
+          s = any ? s + t : t;
+          any = true;
+        }
       u[m] = s;
       U.p[m][idx] = s;
     }
@@ -283,10 +291,15 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
 #pragma unroll
       for (int l = 0; l < kMaxDim; ++l) {
         if (l >= nd) break;
-        double s = M.get(l, 0, idx) * u[0];
+        double s = 0.0;
+        bool any = false;
 #pragma unroll
-        for (int m = 1; m < kMaxDim; ++m)
-          if (m < nd) s = s + M.get(l, m, idx) * u[m];
+        for (int m = 0; m < kMaxDim; ++m)
+          if (m < nd && ((nzm >> (l * nd + m)) & 1u)) {
+            const double t = M.get(l, m, idx) * u[m];
+            s = any ? s + t : t;
+            any = true;
+          }
         Uh.p[l][idx] = s;
       }
   }
@@ -571,6 +584,20 @@ static __global__ void k_metric_sums(Metric M, double* sumS, double* cflms, doub
     sumS[idx] = tot;
     cflms[idx] = cfl * ms;
   }
+}
+
+// Which metric terms M[l, m] are not identically +-0 over the grid
+// (blockIdx.y = l * nd + m; NaN counts as nonzero).  Terms that are zero at
+// every node contribute exactly +-0 to the divergence sums of
+// formulations.py:135-143, so the generic path skips their line solves
+// (O-grids with a straight axis: 4 of 9 terms in 3-D).
+static __global__ void k_metric_nonzero(const double* __restrict__ m, long long N, int* flags) {
+  const double* f = m + (long long)blockIdx.y * N;
+  bool nz = false;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x)
+    nz |= !(f[idx] == 0.0);
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flags + blockIdx.y, 1);
 }
 
 // 2-D / 3-D metric inversion (grid.py:196-216).  fwd[m*d+l] = dx_m/dxi_l.
