@@ -263,8 +263,9 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
         }
       }
       __syncthreads();
-      constexpr int KR = NS * FS_M / FS_T;  // rows per thread and line
-      constexpr int LB = 8 / KR;            // lines per operand batch
+      // rows per thread and line (exact for full segments), lines per batch
+      constexpr int KR = MM > 0 ? (NS * MM + FS_T - 1) / FS_T : NS * FS_M / FS_T;
+      constexpr int LB = 8 / KR;
       for (int l0 = 0; l0 < nl; l0 += LB) {
         double av[LB][KR], cv[LB][KR];
 #pragma unroll
