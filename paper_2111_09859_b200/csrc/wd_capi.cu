@@ -344,6 +344,10 @@ Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) 
   g.s[1] = g.n[2];
   g.s[0] = (long long)g.n[1] * g.n[2];
   g.N = (long long)g.n[0] * g.n[1] * g.n[2];
+  for (int a = 0; a < kMaxDim; ++a) {
+    g.fs[a] = fdiv_make((unsigned long long)std::max(g.s[a], 1LL));
+    g.fn[a] = fdiv_make((unsigned long long)std::max(g.n[a], 1));
+  }
   for (int f = 0; f < 2 * kMaxDim; ++f) g.face[f] = face ? face[f] : WD_FACE_NONE;
   for (int a = 0; a < kMaxDim; ++a)
     g.per[a] = a < ndim && face && face[2 * a] == WD_FACE_PERIODIC ? 1 : 0;
@@ -377,6 +381,7 @@ struct wd_ctx {
   double* ws = nullptr;
   double* ws_generic = nullptr;  // lazily allocated (ensure_generic)
   double *p, *k, *acc, *dt, *lap, *tmp, *tmp2, *gam, *phiY;
+  double *advf = nullptr, *gmf = nullptr;  // generic: advection, |grad phi|
   double *dphi[3], *U[3], *Uh[3], *nrm[3], *B[3], *F[3], *Ue[3];
   Status* st = nullptr;
   Status* st_scratch = nullptr;
@@ -521,7 +526,17 @@ void launch_divergence(wd_ctx* c, double* const V[3], int csch, double* out, con
 }
 
 void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* const Uh[3],
-                     const Status* st) {
+                     const Status* st, bool extras = false) {
+  AsmExtra x;
+  std::memset(&x, 0, sizeof(x));
+  if (extras) {  // central schemes: advection, |grad phi|, curvature normal
+    x.adv = c->advf;
+    if (c->sd.kind == WD_HJ_CURVATURE) {
+      x.gm = c->gmf;
+      for (int a = 0; a < 3; ++a) x.nrm.p[a] = c->nrm[a];
+      x.eps0 = c->sd.eps0;
+    }
+  }
   Vec3 dv;
   MVec3 Uv, Uhv;
   for (int a = 0; a < 3; ++a) {
@@ -533,7 +548,7 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   for (int t = 0; t < c->g.nd * c->g.nd; ++t)
     if (c->M.m == nullptr || c->mterm[t]) nzm |= 1u << t;
   k_assemble<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv, c->g.N,
-                                                                     c->g.nd, nzm, st);
+                                                                     c->g.nd, nzm, x, st);
 }
 
 // directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
@@ -593,9 +608,16 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
     launch_assemble(c, c->dphi, c->U, nullptr, st);
     launch_divergence(c, c->U, csch, c->lap, st);
   } else {
+    // central schemes: the assemble kernel also leaves adv, |grad phi| and
+    // the curvature normal (bit-identical, k_assemble); UW keeps its own
+    const bool ext = scheme != WD_UW && !getenv("WD_NO_ASM_EXTRA");
     if (!fresh) {
       launch_dphi(c, p, st);
-      launch_assemble(c, c->dphi, c->U, c->Uh, st);
+      launch_assemble(c, c->dphi, c->U, c->Uh, st, ext);
+    }
+    if (ext) {
+      a.adv = c->advf;
+      if (kind == WD_HJ_CURVATURE) a.gm = c->gmf;
     }
     if (kind != WD_EIKONAL) {
       double* const* Ul = c->U;
@@ -615,8 +637,9 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
           uv.p[l] = Ul[l];
           nv.p[l] = c->nrm[l];
         }
-        k_normal<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(uv, nv, c->g.N, nd,
-                                                                         c->sd.eps0, st);
+        if (!ext)
+          k_normal<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(uv, nv, c->g.N, nd,
+                                                                           c->sd.eps0, st);
         launch_divergence(c, c->nrm, csch, c->tmp2, st);
       }
     }
@@ -641,7 +664,9 @@ void enqueue_timestep(wd_ctx* c, const double* p, double* dt, const Status* st) 
   a.cflms_c = c->cflms_c;
   if (c->sd.kind != WD_POISSON) {
     launch_dphi(c, p, st);
-    launch_assemble(c, c->dphi, c->U, c->Uh, st);
+    // extras for the stage-1 tendency of the same iteration (fresh)
+    launch_assemble(c, c->dphi, c->U, c->Uh, st,
+                    c->sd.scheme != WD_UW && !getenv("WD_NO_ASM_EXTRA"));
     if (c->sd.kind == WD_HJ_LAD) launch_gamma_lad(c, p, st);
   }
   k_timestep<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(a, dt, c->g.N, st);
@@ -690,15 +715,15 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
   }
 }
 
-// Generic-path workspace (24 fields), allocated the first time a generic
+// Generic-path workspace (26 fields), allocated the first time a generic
 // kernel sequence is enqueued; the fused path never needs it.
 int ensure_generic(wd_ctx* c) {
   if (c->ws_generic) return WD_OK;
   const long long N = c->g.N;
-  if (cudaMalloc(&c->ws_generic, (size_t)24 * N * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&c->ws_generic, (size_t)26 * N * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(WD_ERR_CUDA, "generic workspace allocation failed (" +
-                                 std::to_string(24.0 * N * 8 / 1e9) + " GB)");
+                                 std::to_string(26.0 * N * 8 / 1e9) + " GB)");
   }
   if (c->M.m && !getenv("WD_NO_ZERO_SKIP")) {
     const int nt = c->g.nd * c->g.nd;
@@ -725,6 +750,8 @@ int ensure_generic(wd_ctx* c) {
   c->lap = take();
   c->gam = take();
   take();
+  c->advf = take();
+  c->gmf = take();
   for (int a = 0; a < 3; ++a) {
     c->dphi[a] = take();
     c->U[a] = take();

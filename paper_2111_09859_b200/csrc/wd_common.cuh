@@ -30,6 +30,23 @@ __device__ __forceinline__ T pick(const T (&a)[K], int i) {
   return r;
 }
 
+// Division by a grid-invariant 32-bit divisor as multiply-high + add +
+// shift (round-up method: l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1,
+// q = (mulhi(m, x) + x) >> l with a 33-bit sum): exact for every 32-bit x,
+// ~3 instructions instead of the ~20 of a runtime unsigned division.
+struct FDiv {
+  unsigned m, l;
+};
+inline FDiv fdiv_make(unsigned long long d) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  const unsigned long long m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+  return FDiv{(unsigned)m, l};
+}
+__device__ __forceinline__ unsigned fdiv(unsigned x, FDiv f) {
+  return (unsigned)(((unsigned long long)__umulhi(x, f.m) + x) >> f.l);
+}
+
 // Structured-grid geometry: C-order (n0, n1[, n2]); unused axes have n = 1.
 struct Geom {
   int nd;
@@ -39,6 +56,7 @@ struct Geom {
   int per[kMaxDim];       // periodic axes
   int face[2 * kMaxDim];  // WD_FACE_* per face (imin, imax, jmin, ...)
   const uint8_t* mask;    // solid mask (N) or nullptr
+  FDiv fs[kMaxDim], fn[kMaxDim];  // fast division by s[a], n[a] (N < 2^32)
 };
 
 // Metric terms: either uniform diagonal constants or (d, d, N) fields.
@@ -169,7 +187,10 @@ __device__ __forceinline__ double d4_at(const L& w, int i, int n, int per) {
 __device__ __forceinline__ int axis_coord(const Geom& g, long long idx, int a) {
   const long long s = pick(g.s, a);
   const int n = pick(g.n, a);
-  if (g.N <= 0xffffffffLL) return (int)(((unsigned)idx / (unsigned)s) % (unsigned)n);
+  if (g.N <= 0xffffffffLL) {
+    const unsigned q = fdiv((unsigned)idx, pick(g.fs, a));
+    return (int)(q - fdiv(q, pick(g.fn, a)) * (unsigned)n);
+  }
   return (int)((idx / s) % n);
 }
 
@@ -178,13 +199,17 @@ struct AxisGeom {
   long long N;   // total nodes
   long long sa;  // stride of the axis
   int n;         // length of the axis
+  FDiv fs, fn;   // fast division by sa, n (N < 2^32)
   __device__ __forceinline__ int coord(long long idx) const {
-    if (N <= 0xffffffffLL) return (int)(((unsigned)idx / (unsigned)sa) % (unsigned)n);
+    if (N <= 0xffffffffLL) {
+      const unsigned q = fdiv((unsigned)idx, fs);
+      return (int)(q - fdiv(q, fn) * (unsigned)n);
+    }
     return (int)((idx / sa) % n);
   }
 };
 __host__ __device__ __forceinline__ AxisGeom axis_geom(const Geom& g, int axis) {
-  return AxisGeom{g.N, g.s[axis], g.n[axis]};
+  return AxisGeom{g.N, g.s[axis], g.n[axis], g.fs[axis], g.fn[axis]};
 }
 
 __device__ __forceinline__ void node_coords(const Geom& g, long long idx, int c[kMaxDim]) {

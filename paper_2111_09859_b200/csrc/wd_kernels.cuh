@@ -264,8 +264,21 @@ struct MVec3 {
 // nzm: bit l*nd+m set when M[l,m] is not identically zero (k_metric_nonzero);
 // a skipped term is +-0, which leaves a running sum unchanged (up to the
 // sign of an all-zero sum), so the result equals the full sum.
+// Optional pointwise products of the same node, computed here from the
+// registers instead of re-reading U / U_hat / dphi in later kernels
+// (expressions identical to k_tendency / k_normal, so bit-identical):
+//   adv = sum_l Uhat_l dphi_l        (formulations.py:114-121, central)
+//   gmo = |grad phi| = sqrt(sum U^2)  (formulations.py:207)
+//   nrm = U / (|grad phi| + eps0)     (formulations.py:212-214)
+struct AsmExtra {
+  double* adv;
+  double* gm;
+  MVec3 nrm;
+  double eps0;
+};
+
 static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd,
-                                  unsigned nzm, const Status* st) {
+                                  unsigned nzm, AsmExtra x, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -287,6 +300,7 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
       u[m] = s;
       U.p[m][idx] = s;
     }
+    double adv = 0.0;
     if (Uh.p[0] != nullptr)
 #pragma unroll
       for (int l = 0; l < kMaxDim; ++l) {
@@ -301,7 +315,26 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
             any = true;
           }
         Uh.p[l][idx] = s;
+        if (x.adv) {
+          const double t = s * d[l];
+          adv = l == 0 ? t : adv + t;
+        }
       }
+    if (x.adv) x.adv[idx] = adv;
+    if (x.gm) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < kMaxDim; ++m) {
+        if (m >= nd) break;
+        s = m == 0 ? u[0] * u[0] : s + u[m] * u[m];
+      }
+      const double gm = sqrt(s);
+      x.gm[idx] = gm;
+      if (x.nrm.p[0])
+#pragma unroll
+        for (int m = 0; m < kMaxDim; ++m)
+          if (m < nd) x.nrm.p[m][idx] = u[m] / (gm + x.eps0);
+    }
   }
 }
 
@@ -342,6 +375,8 @@ struct ResidualArgs {
   const double* lap;
   const double* gam;    // LAD gamma or nullptr
   const double* kappa;  // curvature
+  const double* adv;    // precomputed advection (k_assemble) or nullptr
+  const double* gm;     // precomputed |grad phi| (k_assemble) or nullptr
   Vec3 U, Uh, dphi, B, F;
 };
 
@@ -359,7 +394,7 @@ static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const 
     double adv = 0.0;
 #pragma unroll
     for (int l = 0; l < kMaxDim; ++l) {
-      if (l >= a.nd) break;
+      if (l >= a.nd || a.adv) break;
       const double uh = a.Uh.p[l][idx];
       double t;
       if (a.scheme == WD_UW) {
@@ -370,20 +405,26 @@ static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const 
       }
       adv = l == 0 ? t : adv + t;
     }
+    if (a.adv) adv = a.adv[idx];
     if (a.kind == WD_EIKONAL) {
       k[idx] = 1.0 - adv;
     } else if (a.kind == WD_HJ || a.kind == WD_HJ_LAD) {
       const double gam = a.kind == WD_HJ ? a.eps * a.p[idx] : a.gam[idx];
       k[idx] = 1.0 + gam * a.lap[idx] - adv;
     } else {  // WD_HJ_CURVATURE
-      double s = 0.0;
+      double gm;
+      if (a.gm) {
+        gm = a.gm[idx];
+      } else {
+        double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < kMaxDim; ++m) {
-        if (m >= a.nd) break;
-        const double u = a.U.p[m][idx];
-        s = m == 0 ? u * u : s + u * u;
+        for (int m = 0; m < kMaxDim; ++m) {
+          if (m >= a.nd) break;
+          const double u = a.U.p[m][idx];
+          s = m == 0 ? u * u : s + u * u;
+        }
+        gm = sqrt(s);
       }
-      const double gm = sqrt(s);
       const double om = 1.0 - gm;
       const double nu = 0.001 * (om * om);
       const double gam = a.eps * a.p[idx] + nu;
@@ -450,11 +491,9 @@ static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
       v = phi[s] + cdt * k[s];
     }
     out[idx] = is_pinned(g, idx, c) ? 0.0 : v;
-  }
-  if (stage == 2 || stage == 3) {
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
-         idx += (long long)gridDim.x * blockDim.x)
-      acc[idx] = acc[idx] + 2.0 * k[idx];
+    // stages 2/3 read acc nowhere else, so the accumulation rides along
+    // (k[idx] is k[s] or its neighbour: one DRAM pass over k)
+    if (stage == 2 || stage == 3) acc[idx] = acc[idx] + 2.0 * k[idx];
   }
 }
 
