@@ -488,12 +488,12 @@ void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int
     a.st = st;
     const int n = g.n[axis];
     const long long lines = g.N / n;
-    const int NL = dscan_lines(n);
-    const long long groups = a.sa == 1 ? (lines + NL - 1) / NL
-                                       : (g.N / (n * a.sa)) * ((a.sa + NL - 1) / NL);
-    const int blocks = (int)std::min<long long>(groups, 148LL * 2);
+    const DScanShape sh = dscan_shape(n, a.sa == 1);
+    const long long groups = a.sa == 1 ? (lines + sh.NL - 1) / sh.NL
+                                       : (g.N / (n * a.sa)) * ((a.sa + sh.NL - 1) / sh.NL);
+    const int blocks = (int)std::min<long long>(groups, 148LL * (sh.TT == 256 ? 2 : 1));
     const DScanFn fn = dscan_kernel(n, a.sa == 1, a.per != 0, scheme == WD_C6);
-    fn<<<blocks, FS_T, dscan_smem(n, NL), c->stream>>>(a);
+    fn<<<blocks, sh.TT, dscan_smem(n, sh), c->stream>>>(a);
     return;
   }
   if (scheme == WD_C4 || scheme == WD_C6) {
@@ -867,7 +867,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
       all.insert(all.end(), packed.begin(), packed.end());
       if (sd->arith == 1 && !getenv("WD_NO_DSCAN") &&
           compact_factor_fast(sd->scheme, g.n[a], g.per[a], cfast[a]) == WD_OK &&
-          scan_pack(cfast[a], packed, cscan_m[a], FS_T / dscan_lines(g.n[a]))) {
+          scan_pack(cfast[a], packed, cscan_m[a], dscan_segments(g.n[a]))) {
         off_cscan[a] = all.size();
         all.insert(all.end(), packed.begin(), packed.end());
       } else {

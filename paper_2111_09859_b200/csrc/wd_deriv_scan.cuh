@@ -42,24 +42,36 @@ struct DScanArgs {
   const Status* st;
 };
 
-// NL lines per tile (16: n <= 512; 8: n <= 1024, factor tables then read
-// through L1 instead of shared memory so 2 CTAs still fit per SM)
-inline size_t dscan_smem(int n, int NL) {
+// Tile shapes: NL lines x NS = TT / NL segments, TT threads.
+//   n <= 512:          16 lines x 16 segments, 256 threads, 2 CTAs / SM;
+//   512 < n <= 1024:   stride-1 lines 8 x 32 / 256 threads with the factor
+//                      tables read through L1 (2 CTAs / SM); strided lines
+//                      16 x 32 / 512 threads (1 CTA / SM), so every tile row
+//                      is a 128-byte run in HBM rather than 64 bytes.
+struct DScanShape {
+  int NL, TT;
+};
+inline DScanShape dscan_shape(int n, bool ax2) {
+  if (n <= FS_NMAX) return {16, 256};
+  return ax2 ? DScanShape{8, 256} : DScanShape{16, 512};
+}
+inline int dscan_segments(int n) { return n <= FS_NMAX ? 16 : 32; }
+inline size_t dscan_smem(int n, DScanShape sh) {
   const int NR = n + 2 * DS_G;
-  const size_t tab = NL == 16 ? (size_t)((7 * n + 3) & ~3) : 0;
-  return (tab + (size_t)NL * (size_t)(NR | 1) + 3 * FS_T) * sizeof(double);
+  const bool tg = sh.NL == 8;
+  const size_t tab = tg ? 0 : (size_t)((7 * n + 3) & ~3);
+  return (tab + (size_t)sh.NL * (size_t)(NR | 1) + 3 * (size_t)sh.TT) * sizeof(double);
 }
 
 // MM > 0: every segment has exactly MM rows (n = 16 MM, compile-time row
 // loops without guards: the register window is renamed, not moved); MM = 0:
 // any n in [12, NS * 32].  PER / C6: periodic axis, scheme C6 (else C4).
-// NL lines x NS = 256 / NL segments per tile.
-template <bool AX2, int MM, bool PER, bool C6, int NL>
-__global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
+template <bool AX2, int MM, bool PER, bool C6, int NL, int TT>
+__global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs a) {
   if (a.st && a.st->state != WD_STATE_RUNNING) return;
   extern __shared__ double ds_smem[];
-  constexpr int NS = FS_T / NL;
-  constexpr bool TG = NL != 16;           // tables from global (L1)
+  constexpr int NS = TT / NL;
+  constexpr bool TG = NL == 8;            // tables from global (L1)
   constexpr int UM = MM > 0 ? MM : FS_M;  // unrolled rows per segment
   const int n = a.T.n, m = MM > 0 ? MM : a.T.m;
   constexpr bool per = PER;
@@ -72,10 +84,10 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
   const int NR = n + 2 * DS_G;
   const int LS = NR | 1;
   double* Yend = tile + (AX2 ? NL * LS : NR * NL);
-  double* Xst = Yend + FS_T;
-  double* Hs = Xst + FS_T;
+  double* Xst = Yend + TT;
+  double* Hs = Xst + TT;
   if (!TG)
-    for (int t = threadIdx.x; t < 7 * n; t += FS_T) ds_smem[t] = a.T.tab[t];
+    for (int t = threadIdx.x; t < 7 * n; t += TT) ds_smem[t] = a.T.tab[t];
 
   const int tid = threadIdx.x, l = tid % NL, s = tid / NL;
   const int r0 = s * m;
@@ -104,7 +116,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
       for (int ll = 0; ll < nl; ++ll) {
         const double* src = in + ll * lstride;
         double* dst = tile + ll * LS + DS_G;
-        for (int r = tid; r < n; r += FS_T) cp_async8(dst + r, src + r, true);
+        for (int r = tid; r < n; r += TT) cp_async8(dst + r, src + r, true);
       }
       if (tid < 2 * DS_G * NL) {
         const int ll = tid / (2 * DS_G), gq = tid - ll * 2 * DS_G;
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
       }
       __syncthreads();
       // rows per thread and line (exact for full segments), lines per batch
-      constexpr int KR = MM > 0 ? (NS * MM + FS_T - 1) / FS_T : NS * FS_M / FS_T;
+      constexpr int KR = MM > 0 ? (NS * MM + TT - 1) / TT : NS * FS_M / TT;
       constexpr int LB = 8 / KR;
       for (int l0 = 0; l0 < nl; l0 += LB) {
         double av[LB][KR], cv[LB][KR];
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
         for (int u = 0; u < LB; ++u)
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
-            const int r = tid + k * FS_T;
+            const int r = tid + k * TT;
             const bool ok = l0 + u < nl && r < n;
             const long long idx = base + (l0 + u) * lstride + r;
             av[u][k] = ok && need_acc ? e.acc[idx] : 0.0;
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
         for (int u = 0; u < LB; ++u)
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
-            const int r = tid + k * FS_T;
+            const int r = tid + k * TT;
             if (l0 + u < nl && r < n) {
               const long long idx = base + (l0 + u) * lstride + r;
               __stcs(a.out + idx, fin(tile[(l0 + u) * LS + DS_G + r], av[u][k], cv[u][k]));
@@ -303,26 +315,27 @@ __global__ void __launch_bounds__(FS_T, 2) k_deriv_scan(DScanArgs a) {
 namespace wd {
 
 using DScanFn = void (*)(DScanArgs);
-template <bool AX2, int MM, int NL>
+template <bool AX2, int MM, int NL, int TT>
 inline DScanFn dscan_pick4(bool per, bool c6) {
-  if (per) return c6 ? k_deriv_scan<AX2, MM, true, true, NL> : k_deriv_scan<AX2, MM, true, false, NL>;
-  return c6 ? k_deriv_scan<AX2, MM, false, true, NL> : k_deriv_scan<AX2, MM, false, false, NL>;
+  if (per)
+    return c6 ? k_deriv_scan<AX2, MM, true, true, NL, TT> : k_deriv_scan<AX2, MM, true, false, NL, TT>;
+  return c6 ? k_deriv_scan<AX2, MM, false, true, NL, TT> : k_deriv_scan<AX2, MM, false, false, NL, TT>;
 }
 template <bool AX2>
 inline DScanFn dscan_pick(int n, bool per, bool c6) {
-  if (n == 512) return dscan_pick4<AX2, 32, 16>(per, c6);
-  if (n == 256) return dscan_pick4<AX2, 16, 16>(per, c6);
-  if (n <= FS_NMAX) return dscan_pick4<AX2, 0, 16>(per, c6);
-  if (n == 2 * FS_NMAX) return dscan_pick4<AX2, 32, 8>(per, c6);
-  return dscan_pick4<AX2, 0, 8>(per, c6);
+  constexpr int NLB = AX2 ? 8 : 16, TTB = AX2 ? 256 : 512;  // n > 512
+  if (n == 512) return dscan_pick4<AX2, 32, 16, 256>(per, c6);
+  if (n == 256) return dscan_pick4<AX2, 16, 16, 256>(per, c6);
+  if (n <= FS_NMAX) return dscan_pick4<AX2, 0, 16, 256>(per, c6);
+  if (n == 2 * FS_NMAX) return dscan_pick4<AX2, 32, NLB, TTB>(per, c6);
+  return dscan_pick4<AX2, 0, NLB, TTB>(per, c6);
 }
-inline int dscan_lines(int n) { return n <= FS_NMAX ? 16 : 8; }
 // the instantiation for a line length / stride / periodicity / scheme; its
 // dynamic shared-memory limit is raised on every call (cheap, host only)
 inline DScanFn dscan_kernel(int n, bool ax2, bool per, bool c6) {
   const DScanFn f = ax2 ? dscan_pick<true>(n, per, c6) : dscan_pick<false>(n, per, c6);
   cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)dscan_smem(n, dscan_lines(n)));
+                       (int)dscan_smem(n, dscan_shape(n, ax2)));
   return f;
 }
 
