@@ -382,6 +382,7 @@ struct wd_ctx {
   double* ws_generic = nullptr;  // lazily allocated (ensure_generic)
   double *p, *k, *acc, *dt, *lap, *tmp, *tmp2, *gam, *phiY;
   double *advf = nullptr, *gmf = nullptr;  // generic: advection, |grad phi|
+  double* uabsf = nullptr;                 // generic: sum |U_hat| for the time step
   double *dphi[3], *U[3], *Uh[3], *nrm[3], *B[3], *F[3], *Ue[3];
   Status* st = nullptr;
   Status* st_scratch = nullptr;
@@ -526,9 +527,10 @@ void launch_divergence(wd_ctx* c, double* const V[3], int csch, double* out, con
 }
 
 void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* const Uh[3],
-                     const Status* st, bool extras = false) {
+                     const Status* st, bool extras = false, bool uabs = false) {
   AsmExtra x;
   std::memset(&x, 0, sizeof(x));
+  if (uabs) x.uabs = c->uabsf;
   if (extras) {  // central schemes: advection, |grad phi|, curvature normal
     x.adv = c->advf;
     if (c->sd.kind == WD_HJ_CURVATURE) {
@@ -613,7 +615,8 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
     const bool ext = scheme != WD_UW && !getenv("WD_NO_ASM_EXTRA");
     if (!fresh) {
       launch_dphi(c, p, st);
-      launch_assemble(c, c->dphi, c->U, c->Uh, st, ext);
+      // with the extras nothing downstream reads U_hat: not written
+      launch_assemble(c, c->dphi, c->U, ext ? nullptr : c->Uh, st, ext);
     }
     if (ext) {
       a.adv = c->advf;
@@ -665,8 +668,9 @@ void enqueue_timestep(wd_ctx* c, const double* p, double* dt, const Status* st) 
   if (c->sd.kind != WD_POISSON) {
     launch_dphi(c, p, st);
     // extras for the stage-1 tendency of the same iteration (fresh)
-    launch_assemble(c, c->dphi, c->U, c->Uh, st,
-                    c->sd.scheme != WD_UW && !getenv("WD_NO_ASM_EXTRA"));
+    const bool ext = c->sd.scheme != WD_UW && !getenv("WD_NO_ASM_EXTRA");
+    launch_assemble(c, c->dphi, c->U, ext ? nullptr : c->Uh, st, ext, ext);
+    if (ext) a.uabs = c->uabsf;
     if (c->sd.kind == WD_HJ_LAD) launch_gamma_lad(c, p, st);
   }
   k_timestep<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(a, dt, c->g.N, st);
@@ -715,15 +719,15 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
   }
 }
 
-// Generic-path workspace (26 fields), allocated the first time a generic
+// Generic-path workspace (27 fields), allocated the first time a generic
 // kernel sequence is enqueued; the fused path never needs it.
 int ensure_generic(wd_ctx* c) {
   if (c->ws_generic) return WD_OK;
   const long long N = c->g.N;
-  if (cudaMalloc(&c->ws_generic, (size_t)26 * N * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&c->ws_generic, (size_t)27 * N * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(WD_ERR_CUDA, "generic workspace allocation failed (" +
-                                 std::to_string(26.0 * N * 8 / 1e9) + " GB)");
+                                 std::to_string(27.0 * N * 8 / 1e9) + " GB)");
   }
   if (c->M.m && !getenv("WD_NO_ZERO_SKIP")) {
     const int nt = c->g.nd * c->g.nd;
@@ -752,6 +756,7 @@ int ensure_generic(wd_ctx* c) {
   take();
   c->advf = take();
   c->gmf = take();
+  c->uabsf = take();
   for (int a = 0; a < 3; ++a) {
     c->dphi[a] = take();
     c->U[a] = take();

@@ -270,11 +270,14 @@ struct MVec3 {
 //   adv = sum_l Uhat_l dphi_l        (formulations.py:114-121, central)
 //   gmo = |grad phi| = sqrt(sum U^2)  (formulations.py:207)
 //   nrm = U / (|grad phi| + eps0)     (formulations.py:212-214)
+//   uabs = sum_l |Uhat_l|             (solver.py:170, k_timestep's order)
+// U_hat itself is then only written when Uh.p[0] != nullptr.
 struct AsmExtra {
   double* adv;
   double* gm;
   MVec3 nrm;
   double eps0;
+  double* uabs;
 };
 
 static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd,
@@ -300,8 +303,8 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
       u[m] = s;
       U.p[m][idx] = s;
     }
-    double adv = 0.0;
-    if (Uh.p[0] != nullptr)
+    double adv = 0.0, ua = 0.0;
+    if (Uh.p[0] != nullptr || x.adv || x.uabs)
 #pragma unroll
       for (int l = 0; l < kMaxDim; ++l) {
         if (l >= nd) break;
@@ -314,13 +317,15 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
             s = any ? s + t : t;
             any = true;
           }
-        Uh.p[l][idx] = s;
+        if (Uh.p[0] != nullptr) Uh.p[l][idx] = s;
         if (x.adv) {
           const double t = s * d[l];
           adv = l == 0 ? t : adv + t;
         }
+        ua = l == 0 ? fabs(s) : ua + fabs(s);
       }
     if (x.adv) x.adv[idx] = adv;
+    if (x.uabs) x.uabs[idx] = ua;
     if (x.gm) {
       double s = 0.0;
 #pragma unroll
@@ -440,6 +445,7 @@ struct DtArgs {
   const double* p;
   const double* gam;     // LAD gamma
   Vec3 Uh;
+  const double* uabs;    // precomputed sum |U_hat| (k_assemble) or nullptr
   const double* sumS;    // field or nullptr (then sumS_c)
   double sumS_c;
   const double* cflms;   // cfl * min_spacing field or nullptr
@@ -456,10 +462,15 @@ static __global__ void k_timestep(DtArgs a, double* dt, long long N, const Statu
       dt[idx] = a.cfl / (2.0 * sS);
       continue;
     }
-    double den = fabs(a.Uh.p[0][idx]);
+    double den;
+    if (a.uabs) {
+      den = a.uabs[idx];
+    } else {
+      den = fabs(a.Uh.p[0][idx]);
 #pragma unroll
-    for (int l = 1; l < kMaxDim; ++l)
-      if (l < a.nd) den = den + fabs(a.Uh.p[l][idx]);
+      for (int l = 1; l < kMaxDim; ++l)
+        if (l < a.nd) den = den + fabs(a.Uh.p[l][idx]);
+    }
     if (a.kind == WD_HJ || a.kind == WD_HJ_CURVATURE)
       den = den + 2.0 * (a.eps * a.p[idx]) * sS;
     else if (a.kind == WD_HJ_LAD)

@@ -430,8 +430,11 @@ __device__ __forceinline__ void lt_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+#ifndef WD_LT_MINB
+#define WD_LT_MINB 1
+#endif
 template <int JOB>
-static __global__ void __launch_bounds__(LS_WARPS * 32, 1)
+static __global__ void __launch_bounds__(LS_WARPS * 32, WD_LT_MINB)
     k_line_solve_t(const double* __restrict__ in, double* y, double* out, Geom g, int axis, int n,
                    long long sa, TriDev T, Epi epi, const uint8_t* pin, int use_geom_pin,
                    const Status* st) {
