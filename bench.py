@@ -383,17 +383,15 @@ def run_b200(args, world, rank, local):
         scfg = W.SolveConfig(formulation=fc, scheme=cfg["scheme"], filter_config=filt, cfl=0.5,
                              tol=1e-15, max_iters=K, arith=args.arith)
         bnd = W.BoundarySpec(cfg["faces"])
-        # untimed warm-up calls (graph capture paths, the pinned-host cache
-        # that receives the result, and ~1 s of GPU work so the SM clocks
-        # have ramped back up after the host-side phase above: without it
-        # the first timed solves ran 30-40 % slower); reports dropped
+        # untimed warm-up calls: the first solve allocates the page-locked
+        # result buffer (~0.4 s) and the field workspace that later solves
+        # recycle; reports dropped
         for _ in range(2):
             del_rep = W.solve_steady(grid, bnd, scfg, phi0=phi0, chunk=chunk)
             del del_rep
         torch.cuda.synchronize()
         # three complete timed solves (each: context, H2D, K steps, D2H), the
-        # median reported: a single one-shot solve varies by ~+-100 ms on a
-        # fresh box (context / allocation setup), all samples are listed
+        # median reported and all samples listed
         samples = []
         for _ in range(3):
             barrier(world)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <string>
 #include <utility>
@@ -358,6 +359,41 @@ Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) 
 }  // namespace
 
 // ====================================================================== ctx
+
+// Field workspaces are recycled across contexts: a cudaMalloc / cudaFree of
+// the 7.5 GB workspace of a 512^3 solve took 2-170 ms (measured per call),
+// which made one-shot solve_steady() times vary by up to ~2x.  Freed blocks
+// of an exact size are kept (at most kWsCacheMax of them, LIFO) and handed
+// to the next context that asks for that size; WD_NO_WS_CACHE disables it.
+namespace {
+constexpr size_t kWsCacheMax = 2;
+std::mutex g_ws_mu;
+std::vector<std::pair<size_t, void*>> g_ws_cache;
+cudaError_t ws_alloc(void** p, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (size_t i = g_ws_cache.size(); i-- > 0;)
+      if (g_ws_cache[i].first == bytes) {
+        *p = g_ws_cache[i].second;
+        g_ws_cache.erase(g_ws_cache.begin() + i);
+        return cudaSuccess;
+      }
+  }
+  return cudaMalloc(p, bytes);
+}
+void ws_free(void* p, size_t bytes) {
+  if (!p) return;
+  static const bool off = getenv("WD_NO_WS_CACHE") != nullptr;
+  if (!off) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (g_ws_cache.size() < kWsCacheMax) {
+      g_ws_cache.emplace_back(bytes, p);
+      return;
+    }
+  }
+  cudaFree(p);
+}
+}  // namespace
 
 struct wd_ctx {
   wd_grid_desc gd;
@@ -724,7 +760,7 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
 int ensure_generic(wd_ctx* c) {
   if (c->ws_generic) return WD_OK;
   const long long N = c->g.N;
-  if (cudaMalloc(&c->ws_generic, (size_t)27 * N * sizeof(double)) != cudaSuccess) {
+  if (ws_alloc((void**)&c->ws_generic, (size_t)27 * N * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(WD_ERR_CUDA, "generic workspace allocation failed (" +
                                  std::to_string(27.0 * N * 8 / 1e9) + " GB)");
@@ -924,7 +960,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   // workspace: the 7 fields every path uses; the generic path's 24 more
   // (derivatives, U, U_hat, ...) are allocated on first use (ensure_generic)
   const int ncore = 7;
-  if (cudaMalloc(&c->ws, (size_t)ncore * g.N * sizeof(double)) != cudaSuccess) {
+  if (ws_alloc((void**)&c->ws, (size_t)ncore * g.N * sizeof(double)) != cudaSuccess) {
     wd_destroy(c);
     return fail(WD_ERR_CUDA, "workspace allocation failed (" +
                                  std::to_string((double)ncore * g.N * 8 / 1e9) + " GB)");
@@ -1008,8 +1044,8 @@ int wd_destroy(wd_ctx* c) {
   for (auto& kv : c->d0tab) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
-  cudaFree(c->ws);
-  cudaFree(c->ws_generic);
+  ws_free(c->ws, (size_t)7 * c->g.N * sizeof(double));
+  ws_free(c->ws_generic, (size_t)27 * c->g.N * sizeof(double));
   cudaFree(c->st);
   cudaFree(c->hist_scratch);
   cudaFree(c->flag_dev);

@@ -63,6 +63,21 @@ static __global__ void k_line_rhs(const double* __restrict__ in, double* __restr
     const int i = ag.coord(idx);
     double r;
     constexpr int H = JOB == 0 ? 2 : 5;  // stencil reach
+    if (i >= H && i < n - H && sa == 1) {
+      // stride-1 interior: compile-time offsets (same expressions)
+      const double* q = in + idx;
+      if (JOB == 0) {
+        if (scheme == WD_C4) r = C4_CA * (q[1] - q[-1]);
+        else r = C6_CA * (q[1] - q[-1]) + C6_CB * (q[2] - q[-2]);
+      } else {
+        const double* c = fc.hc + 30;
+        r = c[0] * q[0];
+#pragma unroll
+        for (int k = 1; k <= 5; ++k) r = r + c[k] * (q[k] + q[-k]);
+      }
+      rhs[idx] = r;
+      continue;
+    }
     if (i >= H && i < n - H) {
       // interior row (no wrap, no closure, full order): the same
       // expressions as compact_rhs_at / the h = 5 filter row
