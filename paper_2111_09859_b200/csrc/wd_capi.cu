@@ -721,6 +721,20 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
   for (int a = 0; a < g.nd; ++a) {
     double* nxt = bufs[a & 1];
     const long long L = g.N / g.n[a];
+    // arith="fast", 3-D, no solid mask: the segmented-scan sweep
+    // (wd_filter_scan.cuh).  It does not restore pinned nodes, which is
+    // exact here: the input is BC'd (walls are 0), a wall of this axis is a
+    // line end (identity row) and a wall of another axis holds whole lines
+    // of zeros, which the linear sweep maps to zeros.
+    if (st && c->sd.arith == 1 && g.nd == 3 && g.mask == nullptr && c->scan[a].tab &&
+        !getenv("WD_NO_GEN_SCANF")) {
+      FusedPlan fp;
+      fp.in.fcoef = c->fcoef;
+      fused_filter_any(fp, a, cur, nxt, g.n[0], g.n[1], g.n[2], g.per[a], c->filt[a], nullptr,
+                       const_cast<Status*>(st), c->stream, &c->scan[a]);
+      cur = nxt;
+      continue;
+    }
     if (line_solve_ok(g.n[a])) {
       launch_line_solve<1>(cur, nxt, nxt, g, a, g.per[a], 0.0, 0, c->filt[a], epi_plain(),
                            c->fcoef, nullptr, 1, st, c->stream);

@@ -104,6 +104,7 @@ template <bool AX2, bool RED>
 void scan_mm(const ScanArgs& a, long long groups, cudaStream_t s) {
   static const bool generic = getenv("WD_SCAN_GENERIC") != nullptr;  // A/B knob
   if (a.T.n == FS_S * FS_M && !generic) scan_one<AX2, FS_M, RED>(a, groups, s);
+  else if (a.T.n == FS_S * 16 && !generic) scan_one<AX2, 16, RED>(a, groups, s);
   else scan_one<AX2, 0, RED>(a, groups, s);
 }
 

@@ -194,3 +194,15 @@ def test_plate_1024_contiguous_closures():
     pg = G.build_cartesian(12, 1024, Lx=0.1, Ly=1.0)
     ro, rp = _pair(og, pg, faces, "hj", "C6", 0.49, 6)
     _close(ro, rp)
+
+
+def test_fused_fast_256_last_axis_filter_reduction():
+    """Fused 3-D fast path with a 256-node last axis: the scan filter's
+    16-row full-segment instantiation with the convergence reduction."""
+    faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "wall",
+             "kmin": "periodic", "kmax": "periodic"}
+    dims = (12, 40, 256)
+    og = wd.cartesian(*dims, Lx=12 / 40, Ly=1.0, Lz=256 / 40, periodic=(True, False, True))
+    pg = G.build_cartesian(*dims, Lx=12 / 40, Ly=1.0, Lz=256 / 40, periodic=(True, False, True))
+    ro, rp = _pair(og, pg, faces, "hj", "E6", 0.49, 6)
+    _close(ro, rp)

@@ -60,6 +60,11 @@ CASES = [
     ((3, 512, 17), 1, True),
     ((5, 18, 512), 2, True),
     ((5, 18, 512), 2, False),
+    # n = 256: the 16-row full-segment instantiation
+    ((256, 3, 20), 0, True),
+    ((3, 256, 24), 1, False),
+    ((5, 18, 256), 2, True),
+    ((5, 18, 256), 2, False),
     ((100, 3, 17), 0, False),
     ((3, 7, 37), 2, True),
     ((2, 45, 33), 1, False),
