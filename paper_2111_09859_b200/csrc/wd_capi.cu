@@ -585,8 +585,12 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   unsigned nzm = 0;
   for (int t = 0; t < c->g.nd * c->g.nd; ++t)
     if (c->M.m == nullptr || c->mterm[t]) nzm |= 1u << t;
-  k_assemble<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv, c->g.N,
-                                                                     c->g.nd, nzm, x, st);
+  if (c->g.nd == 3)
+    k_assemble<3><<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv,
+                                                                        c->g.N, 3, nzm, x, st);
+  else
+    k_assemble<2><<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv,
+                                                                        c->g.N, 2, nzm, x, st);
 }
 
 // directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
@@ -747,6 +751,12 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
   k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
 }
 
+void rk_stage(int nd, int nb, cudaStream_t s, int stage, const double* phi, const double* dt,
+              const double* k, double* acc, double* out, const Geom& g, const Status* st) {
+  if (nd == 3) k_rk_stage<3><<<nb, kThreads, 0, s>>>(stage, phi, dt, k, acc, out, g, st);
+  else k_rk_stage<2><<<nb, kThreads, 0, s>>>(stage, phi, dt, k, acc, out, g, st);
+}
+
 // one RK4 step A -> B given dt already in c->dt (solver.py:183-212)
 void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
                  bool dt_fresh = false) {
@@ -755,17 +765,17 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
   // stage 1 evaluates the tendency at A, where enqueue_timestep just left
   // dphi / U / Uh (/ gamma) -- except for Poisson, whose time step is static
   enqueue_tendency(c, A, c->acc, st, dt_fresh && c->sd.kind != WD_POISSON);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(1, A, c->dt, c->acc, c->acc, c->p, g, st);
+  rk_stage(c->g.nd, nb, c->stream, 1, A, c->dt, c->acc, c->acc, c->p, g, st);
   enqueue_tendency(c, c->p, c->k, st);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(2, A, c->dt, c->k, c->acc, c->p, g, st);
+  rk_stage(c->g.nd, nb, c->stream, 2, A, c->dt, c->k, c->acc, c->p, g, st);
   enqueue_tendency(c, c->p, c->k, st);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(3, A, c->dt, c->k, c->acc, c->p, g, st);
+  rk_stage(c->g.nd, nb, c->stream, 3, A, c->dt, c->k, c->acc, c->p, g, st);
   enqueue_tendency(c, c->p, c->k, st);
   if (c->sd.use_filter) {
-    k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, A, c->dt, c->k, c->acc, c->p, g, st);
+    rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, c->p, g, st);
     enqueue_filter_bc(c, c->p, B, st);
   } else {
-    k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, A, c->dt, c->k, c->acc, B, g, st);
+    rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, B, g, st);
   }
 }
 
@@ -1525,13 +1535,13 @@ int wd_levelset_step(wd_ctx* c, const double* p0, double* out, double F, double 
   // (levelset.py:190-199): the solver's stage kernels with dt as a field
   k_fill<<<nb, kThreads, 0, c->stream>>>(c->dt, dt, g.N);
   rate(p0, c->acc);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(1, p0, c->dt, c->acc, c->acc, c->p, g, nullptr);
+  rk_stage(c->g.nd, nb, c->stream, 1, p0, c->dt, c->acc, c->acc, c->p, g, nullptr);
   rate(c->p, c->k);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(2, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
+  rk_stage(c->g.nd, nb, c->stream, 2, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
   rate(c->p, c->k);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(3, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
+  rk_stage(c->g.nd, nb, c->stream, 3, p0, c->dt, c->k, c->acc, c->p, g, nullptr);
   rate(c->p, c->k);
-  k_rk_stage<<<nb, kThreads, 0, c->stream>>>(4, p0, c->dt, c->k, c->acc, out, g, nullptr);
+  rk_stage(c->g.nd, nb, c->stream, 4, p0, c->dt, c->k, c->acc, out, g, nullptr);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
   return WD_OK;

@@ -280,8 +280,17 @@ struct AsmExtra {
   double* uabs;
 };
 
-static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd,
+// M[l, m] at node idx with a compile-time dimension (constant field offsets)
+template <int ND>
+__device__ __forceinline__ double mget(const Metric& M, int l, int m, long long idx) {
+  if (M.m == nullptr) return l == m ? pick(M.c, l) : 0.0;
+  return M.m[(long long)(l * ND + m) * M.N + idx];
+}
+
+template <int ND>
+static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long long N, int nd_,
                                   unsigned nzm, AsmExtra x, const Status* st) {
+  constexpr int nd = ND;
   if (st && st->state != WD_STATE_RUNNING) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -296,7 +305,7 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
 #pragma unroll
       for (int l = 0; l < kMaxDim; ++l)
         if (l < nd && ((nzm >> (l * nd + m)) & 1u)) {
-          const double t = M.get(l, m, idx) * d[l];
+          const double t = mget<ND>(M, l, m, idx) * d[l];
           s = any ? s + t : t;
           any = true;
         }
@@ -313,7 +322,7 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
 #pragma unroll
         for (int m = 0; m < kMaxDim; ++m)
           if (m < nd && ((nzm >> (l * nd + m)) & 1u)) {
-            const double t = M.get(l, m, idx) * u[m];
+            const double t = mget<ND>(M, l, m, idx) * u[m];
             s = any ? s + t : t;
             any = true;
           }
@@ -485,15 +494,54 @@ static __global__ void k_timestep(DtArgs a, double* dt, long long N, const Statu
 //   stage 1..3: out = BC(phi + c(dt) k), c = 0.5*dt | 0.5*dt | dt
 //   stage 2, 3 also: acc = acc + 2 k   (acc holds k1 after stage 1)
 //   stage 4:  out = BC(phi + (dt/6)(acc + k))
+// Node coordinates by successive division by the axis lengths (2 fast
+// divisions in 3-D instead of a division and a modulo per axis).
+template <int ND>
+__device__ __forceinline__ void node_coords_nd(const Geom& g, long long idx, int c[kMaxDim]) {
+  c[0] = c[1] = c[2] = 0;
+  if (g.N <= 0xffffffffLL) {
+    unsigned q = (unsigned)idx;
+#pragma unroll
+    for (int a = ND - 1; a > 0; --a) {
+      const unsigned qn = fdiv(q, g.fn[a]);
+      c[a] = (int)(q - qn * (unsigned)g.n[a]);
+      q = qn;
+    }
+    c[0] = (int)q;
+    return;
+  }
+  long long q = idx;
+#pragma unroll
+  for (int a = ND - 1; a > 0; --a) {
+    c[a] = (int)(q % g.n[a]);
+    q /= g.n[a];
+  }
+  c[0] = (int)q;
+}
+
+template <int ND>
 static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
-                           const double* __restrict__ dt, const double* __restrict__ k,
-                           double* acc, double* out, Geom g, const Status* st) {
+                                  const double* __restrict__ dt, const double* __restrict__ k,
+                                  double* acc, double* out, Geom g, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
        idx += (long long)gridDim.x * blockDim.x) {
     int c[kMaxDim];
-    node_coords(g, idx, c);
-    const long long s = bc_source(g, idx, c);
+    node_coords_nd<ND>(g, idx, c);
+    long long s = idx;
+    bool pinned = false;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {  // bc_source / is_pinned, ND axes
+      if (c[a] == 0) {
+        if (g.face[2 * a] == WD_FACE_FARFIELD) s += g.s[a];
+        if (g.face[2 * a] == WD_FACE_WALL) pinned = true;
+      }
+      if (c[a] == g.n[a] - 1) {
+        if (g.face[2 * a + 1] == WD_FACE_FARFIELD) s -= g.s[a];
+        if (g.face[2 * a + 1] == WD_FACE_WALL) pinned = true;
+      }
+    }
+    if (g.mask != nullptr && g.mask[idx] != 0) pinned = true;
     double v;
     if (stage == 4) {
       v = phi[s] + (dt[s] / 6.0) * (acc[s] + k[s]);
@@ -501,7 +549,7 @@ static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
       const double cdt = stage == 3 ? dt[s] : 0.5 * dt[s];
       v = phi[s] + cdt * k[s];
     }
-    out[idx] = is_pinned(g, idx, c) ? 0.0 : v;
+    out[idx] = pinned ? 0.0 : v;
     // stages 2/3 read acc nowhere else, so the accumulation rides along
     // (k[idx] is k[s] or its neighbour: one DRAM pass over k)
     if (stage == 2 || stage == 3) acc[idx] = acc[idx] + 2.0 * k[idx];
