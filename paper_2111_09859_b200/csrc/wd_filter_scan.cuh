@@ -105,6 +105,11 @@ template <bool AX2, int MM, bool RED>
 #ifndef WD_SCAN_TG
 #define WD_SCAN_TG 0  // 1: factor tables read from global memory (L1) instead of shared
 #endif
+#ifndef WD_SCAN_PF
+#define WD_SCAN_PF 1  // L2 prefetch of A and the next tile, stride-1 lines
+                      // (A/B: filter along k 0.83 -> 0.70 ms at 512^3; on
+                      // the strided axes it measured neutral to slower)
+#endif
 #ifndef WD_SCAN_MINB
 #define WD_SCAN_MINB 2
 #endif
@@ -230,6 +235,28 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
   for (; q < groups; q += gridDim.x) {
     cp_async_wait_all();
     __syncthreads();
+#if WD_SCAN_PF
+    // full-segment tiles: pull the convergence operand of this tile and the
+    // input rows of the next one into L2 while this tile is solved, so the
+    // store-phase loads of A and the next cp.async fill see L2 latency
+    if (MM > 0 && AX2) {
+      auto pf = [](const double* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); };
+      long long nb2 = 0;
+      int nl2 = 0;
+      const bool nxt = q + gridDim.x < groups;
+      if (nxt) tile_of(q + gridDim.x, nb2, nl2);
+#pragma unroll
+      for (int k = tid; k < FS_L * (FS_NMAX / 16); k += FS_T) {
+        // AX2: 16 lines x (n / 16) 128-byte pieces; else n rows x 128 bytes
+        const int ll = AX2 ? k / (n / 16) : 0, pc = AX2 ? k % (n / 16) : k;
+        const long long off = AX2 ? ll * lstride + pc * 16 : (long long)pc * rstride;
+        if (AX2 ? ll < nl : pc < n) {
+          if (RED) pf(a.A + base + off);
+        }
+        if (nxt && (AX2 ? ll < nl2 : pc < n)) pf(a.in + nb2 + off);
+      }
+    }
+#endif
     // ---- 1. right-hand side + local forward recurrence (from zero)
     double yv[MM > 0 ? 10 : FS_M];  // MM > 0: rows 0-4 and MM-5..MM-1 only
     double hs = 0.0, yp = 0.0;
