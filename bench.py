@@ -19,6 +19,7 @@ test) -- strong scaling, max time over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -389,6 +390,7 @@ def run_b200(args, world, rank, local):
         for _ in range(2):
             del_rep = W.solve_steady(grid, bnd, scfg, phi0=phi0, chunk=chunk)
             del del_rep
+            gc.collect()  # the result array must be gone for its buffer to recycle
         torch.cuda.synchronize()
         # three complete timed solves (each: context, H2D, K steps, D2H), the
         # median reported and all samples listed
@@ -401,6 +403,7 @@ def run_b200(args, world, rank, local):
             samples.append(allreduce_max(time.perf_counter() - t0, world))
             assert rep.iters == K
             del rep
+            gc.collect()
         t_e2e = sorted(samples)[1]
         e2e = {"value": N * K * world / t_e2e / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(N * 8 / K),
