@@ -213,9 +213,10 @@ def _device_steps(grid, cfg, fc, filt, K, Wm, arith):
 
 
 def _time_to_converge(ms_per_step, arith):
-    """Iterations to tol 1e-8 measured for this configuration (profiles/
-    converge.json, written from tools/converge.py / the strip goldens) x the
-    measured step time."""
+    """Iterations to tol 1e-8 for this configuration: the oracle's count
+    (bit-exact x/z-invariant strip, tests/golden/strip_c4_ny512.npz) and the
+    full 512^3 solve measured through solve_steady on one B200
+    (tools/converge_c4.py -> profiles/converge.json)."""
     path = os.path.join(ROOT, "profiles", "converge.json")
     try:
         rec = json.load(open(path))["c4"]
@@ -223,9 +224,11 @@ def _time_to_converge(ms_per_step, arith):
         return None
     iters = rec.get("iters")
     out = {"iters_to_tol_1e-8": iters, "source": rec.get("source"),
-           "est_seconds": round(iters * ms_per_step / 1e3, 2) if iters else None}
+           "est_seconds_at_this_step_time": round(iters * ms_per_step / 1e3, 2) if iters else None}
     if rec.get("measured_s") and rec.get("arith") == arith:
-        out["measured_seconds"] = rec["measured_s"]
+        out.update(measured_seconds=rec["measured_s"], measured_iters=rec.get("measured_iters"),
+                   measured_rel_dev_vs_oracle=rec.get("measured_rel_dev_vs_oracle"),
+                   measured_on=rec.get("measured_on"))
     return out
 
 
@@ -314,8 +317,10 @@ def run_b200(args, world, rank, local):
     nat.check(lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
     stream = ctx.stream()
     chunk = 2
+    warm_steps = 0
     for _ in range((Wm + chunk - 1) // chunk):
         nat.check(lib.wd_steps(ctx.ptr, chunk))
+        warm_steps += chunk
     torch.cuda.synchronize()
     # timed region
     barrier(world)
@@ -338,8 +343,11 @@ def run_b200(args, world, rank, local):
     secs = e0.elapsed_time(e1) / 1e3
     st = nat.Status()
     nat.check(lib.wd_read_status(ctx.ptr, ctypes.byref(st)))
-    if st.state == nat.STATE_DIVERGED:
-        raise RuntimeError("benchmark run diverged")
+    # a status that left RUNNING would turn the remaining replays into
+    # no-ops and inflate the number: every timed step must have run
+    if st.state != nat.STATE_RUNNING or st.iters != warm_steps + K:
+        raise RuntimeError(f"benchmark run stopped early (state {st.state}, {st.iters} of "
+                           f"{warm_steps + K} steps)")
     secs_max = allreduce_max(secs, world)
     value = N * K * world / secs_max / 1e9
 

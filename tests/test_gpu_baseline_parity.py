@@ -1,0 +1,137 @@
+"""CUDA path vs the oracle at (or near) the BASELINE sizes of configs 2, 3 and 5.
+
+Goldens come from tests/golden/make_baseline_golden.py (the CPU oracle,
+pinned bit-for-bit to the reference on every shared path).  Exact mode must
+match bit for bit: iteration count, every entry of the residual history, the
+stop outcome (converged / stalled at max_iters / the divergence iteration)
+and the field, compared through a SHA-256 of its bytes after ``+ 0.0``
+(sign of zero normalised; the kernels skip the ``0 + x`` of Python ``sum``).
+Fast mode on the converged C5 cylinder: iteration count within 1 and the
+field within 1e-10 of max |phi| (north_star's tolerance).
+"""
+import hashlib
+import re
+
+import numpy as np
+import pytest
+
+import goldens
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_2111_09859_b200")
+from paper_2111_09859_b200.errors import DivergenceError  # noqa: E402
+
+RING = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield"}
+CYL = dict(RING, kmin="periodic", kmax="periodic")
+PLATE = {"imin": "farfield", "imax": "farfield", "jmin": "wall", "jmax": "farfield"}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2111_09859_b200 import _native
+    _native.lib()
+
+
+def _hash(phi):
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(phi, dtype=np.float64) + 0.0)
+                          .tobytes()).hexdigest()
+
+
+def _alpha(z):
+    a = float(z["alpha_f"])
+    return None if np.isnan(a) else a
+
+
+def _solve(grid, faces, z, arith="exact", max_iters=None):
+    """solve_steady with the golden's settings; returns (report | None,
+    diverged_iter | None)."""
+    af = _alpha(z)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=str(z["kind"])),
+                        scheme=str(z["scheme"]),
+                        filter_config=None if af is None else W.FilterConfig(af),
+                        cfl=0.5, tol=float(z["tol"]),
+                        max_iters=int(z["max_iters"]) if max_iters is None else max_iters,
+                        arith=arith)
+    try:
+        return W.solve_steady(grid, W.BoundarySpec(faces), cfg), None
+    except DivergenceError as exc:
+        m = re.search(r"at iteration (\d+)", str(exc))
+        return None, int(m.group(1)) if m else -2
+
+
+def _check_exact(rep, div, z):
+    if int(z["diverged_at"]) > 0:
+        assert rep is None and div == int(z["diverged_at"]), (div, int(z["diverged_at"]))
+        return
+    assert rep is not None, f"diverged at {div}"
+    assert rep.iters == int(z["iters"])
+    assert rep.converged == bool(z["converged"])
+    assert np.array_equal(rep.residual_history, z["residual_history"])
+    assert _hash(rep.phi) == str(z["sha256"])
+    if "sha256_prime" in z:
+        assert _hash(rep.phi_prime) == str(z["sha256_prime"])
+
+
+# --------------------------------------------------------------- config 2
+def test_c2_annulus_257x129_curvature_c6_2000_steps_exact():
+    z = goldens.load("base_c2_annulus_curv_C6")
+    g = W.build_annulus(257, 129, scheme="C6")
+    rep, div = _solve(g, RING, z)
+    _check_exact(rep, div, z)
+    assert np.array_equal(rep.phi, z["phi"])
+
+
+def test_c2_annulus_257x129_curvature_c6_outcome_exact():
+    """The oracle's whole run (to tol 1e-8 or its stall at max_iters)."""
+    z = goldens.load("base_c2_annulus_curv_C6_full")
+    g = W.build_annulus(257, 129, scheme="C6")
+    rep, div = _solve(g, RING, z)
+    _check_exact(rep, div, z)
+    assert np.array_equal(rep.phi, z["phi"])
+
+
+# --------------------------------------------------------------- config 3
+@pytest.mark.parametrize("kind", ["hj", "eikonal", "hj_lad"])
+def test_c3_bump_1025x513_e6_exact(kind):
+    z = goldens.load(f"base_c3_bump_{kind}_E6")
+    g = W.build_sinusoidal_bump(1025, 513, scheme="E6")
+    rep, div = _solve(g, PLATE, z)
+    _check_exact(rep, div, z)
+
+
+# --------------------------------------------------------------- config 5
+@pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
+def test_c5_cylinder_128x64x32_c6_50_steps_exact(kind):
+    z = goldens.load(f"base_c5_cyl128_{kind}_C6")
+    g = W.build_cylinder(128, 64, 32, scheme="C6")
+    rep, div = _solve(g, CYL, z)
+    _check_exact(rep, div, z)
+
+
+@pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
+def test_c5_cylinder_64x32x16_c6_converged_fast(kind):
+    """Fast arithmetic (scan derivatives / scan filter) to tol 1e-8: iteration
+    count within 1 of the oracle's, field within 1e-10 * max|phi|."""
+    z = goldens.load(f"base_c5_cyl64_{kind}_C6_conv")
+    assert bool(z["converged"]), "oracle run did not converge"
+    g = W.build_cylinder(64, 32, 16, scheme="C6")
+    rep, div = _solve(g, CYL, z, arith="fast", max_iters=int(z["iters"]) + 50)
+    assert rep is not None, f"diverged at {div}"
+    assert rep.converged
+    assert abs(rep.iters - int(z["iters"])) <= 1, (rep.iters, int(z["iters"]))
+    ref = z["phi"]
+    err = float(np.max(np.abs(rep.phi - ref)))
+    assert err <= 1e-10 * float(np.max(np.abs(ref))), err
+
+
+@pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
+def test_c5_cylinder_64x32x16_c6_converged_exact(kind):
+    z = goldens.load(f"base_c5_cyl64_{kind}_C6_conv")
+    g = W.build_cylinder(64, 32, 16, scheme="C6")
+    rep, div = _solve(g, CYL, z)
+    _check_exact(rep, div, z)
+    assert np.array_equal(rep.phi, z["phi"])
