@@ -7,7 +7,11 @@
  * path (INTEGRATION.md shows the binding).  Each function cites the
  * reference interface it replaces.  All pointers named *_dev are CUDA device
  * pointers owned by the caller; every call is asynchronous on the given
- * stream unless stated otherwise.  Fields are fp64, C-order (n0, n1[, n2]),
+ * context's stream unless stated otherwise.  A context runs on its OWN
+ * non-blocking stream (wd_get_stream); the `stream` argument of wd_create is
+ * reserved.  Results of wd_steps are valid for other streams only after
+ * wd_finish / wd_read_status (both synchronise the context stream) or after
+ * waiting on an event recorded on wd_get_stream().  Fields are fp64, C-order (n0, n1[, n2]),
  * axis 0 slowest (reference grid.py:5-11).  Metrics are (d, d, N) with
  * metrics[l][m] = d xi_l / d x_m (grid.py:9, 32).
  *
@@ -150,6 +154,10 @@ int wd_local_timestep(wd_ctx* ctx, const double* phi_dev, double* dt_dev);
 int wd_apply_bc(wd_ctx* ctx, double* phi_dev);
 /* poisson_postprocess formulations.py:255-270 (+ BC, solver.py:284-285)  */
 int wd_poisson_post(wd_ctx* ctx, const double* pp_dev, double* phi_dev);
+/* the same map with the boundary conditions optional: apply_bc = 0 is the
+ * reference's _l2_vs_exact sampling (solver.py:289-293), which post-maps
+ * without re-applying the BCs                                            */
+int wd_poisson_map(wd_ctx* ctx, const double* pp_dev, double* phi_dev, int apply_bc);
 
 /* central_derivative operators.py:94-148 (E6/periodic: EXTENSION).
  * offset = coordinate jump per period (coordinate differencing only).    */

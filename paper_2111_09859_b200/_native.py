@@ -104,6 +104,7 @@ SIGNATURES = {
     "wd_local_timestep": (_I, [_P, _P, _P]),
     "wd_apply_bc": (_I, [_P, _P]),
     "wd_poisson_post": (_I, [_P, _P, _P]),
+    "wd_poisson_map": (_I, [_P, _P, _P, _I]),
     "wd_derivative": (_I, [_P, _P, _I, _IP, _I, _I, _I, _D, _P]),
     "wd_fourth_derivative": (_I, [_P, _P, _I, _IP, _I, _I, _P]),
     "wd_filter": (_I, [_P, _P, _P, _I, _IP, _I, _D, _I, _P]),
@@ -194,6 +195,7 @@ def to_host(t):
     import torch
     key = (tuple(t.shape), t.dtype)
     pool = _PINNED.setdefault(key, [])
+    _trim_pinned(key)
     for i, (h, ref) in enumerate(pool):
         if ref() is None:  # the array handed out last time is gone: reuse
             break
@@ -209,6 +211,27 @@ def to_host(t):
     a = h.numpy()
     pool[i] = (h, weakref.ref(a))
     return a
+
+
+def _trim_pinned(keep_key, max_idle_bytes=2 << 30):
+    """Free page-locked buffers whose arrays have been dropped once the idle
+    ones hold more than ``max_idle_bytes`` (a 512^3 result pins 1 GB); one
+    idle buffer of the shape being requested is always kept for reuse."""
+    idle = [(k, i) for k, pool in _PINNED.items() for i, (h, ref) in enumerate(pool)
+            if ref() is None]
+    total = sum(_PINNED[k][i][0].numel() * _PINNED[k][i][0].element_size() for k, i in idle)
+    kept_one = False
+    for k, i in sorted(idle, key=lambda ki: -ki[1]):
+        if total <= max_idle_bytes:
+            break
+        if k == keep_key and not kept_one:
+            kept_one = True
+            continue
+        h = _PINNED[k][i][0]
+        total -= h.numel() * h.element_size()
+        _PINNED[k][i] = None
+    for k in list(_PINNED):
+        _PINNED[k] = [e for e in _PINNED[k] if e is not None]
 
 
 _PINNED = {}  # (shape, dtype) -> [(pinned tensor, weakref to its live array)]

@@ -368,13 +368,24 @@ Geom make_geom(int ndim, const int* dims, const int* face, const uint8_t* mask) 
 namespace {
 constexpr size_t kWsCacheMax = 2;
 std::mutex g_ws_mu;
-std::vector<std::pair<size_t, void*>> g_ws_cache;
+struct WsBlock {
+  int device;
+  size_t bytes;
+  void* ptr;
+};
+std::vector<WsBlock> g_ws_cache;  // keyed on (device, size): a block never crosses devices
+int ws_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
 cudaError_t ws_alloc(void** p, size_t bytes) {
   {
+    const int dev = ws_device();
     std::lock_guard<std::mutex> lk(g_ws_mu);
     for (size_t i = g_ws_cache.size(); i-- > 0;)
-      if (g_ws_cache[i].first == bytes) {
-        *p = g_ws_cache[i].second;
+      if (g_ws_cache[i].bytes == bytes && g_ws_cache[i].device == dev) {
+        *p = g_ws_cache[i].ptr;
         g_ws_cache.erase(g_ws_cache.begin() + i);
         return cudaSuccess;
       }
@@ -387,7 +398,7 @@ void ws_free(void* p, size_t bytes) {
   if (!off) {
     std::lock_guard<std::mutex> lk(g_ws_mu);
     if (g_ws_cache.size() < kWsCacheMax) {
-      g_ws_cache.emplace_back(bytes, p);
+      g_ws_cache.push_back(WsBlock{ws_device(), bytes, p});
       return;
     }
   }
@@ -1242,6 +1253,10 @@ int wd_rk4_step(wd_ctx* c, const double* phi, const double* dt, double* out, int
 }
 
 int wd_poisson_post(wd_ctx* c, const double* pp, double* phi) {
+  return wd_poisson_map(c, pp, phi, 1);
+}
+
+int wd_poisson_map(wd_ctx* c, const double* pp, double* phi, int apply_bc) {
   if (!c) return fail(WD_ERR_INVALID, "null ctx");
   if (const int rc = ensure_generic(c)) return rc;
   CK(cudaDeviceSynchronize());
@@ -1257,7 +1272,10 @@ int wd_poisson_post(wd_ctx* c, const double* pp, double* phi) {
   k_poisson_map<<<nb, kThreads, 0, c->stream>>>(c->p, uv, c->tmp, g.N, g.nd, c->flag_dev);
   int neg = 0;
   CK(cudaMemcpyAsync(&neg, c->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  k_bc<<<nb, kThreads, 0, c->stream>>>(c->tmp, phi, g, nullptr);
+  if (apply_bc)
+    k_bc<<<nb, kThreads, 0, c->stream>>>(c->tmp, phi, g, nullptr);
+  else
+    CK(cudaMemcpyAsync(phi, c->tmp, g.N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (neg) return fail(WD_ERR_NEGATIVE_RADICAND, "negative radicand in the Poisson map");
   return WD_OK;

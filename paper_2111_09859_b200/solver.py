@@ -232,6 +232,10 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
         sample_l2 = exact is not None and config.l2_every > 0
         if sample_l2:
             k = kmax = int(config.l2_every)
+        if sample_l2 and tuple(np.shape(exact)) != tuple(grid.dims):
+            # metrics.py l2_norm raises on a shape mismatch
+            raise ValueError(f"exact field shape {tuple(np.shape(exact))} does not match the "
+                             f"grid {tuple(grid.dims)}")
         exact_t = ctx.field(exact) if sample_l2 else None
         st = nat.Status()
         seconds = []
@@ -287,7 +291,8 @@ def _l2_norm(ctx, phi, exact_t, grid, config):
     p = phi
     if config.formulation.kind == "poisson":
         p = ctx.empty()
-        nat.check(ctx.lib.wd_poisson_post(ctx.ptr, phi.data_ptr(), p.data_ptr()))
+        # _l2_vs_exact (solver.py:289-293) post-maps WITHOUT re-applying BCs
+        nat.check(ctx.lib.wd_poisson_map(ctx.ptr, phi.data_ptr(), p.data_ptr(), 0))
     if getattr(ctx, "_jac_dev", None) is None:
         ctx._jac_dev = torch.from_numpy(np.ascontiguousarray(grid.jacobian)).to("cuda")
     out = ctypes.c_double(0.0)
