@@ -172,7 +172,7 @@ def run_reference(args, world, rank):
     cb = cpu_sample(cfg, args.steps, args.warmup)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": cfg["workload"], "sample_dims": [32, 512, 64]},
@@ -233,36 +233,46 @@ def _time_to_converge(ms_per_step, arith):
 
 
 def run_b200_dist(args, world, rank, local):
-    """N > 1: slab decomposition of the same global grid (strong scaling)."""
+    """Slab decomposition of the same global grid over the N ranks (strong
+    scaling; also at N = 1 with --dist): the native step program of
+    csrc/wd_dist.cuh with the NCCL communicator, k steps per CUDA graph."""
+    import ctypes
     import torch
     import paper_2111_09859_b200 as W
-    from paper_2111_09859_b200 import dist
+    from paper_2111_09859_b200 import dist, _native as nat
 
     cfg = CONFIGS[args.config]
     dims = tuple(args.n if args.n else d for d in cfg["dims"])
-    sp = tuple((1.0 / dims[d]) if cfg["periodic"][d] else 1.0 / (dims[d] - 1) for d in range(3))
-    if args.n:
-        sp = (1.0 / 512, 1.0 / (dims[1] - 1), 1.0 / 512)
+    grid = W.build_cartesian(*dims, Lx=dims[0] / 512 if args.n else 1.0, Ly=1.0,
+                             Lz=dims[2] / 512 if args.n else 1.0, periodic=cfg["periodic"])
     fc = W.FormulationConfig(kind=cfg["kind"])
     filt = W.FilterConfig(cfg["alpha_f"])
     K, Wm = args.steps, args.warmup
-    comm = dist.TorchComm()
-    ds = dist.DistributedSolve(dims, sp, cfg["faces"], cfg["scheme"], fc, filt, 0.5, 1e-15,
-                               K + Wm + 8, args.arith, comm, [rank], filter0=args.filter0)
-    nl = dims[0] // world
-    ds.set_state([torch.zeros((nl, dims[1], dims[2]), dtype=torch.float64, device="cuda")])
-    for _ in range(Wm):
-        ds.step()
+    chunk = 2
+    scfg = W.SolveConfig(formulation=fc, scheme=cfg["scheme"], filter_config=filt, cfl=0.5,
+                         tol=1e-15, max_iters=10**9, arith=args.arith)
+    comm = dist.NcclComm.from_torch() if world > 1 else dist.NcclComm(0, 1)
+    ds = dist.DistributedSolve(grid, cfg["faces"], scfg, comm, filter0=args.filter0,
+                               overlap=not args.no_overlap, hist_len=K + Wm + 8)
+    ds.bind(None)
+    warm_steps = 0
+    for _ in range((Wm + chunk - 1) // chunk):
+        ds.steps(chunk)
+        warm_steps += chunk
     torch.cuda.synchronize()
     barrier(world)
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    stream = ds.ctxs[0].stream()
+    stream = ds.stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(K):
-        ds.step()
+    done = 0
+    while done < K:
+        c = min(chunk, K - done)
+        ds.steps(c)
+        done += c
     e1.record(stream)
     e1.synchronize()
     torch.cuda.synchronize()
@@ -270,27 +280,84 @@ def run_b200_dist(args, world, rank, local):
     clk = clocks.stop()
     secs = allreduce_max(e0.elapsed_time(e1) / 1e3, world)
     st = ds.status()
-    if st.state == 2:
-        raise RuntimeError("benchmark run diverged")
+    if st.state != nat.STATE_RUNNING or st.iters != warm_steps + K:
+        raise RuntimeError(f"benchmark run stopped early (state {st.state}, {st.iters} of "
+                           f"{warm_steps + K} steps)")
     N = int(np.prod(dims))
+    Nl = N // world
     value = N * K / secs / 1e9
     peak, peak_kind = _peaks()
+    # dominant kernel of this rank's slab: the RK stage kernels on its planes
+    lib = ds.lib
+    lctx = lib.wd_dist_context(ds.ptr)
+    kern, kwords = {}, {}
+    avg = ctypes.c_double(0.0)
+    for kid in (1, 2, 3, 4):
+        if ds.fused and lib.wd_time_kernel(lctx, kid, 5, ctypes.byref(avg)) == 0:
+            kern[f"stage{kid}"] = avg.value
+            kwords[f"stage{kid}"] = lib.wd_kernel_words(lctx, kid)
+    roof = None
+    if kern:
+        dom = max(kern, key=kern.get)
+        ach = kwords[dom] * 8 * Nl / (kern[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "kernel": dom + " (rank slab)",
+                "alg_bytes_per_launch": kwords[dom] * 8 * Nl, "peak_source": peak_kind}
     w_upd = words_per_update(3, True)
-    step_ach = w_upd * 8 * N / world / (secs / K) / 1e9
+    step_ach = w_upd * 8 * Nl / (secs / K) / 1e9
+    ranges = 3 if ds.overlap else 1
+    launches = 4 * ranges * 2 + (2 if ds.filter0 == "partitioned" else 3) + 2 + 1 + \
+        (2 if world > 1 else 0)
+    ds.close()
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e:
+        phi0 = torch.zeros(dims, dtype=torch.float64).pin_memory()
+        ecfg = W.SolveConfig(formulation=fc, scheme=cfg["scheme"], filter_config=filt, cfl=0.5,
+                             tol=1e-15, max_iters=K, arith=args.arith)
+        bnd = W.BoundarySpec(cfg["faces"])
+        for _ in range(2):
+            rep = W.solve_steady(grid, bnd, ecfg, phi0=phi0, chunk=chunk, comm=comm)
+            del rep
+            gc.collect()
+        samples = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            rep = W.solve_steady(grid, bnd, ecfg, phi0=phi0, chunk=chunk, comm=comm)
+            torch.cuda.synchronize()
+            samples.append(allreduce_max(time.perf_counter() - t0, world))
+            assert rep.iters == K
+            del rep
+            gc.collect()
+        t_e2e = sorted(samples)[1]
+        e2e = {"value": N * K / t_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(N * 8 / K),
+               "d2h_bytes_per_step": int(world * (N * 8 + 8 * K) / K),
+               "seconds": t_e2e, "samples_s": [round(x, 4) for x in samples],
+               "includes": "median of 3 solve_steady(comm=) calls on every rank, each: context "
+                           "setup + H2D of the rank's slab of phi0 (pinned) + K steps + "
+                           "all_gather of the slabs + D2H of the global field on every rank"}
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": Wm, "ms_per_step": round(secs / K * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "dims": list(dims), "arith": args.arith,
                        "global_nodes": N, "parallelism": f"slab{world}",
-                       "axis0_filter": ds.filter0,
+                       "axis0_filter": ds.filter0, "overlap": ds.overlap, "cuda_graph": ds.graph,
+                       "comm": "nccl (libwd_b200: wd_comm_init)" if world > 1 else "none (1 rank)",
                        "l2": "inputs larger than L2"},
-            "roofline": None,
-            "step_roofline": {"achieved_per_gpu": round(step_ach, 1), "peak": peak, "unit": "GB/s",
-                              "frac": round(step_ach / peak, 4), "words_per_update": w_upd,
-                              "peak_source": peak_kind},
-            "gpu_launches": K * 20, "clocks": clk, "e2e": None}
-    ds.close()
+            "roofline": roof,
+            "step_roofline": {"achieved": round(step_ach, 1), "per": "gpu", "peak": peak,
+                              "unit": "GB/s", "frac": round(step_ach / peak, 4),
+                              "words_per_update": w_upd, "peak_source": peak_kind},
+            "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
+            "gpu_launches": K * launches, "clocks": clk, "e2e": e2e,
+            "time_to_converge": _time_to_converge(secs / K * 1e3, args.arith)}
+    if rank == 0 and not args.no_cpu and world == 1:
+        line["cpu_baseline"] = cpu_sample(cfg, 3, 1)
+    comm.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -357,6 +424,8 @@ def run_b200(args, world, rank, local):
         avg = ctypes.c_double(0.0)
         names = {1: "stage1", 2: "stage2", 3: "stage3", 4: "stage4", 5: "filter_axis0",
                  6: "filter_axis1", 7: "filter_axis2", 8: "change"}
+        if filt is not None:
+            del names[8]  # the change reduction is fused into the last sweep
         for kid, name in names.items():
             if lib.wd_time_kernel(ctx.ptr, kid, 5, ctypes.byref(avg)) == 0:
                 kern[name] = avg.value
@@ -426,10 +495,10 @@ def run_b200(args, world, rank, local):
     ttc = _time_to_converge(secs_max / K * 1e3, args.arith)
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": Wm, "ms_per_step": round(secs_max / K * 1e3, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "dims": list(dims), "arith": args.arith,
-                       "global_nodes": N * world, "parallelism": f"replica{world}",
+                       "global_nodes": N * world, "parallelism": "slab1 (single-GPU fused step)",
                        "l2": "inputs larger than L2 (1.07 GB per field)",
                        "fused": True if kern else False},
             "roofline": roof,
@@ -437,7 +506,7 @@ def run_b200(args, world, rank, local):
                               "frac": round(step_ach / peak, 4), "words_per_update": w_upd,
                               "model": "SURVEY 8(d) B_alg (21 stage words + 2 per filter "
                                        "sweep + 1 convergence read)",
-                              "words_moved": (sum(kwords[k] for k in kwords if k != "change")
+                              "words_moved": (sum(kwords[k] for k in kwords)
                                               if kern else None)},
             "kernel_ms": {k: round(v, 4) for k, v in kern.items()},
             "gpu_launches": K * (12 if kern else 0),
@@ -464,6 +533,8 @@ def main():
                          "within 1e-10); exact: bit-identical to the reference algorithm")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-mode side run")
     ap.add_argument("--dist", action="store_true", help="slab-decomposed path even at N=1")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="decomposed path: ghost exchange not overlapped with interior planes")
     ap.add_argument("--filter0", default=None, choices=["partitioned", "transpose"],
                     help="decomposed axis-0 filter (default: partitioned in fast arithmetic)")
     args = ap.parse_args()
@@ -473,12 +544,6 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
     elif world > 1 or args.dist:
-        if world == 1:
-            import torch.distributed as tdist
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            tdist.init_process_group("nccl", rank=0, world_size=1,
-                                     device_id=__import__("torch").device("cuda", 0))
         run_b200_dist(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)

@@ -202,38 +202,79 @@ int wd_gradient_magnitude(wd_ctx* ctx, const double* phi_dev, double* out_dev);
 int wd_levelset_step(wd_ctx* ctx, const double* phi_dev, double* out_dev, double F, double dt,
                      double source);
 
-/* ---- slab decomposition (EXTENSION; paper_2111_09859_b200/dist.py) ----
- * The context is created for a rank's ghosted slab (nl + 2G, n1, n2) with
- * axis 0 non-periodic; the host exchanges ghost planes between stages and
- * transposes slab <-> pencil around the axis-0 filter (all_to_all), so the
- * per-node and per-line arithmetic equals the single-GPU path exactly.   */
-/* stages update planes [i_lo, i_hi) only (the slab interior)             */
-int wd_dist_configure(wd_ctx* ctx, int i_lo, int i_hi);
-/* one RK stage (1..4): out = stage(p) with phi0 = A (all ghosted)        */
-int wd_dist_stage(wd_ctx* ctx, int stage, const double* A_dev, const double* p_dev,
-                  double* out_dev);
-/* implicit-filter sweep along `axis` of an (n0, n1, n2) array; with A_dev
- * the sweep also accumulates max|out - A|, max|out| into the status     */
-int wd_dist_filter(wd_ctx* ctx, int axis, const double* in_dev, double* out_dev, int n0, int n1,
-                   int n2, int periodic, const double* A_dev);
-/* slab (nl, n1, n2) <-> all_to_all buffer (P, nl, n1/P, n2)              */
-int wd_dist_pack(const double* slab_dev, double* buf_dev, int nl, int n1, int n2, int P,
-                 void* stream);
-int wd_dist_unpack(const double* buf_dev, double* slab_dev, int nl, int n1, int n2, int P,
+/* ---- multi-GPU: slab decomposition along axis 0 (EXTENSION) --
+ * One process per GPU.  The reference has no distributed path; these entry
+ * points put its solve loop (solver.py:221-286) on P ranks that each own the
+ * planes [rank n0/P, (rank+1) n0/P) of the PERIODIC axis 0.  Explicit
+ * stencils exchange ghost planes (NCCL send/recv over NVLink) per RK stage;
+ * compact derivatives, the filter and the other line operators ALONG axis 0
+ * run on pencils between two all_to_all transposes (operators.py:130-148,
+ * 305-352 see whole lines), or -- fast arithmetic on the fused path -- as a
+ * partitioned solve with one all_gather of per-line carries; the stop test
+ * (solver.py:253-272) all_reduces (max) three words per step.  Results:
+ * bit-identical to one GPU with transposes, round-off level with the
+ * partitioned filter.                                                      */
+typedef struct wd_comm wd_comm;
+typedef struct wd_dist wd_dist;
+#define WD_NCCL_ID_BYTES 128
+#define WD_DECOMP_SLAB0 0        /* contiguous slabs of axis 0              */
+#define WD_FILTER0_AUTO (-1)     /* partitioned if arith = fast, else transpose */
+#define WD_FILTER0_PARTITIONED 0
+#define WD_FILTER0_TRANSPOSE 1
+/* rank 0: a fresh NCCL unique id (128 bytes) to hand to every rank        */
+int wd_comm_unique_id(void* id_out);
+/* wd_comm_init(nccl_id, rank, nranks, decomposition).  Call
+ * with the rank's device current; collective over the ranks.  nranks == 1
+ * needs no id and no NCCL.                                                 */
+int wd_comm_init(const void* nccl_id, int rank, int nranks, int decomposition, wd_comm** out);
+/* The same four collectives through host callbacks (another transport, or P
+ * logical ranks in one process, for tests): each gets device pointers and
+ * the stream the operation must be ordered on, returns 0 on success.  Not
+ * CUDA-graph capturable.                                                   */
+typedef struct wd_comm_callbacks {
+  void* user;
+  /* ghost planes of a (nl + 2G) x plane slab: [nl, nl+G) -> right rank's
+   * [0, G), [G, 2G) -> left rank's [nl+G, nl+2G)                           */
+  int (*halo)(void* user, double* slab_dev, long long plane, int nl, int G, void* stream);
+  /* all[q * count ..] <- rank q's mine[0 .. count)                         */
+  int (*allgather)(void* user, const double* mine_dev, double* all_dev, long long count,
                    void* stream);
-/* status maxima -> dev3 (int64 x3) for all_reduce(max); then finalize    */
-/* Partitioned axis-0 filter (fast arithmetic; wd_dist_filter0.cuh): the
- * rank's rows [rank nl, (rank+1) nl) of the n0-long periodic lines, three
- * phases around two all_gathers of per-line carries.  in: ghosted slab
- * (nl + 2G, n1, n2), G >= 5 ghosts filled; out: interior (nl, n1, n2).
- * phase 1 writes mine[2][n1 n2] (Y_blk, h.rhs); phase 2 reads xa =
- * gathered phase-1 slots [P][2][n1 n2], writes out (x') and mine[n1 n2]
- * (X_blk); phase 3 reads xa and xb = gathered phase-2 slots [P][n1 n2].   */
-int wd_dist_filter0(wd_ctx* ctx, int phase, const double* in_dev, double* out_dev, int n0,
-                    int n1, int n2, int G, int P, int rank, const double* xa_dev,
-                    const double* xb_dev, double* mine_dev);
-int wd_dist_stats(wd_ctx* ctx, long long* dev3);
-int wd_dist_finalize(wd_ctx* ctx, const long long* dev3);
+  /* recv[q * count ..] <- rank q's send[my_rank * count ..]                */
+  int (*alltoall)(void* user, const double* send_dev, double* recv_dev, long long count,
+                  void* stream);
+  /* element-wise max of n int64 words over the ranks, in place             */
+  int (*allreduce_max)(void* user, long long* buf_dev, int n, void* stream);
+} wd_comm_callbacks;
+int wd_comm_init_callbacks(const wd_comm_callbacks* cb, int rank, int nranks, wd_comm** out);
+/* One rank of an nranks-way decomposition run ALONE (benchmarking): its slab
+ * wraps onto itself, collectives are device copies of the real volume.     */
+int wd_comm_init_solo(int rank, int nranks, wd_comm** out);
+/* all[q * count ..] <- rank q's mine[0 .. count) (collecting the slabs of
+ * a result)                                                                */
+int wd_comm_allgather(wd_comm* comm, const double* mine_dev, double* all_dev, long long count,
+                      void* stream);
+int wd_comm_destroy(wd_comm* comm);
+/* Decomposed solver context.  `grid` describes the GLOBAL grid (dims, faces,
+ * spacing); metrics_dev / solid_mask_dev point at this rank's slab
+ * ((d, d, nl n1 n2) and (nl n1 n2)).  filter0: WD_FILTER0_*; overlap: run
+ * interior planes while ghost planes are in flight (fused path, NCCL).     */
+int wd_dist_create(wd_comm* comm, const wd_grid_desc* grid, const wd_solver_desc* solver,
+                   int filter0, int overlap, wd_dist** out);
+int wd_dist_destroy(wd_dist* d);
+/* phi_dev: this rank's (nl, n1[, n2]) slab (in/out); history as wd_bind    */
+int wd_dist_bind(wd_dist* d, double* phi_dev, double* history_dev);
+/* k pseudo-steps; with an NCCL communicator one CUDA graph per k holds the
+ * kernels AND the collectives, frozen in-device at the stop               */
+int wd_dist_steps(wd_dist* d, int k);
+int wd_dist_read_status(wd_dist* d, wd_status* out);
+/* the bound slab holds the latest state afterwards                         */
+int wd_dist_finish(wd_dist* d);
+void* wd_dist_stream(wd_dist* d);
+/* the rank's local solver context (operator-level calls on the slab; the
+ * axis-0 operators of a GENERIC-program context are collective)            */
+wd_ctx* wd_dist_context(wd_dist* d);
+/* out8 = {nl, G, fused, filter0, overlap, graph, nranks, rank}             */
+int wd_dist_info(wd_dist* d, int* out8);
 
 #ifdef __cplusplus
 }

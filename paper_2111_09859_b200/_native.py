@@ -70,6 +70,21 @@ class SolverDesc(ctypes.Structure):
     ]
 
 
+_LL = ctypes.c_longlong
+HALO_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, _LL, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_void_p)
+GATHER_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _LL,
+                             ctypes.c_void_p)
+REDUCE_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                             ctypes.c_void_p)
+
+
+class CommCallbacks(ctypes.Structure):
+    """wd_comm_callbacks (walldist_b200.h)."""
+    _fields_ = [("user", ctypes.c_void_p), ("halo", HALO_CB), ("allgather", GATHER_CB),
+                ("alltoall", GATHER_CB), ("allreduce_max", REDUCE_CB)]
+
+
 class Status(ctypes.Structure):
     _fields_ = [
         ("state", ctypes.c_int),
@@ -118,14 +133,22 @@ SIGNATURES = {
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
     "wd_kernel_words": (_I, [_P, _I]),
-    "wd_dist_configure": (_I, [_P, _I, _I]),
-    "wd_dist_stage": (_I, [_P, _I, _P, _P, _P]),
-    "wd_dist_filter": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _P]),
-    "wd_dist_pack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
-    "wd_dist_unpack": (_I, [_P, _P, _I, _I, _I, _I, _P]),
-    "wd_dist_filter0": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
-    "wd_dist_stats": (_I, [_P, _P]),
-    "wd_dist_finalize": (_I, [_P, _P]),
+    "wd_comm_unique_id": (_I, [_P]),
+    "wd_comm_init": (_I, [_P, _I, _I, _I, ctypes.POINTER(_P)]),
+    "wd_comm_init_callbacks": (_I, [_P, _I, _I, ctypes.POINTER(_P)]),
+    "wd_comm_init_solo": (_I, [_I, _I, ctypes.POINTER(_P)]),
+    "wd_comm_allgather": (_I, [_P, _P, _P, ctypes.c_longlong, _P]),
+    "wd_comm_destroy": (_I, [_P]),
+    "wd_dist_create": (_I, [_P, ctypes.POINTER(GridDesc), ctypes.POINTER(SolverDesc), _I, _I,
+                            ctypes.POINTER(_P)]),
+    "wd_dist_destroy": (_I, [_P]),
+    "wd_dist_bind": (_I, [_P, _P, _P]),
+    "wd_dist_steps": (_I, [_P, _I]),
+    "wd_dist_read_status": (_I, [_P, ctypes.POINTER(Status)]),
+    "wd_dist_finish": (_I, [_P]),
+    "wd_dist_stream": (_P, [_P]),
+    "wd_dist_context": (_P, [_P]),
+    "wd_dist_info": (_I, [_P, _IP]),
 }
 
 _lib = None

@@ -406,7 +406,10 @@ void ws_free(void* p, size_t bytes) {
 }
 }  // namespace
 
+struct wd_dist;
+
 struct wd_ctx {
+  wd_dist* dist = nullptr;  // GENERIC slab-decomposed program (wd_dist.cuh): axis-0 hooks
   wd_grid_desc gd;
   wd_solver_desc sd;
   Geom g;
@@ -441,15 +444,19 @@ struct wd_ctx {
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
   long long enq = 0;  // host-side count of enqueued steps (buffer parity)
   FusedPlan fused;    // specialised kernels (wd_fused.cuh), if applicable
-  // distributed path: filter factors for arbitrary (length, periodic)
-  std::map<std::pair<int, int>, std::pair<HostFactor, double*>> dfilt;
-  // partitioned axis-0 filter tables per (n0, P, rank) (wd_dist_filter0.cuh)
-  std::map<std::tuple<int, int, int>, std::pair<D0Tables, double*>> d0tab;
 };
 
 namespace {
 
 double lref(const wd_ctx* c) { return c->gd.ref_length; }
+
+// axis-0 operators of a slab-decomposed context run on pencils (wd_dist.cuh)
+void dist_deriv0(wd_ctx* c, const double* in, double* out, int scheme, const Epi& e,
+                 const Status* st);
+void dist_uw0(wd_ctx* c, const double* p, double* B, double* F, double* dphi, const Status* st);
+void dist_d40(wd_ctx* c, const double* p, double* out, const Epi& e, const Status* st);
+void dist_filter0_generic(wd_ctx* c, const double* cur, double* nxt, const Status* st);
+void dist_reduce_status(wd_ctx* c);
 
 Epi epi_plain() { return Epi{0, nullptr, nullptr, 0.0}; }
 
@@ -522,6 +529,10 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
 void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int axis, int scheme,
                   Epi e, const Status* st) {
   const Geom& g = c->g;
+  if (c->dist && axis == 0) {
+    dist_deriv0(c, in, out, scheme, e, st);
+    return;
+  }
   if ((scheme == WD_C4 || scheme == WD_C6) && c->cscan[axis].tab && scheme == c->sd.scheme) {
     // arith="fast": segmented-scan solve, epilogue fused (wd_deriv_scan.cuh)
     DScanArgs a;
@@ -607,7 +618,9 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
 // directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
 void launch_dphi(wd_ctx* c, const double* p, const Status* st) {
   for (int l = 0; l < c->g.nd; ++l) {
-    if (c->sd.scheme == WD_UW)
+    if (c->sd.scheme == WD_UW && c->dist && l == 0)
+      dist_uw0(c, p, c->B[l], c->F[l], c->dphi[l], st);
+    else if (c->sd.scheme == WD_UW)
       k_uw_bf<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(p, c->B[l], c->F[l],
                                                                       c->dphi[l],
                                                                       axis_geom(c->g, l),
@@ -625,6 +638,10 @@ void launch_gamma_lad(wd_ctx* c, const double* p, const Status* st) {
     e.acc = c->tmp2;
     e.cfield = c->sums_dev ? c->sums_dev + (2 + l) * g.N : nullptr;
     e.cscal = c->sqrtS_c[l];
+    if (c->dist && l == 0) {
+      dist_d40(c, p, c->tmp2, e, st);
+      continue;
+    }
     k_d4<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, axis_geom(g, l), g.per[l], e, st);
   }
   k_gamma_lad<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(p, c->tmp2, c->gam, g.N,
@@ -736,6 +753,11 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
   for (int a = 0; a < g.nd; ++a) {
     double* nxt = bufs[a & 1];
     const long long L = g.N / g.n[a];
+    if (c->dist && a == 0) {
+      dist_filter0_generic(c, cur, nxt, st);
+      cur = nxt;
+      continue;
+    }
     // arith="fast", 3-D, no solid mask: the segmented-scan sweep
     // (wd_filter_scan.cuh).  It does not restore pinned nodes, which is
     // exact here: the input is BC'd (walls are 0), a wall of this axis is a
@@ -849,6 +871,7 @@ void enqueue_step(wd_ctx* c, const double* A, double* B) {
   enqueue_rk4(c, A, B, c->st, true);
   k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
                                                                    c->g.N);
+  if (c->dist) dist_reduce_status(c);
   k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
 }
 
@@ -1075,8 +1098,6 @@ int wd_destroy(wd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   fused_release(c->fused);
-  for (auto& kv : c->dfilt) cudaFree(kv.second.second);
-  for (auto& kv : c->d0tab) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
   ws_free(c->ws, (size_t)7 * c->g.N * sizeof(double));
@@ -1567,216 +1588,4 @@ int wd_levelset_step(wd_ctx* c, const double* p0, double* out, double F, double 
 
 }  // extern "C"
 
-// ====================================================================
-// Slab decomposition (EXTENSION, paper_2111_09859_b200/dist.py): one RK
-// stage on a ghosted slab, filter sweeps on arbitrary arrays, slab <->
-// pencil packing for the all_to_all transpose, and the status reduction
-// hand-off around an all_reduce(max).
-namespace {
-__global__ void k_pack_slab(const double* __restrict__ slab, double* __restrict__ buf, int nl,
-                            int n1, int n2, int P) {
-  // slab (nl, n1, n2) -> buf (P, nl, n1/P, n2)
-  const int m1 = n1 / P;
-  const long long N = (long long)nl * n1 * n2;
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < N;
-       o += (long long)gridDim.x * blockDim.x) {
-    long long t = o;
-    const int k = (int)(t % n2);
-    t /= n2;
-    const int jj = (int)(t % m1);
-    t /= m1;
-    const int i = (int)(t % nl);
-    const int q = (int)(t / nl);
-    buf[o] = slab[((long long)i * n1 + (long long)q * m1 + jj) * n2 + k];
-  }
-}
-__global__ void k_unpack_slab(const double* __restrict__ buf, double* __restrict__ slab, int nl,
-                              int n1, int n2, int P) {
-  const int m1 = n1 / P;
-  const long long N = (long long)nl * n1 * n2;
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < N;
-       o += (long long)gridDim.x * blockDim.x) {
-    long long t = o;
-    const int k = (int)(t % n2);
-    t /= n2;
-    const int jj = (int)(t % m1);
-    t /= m1;
-    const int i = (int)(t % nl);
-    const int q = (int)(t / nl);
-    slab[((long long)i * n1 + (long long)q * m1 + jj) * n2 + k] = buf[o];
-  }
-}
-__global__ void k_stats_out(Status* st, long long* out) {
-  out[0] = (long long)st->max_delta_bits;
-  out[1] = (long long)st->max_abs_bits;
-  out[2] = st->nonfinite;
-}
-__global__ void k_stats_in(Status* st, const long long* in) {
-  st->max_delta_bits = (unsigned long long)in[0];
-  st->max_abs_bits = (unsigned long long)in[1];
-  st->nonfinite = (int)in[2];
-}
-}  // namespace
-
-extern "C" {
-
-int wd_dist_configure(wd_ctx* c, int i_lo, int i_hi) {
-  if (!c || !c->fused.active) return fail(WD_ERR_INVALID, "distributed path needs the fused 3-D path");
-  if (i_lo < 0 || i_hi > c->g.n[0] || i_lo >= i_hi) return fail(WD_ERR_INVALID, "bad plane range");
-  c->fused.i_lo = i_lo;
-  c->fused.i_hi = i_hi;
-  return WD_OK;
-}
-
-int wd_dist_stage(wd_ctx* c, int stage, const double* A, const double* p, double* out) {
-  if (!c || !c->fused.active || stage < 1 || stage > 4) return fail(WD_ERR_INVALID, "bad arguments");
-  fused_stage_ptrs(c->fused, stage, A, p, out, c->st, c->stream);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, int n1, int n2,
-                   int periodic, const double* A) {
-  if (!c || !c->fused.active || !c->sd.use_filter || axis < 0 || axis > 2)
-    return fail(WD_ERR_INVALID, "bad arguments");
-  const int nn[3] = {n0, n1, n2};
-  const int n = nn[axis];
-  auto key = std::make_pair(n, periodic ? 1 : 0);
-  auto it = c->dfilt.find(key);
-  if (it == c->dfilt.end()) {
-    HostFactor F;
-    int rc = filter_factor(c->sd.alpha_f, n, periodic, F);
-    if (rc) return rc;
-    for (double sw : F.swap)
-      if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
-    std::vector<double> packed, sc;
-    factor_pack(F, packed);
-    int m = 0;
-    const size_t nf = packed.size();
-    if (c->sd.arith == 1 && scan_pack(F, sc, m)) packed.insert(packed.end(), sc.begin(), sc.end());
-    double* dev = nullptr;
-    CK(cudaMalloc(&dev, packed.size() * sizeof(double)));
-    CK(cudaMemcpy(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
-    fused_filter_prepare(n);
-    F.scan_m = m;
-    F.scan_off = nf;
-    it = c->dfilt.emplace(key, std::make_pair(F, dev)).first;
-  }
-  const TriDev T = factor_view(it->second.first, it->second.second);
-  ScanDev SD;
-  if (it->second.first.scan_m) {
-    SD.n = n;
-    SD.m = it->second.first.scan_m;
-    SD.tab = it->second.second + it->second.first.scan_off;
-    SD.denom = it->second.first.cyclic ? it->second.first.denom : 1.0;
-  }
-  fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream,
-                   SD.n ? &SD : nullptr);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_filter0(wd_ctx* c, int phase, const double* in, double* out, int n0, int n1, int n2,
-                    int G, int P, int rank, const double* xa, const double* xb, double* mine) {
-  if (!c || !c->fused.active || !c->sd.use_filter || phase < 1 || phase > 3 || P < 1 ||
-      rank < 0 || rank >= P || n0 % P || !in || !out || !mine)
-    return fail(WD_ERR_INVALID, "bad arguments");
-  const int nl = n0 / P;
-  if (G < 5) return fail(WD_ERR_INVALID, "the axis-0 filter needs 5 ghost planes");
-  auto key = std::make_tuple(n0, P, rank);
-  auto it = c->d0tab.find(key);
-  if (it == c->d0tab.end()) {
-    HostFactor F;
-    int rc = filter_factor(c->sd.alpha_f, n0, 1, F);
-    if (rc) return rc;
-    for (double sw : F.swap)
-      if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
-    // global rows (the scan_pack conventions): fm, 1/d, g, h, z
-    std::vector<double> fm(n0), ri(n0), g(n0), h(n0), z(n0);
-    for (int r = 0; r < n0; ++r) {
-      fm[r] = r > 0 ? F.fact[r - 1] : 0.0;
-      ri[r] = 1.0 / F.d[r];
-      g[r] = r < n0 - 1 ? F.du[r] * ri[r] : 0.0;
-      h[r] = F.cyclic ? F.h[r] : 0.0;
-      z[r] = F.cyclic ? F.z[r] : 0.0;
-    }
-    std::vector<double> tab((size_t)6 * nl + 2 * P);
-    const int lo = rank * nl;
-    for (int r = 0; r < nl; ++r) {
-      tab[r] = fm[lo + r];
-      tab[nl + r] = ri[lo + r];
-      tab[2 * nl + r] = g[lo + r];
-      tab[3 * nl + r] = h[lo + r];
-      tab[4 * nl + r] = z[lo + r];
-    }
-    double qp = 1.0;  // Qpref_r = prod_{t = r}^{hi - 1} (-g_t)
-    for (int r = nl - 1; r >= 0; --r) {
-      qp *= -g[lo + r];
-      tab[5 * nl + r] = qp;
-    }
-    for (int q = 0; q < P; ++q) {
-      double pb = 1.0, qb = 1.0;
-      for (int r = q * nl; r < (q + 1) * nl; ++r) {
-        pb *= -fm[r];
-        qb *= -g[r];
-      }
-      tab[6 * nl + 2 * q] = pb;
-      tab[6 * nl + 2 * q + 1] = qb;
-    }
-    double* dev = nullptr;
-    CK(cudaMalloc(&dev, tab.size() * sizeof(double)));
-    CK(cudaMemcpy(dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
-    D0Tables T;
-    T.row = dev;
-    T.blk = dev + 6 * nl;
-    T.P = P;
-    T.rank = rank;
-    T.nl = nl;
-    T.denom = F.cyclic ? F.denom : 0.0;
-    it = c->d0tab.emplace(key, std::make_pair(T, dev)).first;
-  }
-  const D0Tables& T = it->second.first;
-  const long long lines = (long long)n1 * n2;
-  const int blocks = nblocks(lines, 128);
-  if (phase == 1)
-    k_dist_filter0<1><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
-  else if (phase == 2)
-    k_dist_filter0<2><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
-  else
-    k_dist_filter0<3><<<blocks, 128, 0, c->stream>>>(in, out, n1, n2, G, T, c->fcoef, xa, xb, mine, c->st);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_pack(const double* slab, double* buf, int nl, int n1, int n2, int P, void* stream) {
-  if (!slab || !buf || P < 1 || n1 % P) return fail(WD_ERR_INVALID, "bad arguments");
-  const long long N = (long long)nl * n1 * n2;
-  k_pack_slab<<<nblocks(N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(slab, buf, nl, n1, n2, P);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_unpack(const double* buf, double* slab, int nl, int n1, int n2, int P, void* stream) {
-  if (!slab || !buf || P < 1 || n1 % P) return fail(WD_ERR_INVALID, "bad arguments");
-  const long long N = (long long)nl * n1 * n2;
-  k_unpack_slab<<<nblocks(N, kThreads), kThreads, 0, (cudaStream_t)stream>>>(buf, slab, nl, n1, n2, P);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_stats(wd_ctx* c, long long* dev3) {
-  if (!c || !dev3) return fail(WD_ERR_INVALID, "bad arguments");
-  k_stats_out<<<1, 1, 0, c->stream>>>(c->st, dev3);
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-int wd_dist_finalize(wd_ctx* c, const long long* dev3) {
-  if (!c || !dev3 || !c->hist) return fail(WD_ERR_INVALID, "bad arguments");
-  k_stats_in<<<1, 1, 0, c->stream>>>(c->st, dev3);
-  k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
-  CK(cudaGetLastError());
-  return WD_OK;
-}
-
-}  // extern "C"
+#include "wd_dist.cuh"

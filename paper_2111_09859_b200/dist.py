@@ -1,41 +1,43 @@
-"""Slab decomposition of the fused 3-D pseudo-time solve over P GPUs.
+"""Slab decomposition of the pseudo-time solve over P GPUs.
 
-SURVEY §8(e): one process per GPU; the grid is split along axis 0 (the
-memory-slowest axis, periodic in BASELINE configs 4 and 5) into contiguous
-slabs of ``nl = n0 / P`` planes, each stored with ``G`` ghost planes per side.
-One pseudo-step:
+One process per GPU; rank r owns the planes ``[r n0/P, (r+1) n0/P)`` of the
+periodic axis 0 (the memory-slowest axis: ghost planes and slabs are
+contiguous).  The whole step program lives in the native library
+(``csrc/wd_dist.cuh``, C ABI ``wd_comm_*`` / ``wd_dist_*``):
 
-* before each RK stage, exchange the stage input's ghost planes with both
-  ring neighbours (``send/recv``, NCCL over NVLink);
-* run the fused stage kernel on the slab interior (``wd_dist_stage``);
-* filter axis 0 on full x-lines.  Exact arithmetic: pack the slab into P
-  chunks, ``all_to_all`` to pencils ``(n0, n1/P, n2)``, sweep, ``all_to_all``
-  back (bit-identical to one GPU).  Fast arithmetic (default there): the
-  partitioned solve of ``csrc/wd_dist_filter0.cuh`` -- ghost exchange of the
-  filter input, then per line one forward carry and one backward carry
-  ``all_gather``-ed between three local kernels (2 + 1 doubles per line per
-  rank instead of two transposes of the whole slab: ~6 MB vs ~234 MB per GPU
-  and step at 512^3, P = 8);
-* filter axes 1 and 2 on the slab; the last sweep accumulates the local
-  ``max|Δφ|``, ``max|φ|`` and non-finite flag;
-* ``all_reduce(max)`` of those three words, then the stop test.
+* fused 3-D path (BASELINE config 4): ghost-plane exchange per RK stage,
+  overlapped with the interior planes; axis-0 filter as a partitioned solve
+  (fast arithmetic: one local scan kernel, ONE all_gather of three doubles
+  per line, one fix-up) or a slab <-> pencil transpose pair (exact arithmetic:
+  bit-identical to one GPU); one ``all_reduce(max)`` of three words per step;
+* generic path (compact / curvilinear / LAD / curvature / Poisson / UW,
+  BASELINE config 5): every operator ALONG axis 0 runs on pencils between
+  two all_to_all transposes, everything else is local -- bit-identical.
 
-With the transposed axis-0 filter every node and every filter line sees
-exactly the operations of the single-GPU path, so the decomposed solve is
-bit-identical to it; the partitioned filter solves the same linear system
-with another association (round-off level; checked by
-``tests/test_gpu_dist.py`` with P simulated ranks on one GPU).
+Communicators:
+
+* :class:`NcclComm` -- the product path: NCCL inside the library
+  (``wd_comm_init``), the k-step CUDA graph contains the collectives;
+* :class:`TorchComm` -- the same program over any ``torch.distributed``
+  backend through host callbacks (gloo stages through the host; used by the
+  multi-process tests on one GPU or none);
+* :class:`LocalComm` -- P logical ranks in one process, one thread each
+  (device copies stand in for NVLink; every wait is a host barrier, so no
+  kernel ever waits on another rank's kernel).
+
+``solve_steady(grid, boundary, config, comm=...)`` is the user entry point.
 """
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native as nat
 
-GHOST = 7  # >= 4 + R (exact axis-0 windows) and >= 2R (fast mode), R <= 3
+GHOST = 7  # fused path: >= 4 + R (exact axis-0 windows) and >= 2R (fast), R <= 3
 
 
 @dataclass(frozen=True)
@@ -45,7 +47,6 @@ class Slab:
     n0: int
     P: int
     rank: int
-    G: int = GHOST
 
     @property
     def nl(self) -> int:
@@ -56,6 +57,10 @@ class Slab:
         return self.rank * self.nl
 
     @property
+    def hi(self) -> int:
+        return self.lo + self.nl
+
+    @property
     def left(self) -> int:
         return (self.rank - 1) % self.P
 
@@ -63,30 +68,161 @@ class Slab:
     def right(self) -> int:
         return (self.rank + 1) % self.P
 
-    def check(self, n1: int):
+    def check(self):
         if self.n0 % self.P:
             raise ValueError(f"axis 0 ({self.n0}) must divide evenly over {self.P} ranks")
-        if n1 % self.P:
-            raise ValueError(f"axis 1 ({n1}) must divide evenly over {self.P} ranks")
-        if self.nl < self.G:
-            raise ValueError(f"slab of {self.nl} planes is thinner than {self.G} ghost planes")
 
 
 def split_global(field, P):
-    """Global (n0, n1, n2) array -> list of P ghosted slabs (ghosts zero)."""
+    """Global (n0, ...) array -> list of P contiguous slabs."""
     n0 = field.shape[0]
-    out = []
-    for r in range(P):
-        s = Slab(n0, P, r)
-        g = np.zeros((s.nl + 2 * s.G,) + field.shape[1:])
-        g[s.G:s.G + s.nl] = field[s.lo:s.lo + s.nl]
-        out.append(g)
-    return out
+    if n0 % P:
+        raise ValueError(f"axis 0 ({n0}) must divide evenly over {P} ranks")
+    nl = n0 // P
+    return [np.ascontiguousarray(field[r * nl:(r + 1) * nl]) for r in range(P)]
+
+
+class _DevArray:
+    """Raw device memory as a ``__cuda_array_interface__`` object."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2}
+
+
+def dev_view(ptr, n, dtype="f8"):
+    """Zero-copy torch view of ``n`` elements of device memory at ``ptr``."""
+    import torch
+    return torch.as_tensor(_DevArray(ptr, n, "<" + dtype), device="cuda")
 
 
 # ------------------------------------------------------------- communicators
-class TorchComm:
-    """One rank of a torch.distributed group (NCCL on GPUs, gloo on CPU)."""
+class _Comm:
+    """Owner of a native ``wd_comm``."""
+
+    ptr = None
+    P = 1
+    rank = 0
+
+    def close(self):
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            nat.lib().wd_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # collectives used outside the step program (collecting a result)
+    def allgather(self, mine, stream=None):
+        """(P * n,) tensor of every rank's ``mine`` (n,), rank order."""
+        import torch
+        out = torch.empty(self.P * mine.numel(), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        nat.check(nat.lib().wd_comm_allgather(self.ptr, mine.data_ptr(), out.data_ptr(),
+                                              mine.numel(), stream))
+        torch.cuda.synchronize()
+        return out
+
+
+class NcclComm(_Comm):
+    """NCCL communicator owned by the library (``wd_comm_init``).  ``nccl_id``
+    is the 128-byte id made by rank 0 (:meth:`unique_id`); :meth:`from_torch`
+    broadcasts it over an initialised ``torch.distributed`` group."""
+
+    def __init__(self, rank: int, nranks: int, nccl_id: bytes | None = None):
+        lib = nat.lib()
+        self.rank, self.P = int(rank), int(nranks)
+        if self.P > 1 and (nccl_id is None or len(nccl_id) != 128):
+            raise ValueError("a 128-byte NCCL unique id is required for more than one rank")
+        buf = ctypes.create_string_buffer(nccl_id or b"", 128)
+        ptr = ctypes.c_void_p()
+        nat.check(lib.wd_comm_init(buf, self.rank, self.P, 0, ctypes.byref(ptr)))
+        self.ptr = ptr
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        nat.check(nat.lib().wd_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, group=None):
+        import torch.distributed as dist
+        rank, P = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 and P > 1 else None]
+        if P > 1:
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+        return cls(rank, P, box[0])
+
+
+class SoloComm(_Comm):
+    """One rank of a P-way decomposition run alone on one GPU (benchmarking
+    the per-GPU kernel time of a P-way split): the slab wraps onto itself and
+    the collectives are device copies of the real volume."""
+
+    def __init__(self, nranks: int, rank: int = 0):
+        self.rank, self.P = int(rank), int(nranks)
+        ptr = ctypes.c_void_p()
+        nat.check(nat.lib().wd_comm_init_solo(self.rank, self.P, ctypes.byref(ptr)))
+        self.ptr = ptr
+
+
+class _CallbackComm(_Comm):
+    """Base of the host-callback communicators: subclasses implement
+    ``_halo``, ``_allgather``, ``_alltoall``, ``_allreduce_max`` on torch
+    views of the device buffers."""
+
+    def _register(self):
+        import torch
+        lib = nat.load()  # the callback communicator itself needs no device
+
+        def guard(fn):
+            def run(*a):
+                try:
+                    fn(*a)
+                    return 0
+                except Exception as exc:  # surfaced as WD_ERR_CUDA by the library
+                    self.error = exc
+                    return 1
+            return run
+
+        def halo(user, slab, plane, nl, G, stream):
+            stream = stream or 0
+            t = dev_view(slab, (nl + 2 * G) * plane).view(nl + 2 * G, plane)
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self._halo(t, nl, G)
+
+        def gather(user, mine, out, count, stream):
+            stream = stream or 0
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self._allgather(dev_view(mine, count), dev_view(out, count * self.P))
+
+        def a2a(user, send, recv, count, stream):
+            stream = stream or 0
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self._alltoall(dev_view(send, count * self.P), dev_view(recv, count * self.P))
+
+        def red(user, buf, n, stream):
+            stream = stream or 0
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self._allreduce_max(dev_view(buf, n, "i8"))
+
+        self.error = None
+        self._cbs = nat.CommCallbacks(None, nat.HALO_CB(guard(halo)), nat.GATHER_CB(guard(gather)),
+                                      nat.GATHER_CB(guard(a2a)), nat.REDUCE_CB(guard(red)))
+        ptr = ctypes.c_void_p()
+        nat.check(lib.wd_comm_init_callbacks(ctypes.byref(self._cbs), self.rank, self.P,
+                                             ctypes.byref(ptr)))
+        self.ptr = ptr
+
+
+class TorchComm(_CallbackComm):
+    """One rank of a ``torch.distributed`` group.  NCCL groups move device
+    tensors directly; other backends (gloo) stage through the host."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -94,329 +230,288 @@ class TorchComm:
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.on_device = "nccl" in str(dist.get_backend(group))
+        self._register()
 
-    def halo(self, slabs, slab: Slab):
-        """Fill the ghost planes of this rank's (nl + 2G, ...) tensor."""
-        self.halo_finish(self.halo_start(slabs, slab), slabs, slab)
+    def _peer(self, r):
+        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
 
-    def halo_start(self, slabs, slab: Slab):
-        """Post the ghost-plane exchange; the caller may enqueue work that
-        does not read the ghost planes before halo_finish."""
-        (t,) = slabs
-        G, nl = slab.G, slab.nl
-        if self.P == 1:
-            t[:G].copy_(t[nl:nl + G])
-            t[nl + G:].copy_(t[G:2 * G])
-            return None
+    def _stage(self, t):
+        return t if self.on_device else t.cpu()
+
+    def _halo(self, t, nl, G):
         d = self.dist
-        lo = t.new_empty(t[:G].shape)
-        hi = t.new_empty(t[:G].shape)
+        left, right = self._peer((self.rank - 1) % self.P), self._peer((self.rank + 1) % self.P)
+        up, down = self._stage(t[nl:nl + G].contiguous()), self._stage(t[G:2 * G].contiguous())
+        lo = t[:G] if self.on_device else up.new_empty(up.shape)
+        hi = t[nl + G:] if self.on_device else up.new_empty(up.shape)
         # posting order matters when left == right (P = 2): point-to-point
-        # ops between one pair of ranks match in the order they are posted
-        ops = [d.P2POp(d.isend, t[nl:nl + G].contiguous(), slab.right, self.group),
-               d.P2POp(d.irecv, lo, slab.left, self.group),
-               d.P2POp(d.isend, t[G:2 * G].contiguous(), slab.left, self.group),
-               d.P2POp(d.irecv, hi, slab.right, self.group)]
-        return d.batch_isend_irecv(ops), lo, hi
-
-    def halo_finish(self, handle, slabs, slab: Slab):
-        if handle is None:
-            return
-        (t,) = slabs
-        reqs, lo, hi = handle
-        for req in reqs:
+        # operations between one pair of ranks match in posting order
+        ops = [d.P2POp(d.isend, up, right, self.group), d.P2POp(d.irecv, lo, left, self.group),
+               d.P2POp(d.isend, down, left, self.group), d.P2POp(d.irecv, hi, right, self.group)]
+        for req in d.batch_isend_irecv(ops):
             req.wait()
-        t[:slab.G].copy_(lo)
-        t[slab.nl + slab.G:].copy_(hi)
+        if not self.on_device:
+            t[:G].copy_(lo)
+            t[nl + G:].copy_(hi)
 
-    def alltoall(self, outs, ins):
-        (o,), (i,) = outs, ins
-        if self.P == 1:
-            o.copy_(i)
+    def _allgather(self, mine, out):
+        if self.on_device:
+            self.dist.all_gather_into_tensor(out, mine, group=self.group)
             return
-        self.dist.all_to_all_single(o, i, group=self.group)
+        o = out.new_empty(out.shape, device="cpu")
+        self.dist.all_gather_into_tensor(o, mine.cpu(), group=self.group)
+        out.copy_(o)
 
-    def allgather(self, outs, ins):
-        """outs[0] (P * len(ins[0]),) <- every rank's ins[0], rank order."""
-        (o,), (i,) = outs, ins
-        if self.P == 1:
-            o.copy_(i)
+    def _alltoall(self, send, recv):
+        if self.on_device:
+            self.dist.all_to_all_single(recv, send, group=self.group)
             return
-        self.dist.all_gather_into_tensor(o, i, group=self.group)
+        # gloo has no all_to_all on every build: P - 1 pairwise exchanges
+        P, me = self.P, self.rank
+        s = send.cpu().view(P, -1)
+        r = s.new_empty(s.shape)
+        r[me].copy_(s[me])
+        d = self.dist
+        ops = []
+        for q in range(P):
+            if q != me:
+                ops.append(d.P2POp(d.isend, s[q].contiguous(), self._peer(q), self.group))
+                ops.append(d.P2POp(d.irecv, r[q], self._peer(q), self.group))
+        for req in d.batch_isend_irecv(ops):
+            req.wait()
+        recv.copy_(r.view(-1))
 
-    def allreduce_max(self, ts):
-        (t,) = ts
-        if self.P > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+    def _allreduce_max(self, buf):
+        if self.on_device:
+            self.dist.all_reduce(buf, op=self.dist.ReduceOp.MAX, group=self.group)
+            return
+        h = buf.cpu()
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+        buf.copy_(h)
 
 
-class LocalComm:
-    """P logical ranks in one process (device copies stand in for NVLink).
-    Used to check the decomposition on one GPU: no kernel ever waits on
-    another rank's kernel."""
+class LocalGroup:
+    """P logical ranks in one process, one thread per rank.  Collectives
+    publish their device views, meet at a host barrier and copy; used to
+    check the decomposed programs on a single GPU."""
 
     def __init__(self, P):
-        self.P = P
+        self.P = int(P)
+        self.barrier = threading.Barrier(self.P)
+        self.slots = [None] * self.P
+        self.comms = [LocalComm(self, r) for r in range(self.P)]
 
-    def halo_start(self, slabs, slab: Slab):
-        self.halo(slabs, slab)
-        return None
-
-    def halo_finish(self, handle, slabs, slab: Slab):
-        return None
-
-    def halo(self, slabs, slab: Slab):
-        G, nl = slab.G, slab.nl
-        P = self.P
-        lows = [t[G:2 * G].clone() for t in slabs]
-        highs = [t[nl:nl + G].clone() for t in slabs]
-        for r, t in enumerate(slabs):
-            t[:G].copy_(highs[(r - 1) % P])
-            t[nl + G:].copy_(lows[(r + 1) % P])
-
-    def alltoall(self, outs, ins):
-        P = self.P
-        chunks = [i.view(P, -1) for i in ins]
-        for r, o in enumerate(outs):
-            ov = o.view(P, -1)
-            for s in range(P):
-                ov[s].copy_(chunks[s][r])
-
-    def allgather(self, outs, ins):
-        P = self.P
-        for o in outs:
-            ov = o.view(P, -1)
-            for s_ in range(P):
-                ov[s_].copy_(ins[s_])
-
-    def allreduce_max(self, ts):
+    def run(self, fn):
+        """``fn(rank)`` on P threads; returns the list of results and
+        re-raises the first exception."""
         import torch
-        m = torch.stack(list(ts)).max(dim=0).values
+        out, errs = [None] * self.P, [None] * self.P
+        dev = torch.cuda.current_device()
+
+        def work(r):
+            try:
+                torch.cuda.set_device(dev)
+                out[r] = fn(r)
+            except BaseException as exc:  # noqa: BLE001
+                errs[r] = exc
+                self.barrier.abort()
+
+        ts = [threading.Thread(target=work, args=(r,)) for r in range(self.P)]
         for t in ts:
-            t.copy_(m)
+            t.start()
+        for t in ts:
+            t.join()
+        self.barrier.reset()
+        real = [e for e in errs if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+        if real or any(errs):
+            raise (real or [e for e in errs if e is not None])[0]
+        return out
+
+    def exchange(self, rank, view):
+        """Publish ``view``; returns every rank's view once all have posted
+        (their producing streams synchronised)."""
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.slots[rank] = view
+        self.barrier.wait()
+        return list(self.slots)
+
+    def done(self):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+
+
+class LocalComm(_CallbackComm):
+    def __init__(self, group: LocalGroup, rank: int):
+        self.g = group
+        self.P = group.P
+        self.rank = int(rank)
+        self._register()
+
+    def _halo(self, t, nl, G):
+        P, me = self.P, self.rank
+        views = self.g.exchange(me, t)
+        t[:G].copy_(views[(me - 1) % P][nl:nl + G])
+        t[nl + G:].copy_(views[(me + 1) % P][G:2 * G])
+        self.g.done()
+
+    def _allgather(self, mine, out):
+        views = self.g.exchange(self.rank, mine)
+        o = out.view(self.P, -1)
+        for q in range(self.P):
+            o[q].copy_(views[q])
+        self.g.done()
+
+    def _alltoall(self, send, recv):
+        views = self.g.exchange(self.rank, send)
+        r = recv.view(self.P, -1)
+        for q in range(self.P):
+            r[q].copy_(views[q].view(self.P, -1)[self.rank])
+        self.g.done()
+
+    def _allreduce_max(self, buf):
+        import torch
+        views = self.g.exchange(self.rank, buf)
+        m = torch.stack(views).max(dim=0).values
+        self.g.done()   # every rank has read every buffer
+        buf.copy_(m)
+        self.g.done()
 
 
 # ------------------------------------------------------------------ solver
 class DistributedSolve:
-    """Fused 3-D pseudo-time solve on the slabs of ``ranks`` (one entry per
-    local logical rank: 1 under torchrun, P in the simulated mode)."""
+    """This rank's share of a decomposed pseudo-time solve (``wd_dist``).
 
-    def __init__(self, dims, spacing, faces, scheme, formulation, filter_config, cfl, tol,
-                 max_iters, arith, comm, ranks, ref_length=1.0, filter0=None, overlap=True):
+    ``grid`` is the GLOBAL grid (identical on every rank), ``faces`` its face
+    kinds, ``solid_mask`` the global mask or None.  The state is the rank's
+    ``(nl, n1[, n2])`` slab, a CUDA tensor owned by this object.
+    """
+
+    FILTER0 = {None: -1, "partitioned": 0, "transpose": 1}
+
+    def __init__(self, grid, faces, config, comm, solid_mask=None, filter0=None, overlap=True,
+                 hist_len=None):
         import torch
-        from ._context import NativeSolver
-        from .grid import CurvilinearGrid
+        from ._context import face_codes
         self.torch = torch
         self.comm = comm
-        n0, n1, n2 = dims
-        P = comm.P
-        if faces.get("imin") != "periodic":
-            raise ValueError("slab decomposition needs a periodic axis 0")
-        if filter_config is None:
-            raise ValueError("the distributed path runs the filtered scheme")
-        self.dims = dims
-        self.slabs = [Slab(n0, P, r) for r in ranks]
-        for s in self.slabs:
-            s.check(n1)
-        s0 = self.slabs[0]
-        self.nl, self.G = s0.nl, s0.G
-        gdims = (self.nl + 2 * self.G, n1, n2)
-        # local geometry: ghosted slab, axis 0 open (ghosts carry the wrap)
-        lfaces = {k: v for k, v in faces.items() if k not in ("imin", "imax")}
-        per = (False, faces.get("jmin") == "periodic", faces.get("kmin") == "periodic")
-        self.per = per
-        g = CurvilinearGrid._analytic((0.0, 0.0, 0.0), spacing, gdims, ref_length, per,
-                                      [spacing[d] * gdims[d] for d in range(3)])
-        self.ctxs = []
-        self.hists = []
-        for _ in ranks:
-            ctx = NativeSolver(g, lfaces, None, scheme, formulation, filter_config, cfl, tol,
-                               max_iters, arith=arith)
-            if not ctx.fused:
-                raise ValueError("configuration is not on the fused 3-D path")
-            nat.check(ctx.lib.wd_dist_configure(ctx.ptr, self.G, self.G + self.nl))
-            self.ctxs.append(ctx)
-        self.lib = self.ctxs[0].lib
-        f64 = dict(dtype=torch.float64, device="cuda")
-        R = len(ranks)
-        self.A = [torch.zeros(gdims, **f64) for _ in range(R)]
-        self.B = [torch.zeros(gdims, **f64) for _ in range(R)]
-        self.Pa = [torch.zeros(gdims, **f64) for _ in range(R)]
-        self.Pb = [torch.zeros(gdims, **f64) for _ in range(R)]
-        nlc = self.nl * n1 * n2
-        self.send = [torch.empty(nlc, **f64) for _ in range(R)]
-        self.pen = [torch.empty(nlc, **f64) for _ in range(R)]
-        self.pen2 = [torch.empty(nlc, **f64) for _ in range(R)]
-        self.back = [torch.empty(nlc, **f64) for _ in range(R)]
-        self.slab1 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
-        self.slab2 = [torch.empty((self.nl, n1, n2), **f64) for _ in range(R)]
-        self.stats = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(R)]
-        # stage kernels on the planes that need no ghost while the ghost
-        # planes are in flight, then the 2 x G boundary planes
-        self.overlap = bool(overlap) and self.nl >= 2 * self.G + 8
-        # axis-0 filter: "partitioned" (fast arithmetic) or "transpose"
-        self.filter0 = filter0 or ("partitioned" if arith == "fast" else "transpose")
-        if self.filter0 not in ("partitioned", "transpose"):
-            raise ValueError(f"unknown axis-0 filter mode {self.filter0!r}")
-        if self.filter0 == "partitioned" and arith != "fast":
-            raise ValueError("the partitioned axis-0 filter is a fast-arithmetic path")
-        lines = n1 * n2
-        self.mineA = [torch.empty(2 * lines, **f64) for _ in range(R)]
-        self.mineB = [torch.empty(lines, **f64) for _ in range(R)]
-        self.gathA = [torch.empty(P * 2 * lines, **f64) for _ in range(R)]
-        self.gathB = [torch.empty(P * lines, **f64) for _ in range(R)]
-        for ctx in self.ctxs:
-            h = torch.zeros(max(max_iters, 1), **f64)
-            self.hists.append(h)
+        self.lib = lib = nat.lib()
+        self.grid = grid
+        if filter0 not in self.FILTER0:
+            raise ValueError(f"unknown axis-0 filter mode {filter0!r}")
+        self.slab = Slab(int(grid.dims[0]), comm.P, comm.rank)
+        self.slab.check()
+        lo, hi = self.slab.lo, self.slab.hi
+        gd = nat.GridDesc()
+        gd.ndim = grid.ndim
+        for a, n in enumerate(grid.dims):
+            gd.dims[a] = int(n)
+        for i, c in enumerate(face_codes(grid, faces)):
+            gd.face[i] = c
+        self._keep = []
+        if grid.is_uniform:
+            gd.uniform = 1
+            for a, c in enumerate(grid.inv_spacing):
+                gd.inv_spacing[a] = c
+        else:
+            gd.uniform = 0
+            met = grid.device_metrics()
+            d = grid.ndim
+            local = met.view((d * d,) + tuple(grid.dims))[:, lo:hi].contiguous()
+            self._keep.append(local)
+            gd.metrics_dev = local.data_ptr()
+        if solid_mask is not None:
+            m = torch.as_tensor(np.ascontiguousarray(np.asarray(solid_mask, dtype=bool)[lo:hi]))
+            m = m.to(device="cuda", dtype=torch.uint8).contiguous()
+            self._keep.append(m)
+            gd.solid_mask_dev = m.data_ptr()
+        gd.ref_length = float(grid.ref_length)
+        fc = config.formulation
+        sd = nat.SolverDesc()
+        sd.scheme = nat.SCHEME_IDS[config.scheme]
+        sd.kind = nat.KIND_IDS[fc.kind]
+        sd.epsilon = float(fc.epsilon)
+        sd.lad_c = float(fc.lad_c)
+        sd.eps0 = float(fc.eps0) if fc.eps0 is not None else 1e-12 / grid.ref_length
+        sd.use_filter = 1 if config.uses_filter() else 0
+        sd.alpha_f = float(config.filter_config.alpha_f) if config.filter_config else 0.0
+        sd.cfl = float(config.cfl)
+        sd.tol = float(config.tol)
+        sd.max_iters = int(config.max_iters)
+        sd.arith = {"exact": 0, "fast": 1}[config.arith]
+        self.gd, self.sd = gd, sd
+        ptr = ctypes.c_void_p()
+        torch.cuda.synchronize()
+        nat.check(lib.wd_dist_create(comm.ptr, ctypes.byref(gd), ctypes.byref(sd),
+                                     self.FILTER0[filter0], 1 if overlap else 0,
+                                     ctypes.byref(ptr)))
+        self.ptr = ptr
+        info = (ctypes.c_int * 8)()
+        nat.check(lib.wd_dist_info(ptr, info))
+        self.nl, self.G = info[0], info[1]
+        self.fused, self.overlap, self.graph = bool(info[2]), bool(info[4]), bool(info[5])
+        self.filter0 = ("partitioned", "transpose")[info[3]] if self.fused else "transpose"
+        self.local_dims = (self.nl,) + tuple(grid.dims[1:])
+        self.phi = torch.zeros(self.local_dims, dtype=torch.float64, device="cuda")
+        self.hist = torch.zeros(int(hist_len or max(config.max_iters, 1)), dtype=torch.float64,
+                                device="cuda")
         self._bound = False
 
     # -- state
-    def set_state(self, local_slabs):
-        """local_slabs: per local rank, (nl, n1, n2) arrays (numpy or torch)."""
+    def bind(self, local=None):
+        """Set the rank's slab (numpy / tensor (nl, n1[, n2]); None = zeros),
+        apply the boundary conditions and reset the status."""
         torch = self.torch
-        for A, s in zip(self.A, local_slabs):
-            t = s if isinstance(s, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(s))
-            A[self.G:self.G + self.nl].copy_(t.to(A.device))
-        for ctx, A, h in zip(self.ctxs, self.A, self.hists):
-            # wd_bind applies the (wall) BCs of the local geometry and resets status
-            nat.check(self.lib.wd_bind(ctx.ptr, A.data_ptr(), h.data_ptr()))
+        if local is None:
+            self.phi.zero_()
+        else:
+            t = local if isinstance(local, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(np.asarray(local, dtype=float)))
+            if tuple(t.shape) != self.local_dims:
+                raise ValueError(f"slab shape {tuple(t.shape)} != {self.local_dims}")
+            self.phi.copy_(t.to(self.phi.device))
+        torch.cuda.synchronize()
+        nat.check(self.lib.wd_dist_bind(self.ptr, self.phi.data_ptr(), self.hist.data_ptr()))
         self._bound = True
 
-    def state(self):
-        return [A[self.G:self.G + self.nl] for A in self.A]
+    def steps(self, k=1):
+        if not self._bound:
+            raise RuntimeError("bind() a state first")
+        rc = self.lib.wd_dist_steps(self.ptr, int(k))
+        if rc and getattr(self.comm, "error", None) is not None:
+            raise self.comm.error
+        nat.check(rc)
 
-    def _interior(self, t):
-        return t[self.G:self.G + self.nl]
-
-    def step(self):
-        torch = self.torch
-        if isinstance(self.comm, LocalComm):
-            self._step()
-            return
-        # one rank per process: run torch-side transfers on the solver stream
-        with torch.cuda.stream(self.ctxs[0].stream()):
-            self._step()
-
-    def _step(self):
-        lib, comm = self.lib, self.comm
-        n0, n1, n2 = self.dims
-        P, nl = comm.P, self.nl
-        m1 = n1 // P
-        R = len(self.ctxs)
-        bufs = [self.A, self.Pa, self.Pb, self.Pa]
-        outs = [self.Pa, self.Pb, self.Pa, self.Pb]
-        G = self.G
-        for s in range(4):
-            self._sync()
-            h = comm.halo_start(bufs[s], self.slabs[0])
-
-            def launch(lo, hi):
-                for r in range(R):
-                    nat.check(lib.wd_dist_configure(self.ctxs[r].ptr, lo, hi))
-                    nat.check(lib.wd_dist_stage(self.ctxs[r].ptr, s + 1, self.A[r].data_ptr(),
-                                                bufs[s][r].data_ptr(), outs[s][r].data_ptr()))
-            if self.overlap:
-                # planes [2G, nl): every stencil reach (<= G planes) stays
-                # inside the rank's own planes
-                launch(2 * G, nl)
-                comm.halo_finish(h, bufs[s], self.slabs[0])
-                self._sync()
-                launch(G, 2 * G)
-                launch(nl, nl + G)
-            else:
-                comm.halo_finish(h, bufs[s], self.slabs[0])
-                self._sync()
-                launch(G, G + nl)
-        for r in range(R):
-            nat.check(lib.wd_dist_configure(self.ctxs[r].ptr, G, G + nl))
-        streams = [self.ctxs[r].lib.wd_get_stream(self.ctxs[r].ptr) for r in range(R)]
-        if self.filter0 == "partitioned":
-            self._filter0_partitioned()
-        else:
-            self._filter0_transpose(streams)
-        for r in range(R):
-            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 1, self.slab1[r].data_ptr(),
-                                         self.slab2[r].data_ptr(), nl, n1, n2,
-                                         int(self.per[1]), None))
-            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 2, self.slab2[r].data_ptr(),
-                                         self._interior(self.B[r]).data_ptr(), nl, n1, n2,
-                                         int(self.per[2]), self._interior(self.A[r]).data_ptr()))
-            nat.check(lib.wd_dist_stats(self.ctxs[r].ptr, self.stats[r].data_ptr()))
-        self._sync()
-        comm.allreduce_max(self.stats)
-        self._sync()
-        for r in range(R):
-            nat.check(lib.wd_dist_finalize(self.ctxs[r].ptr, self.stats[r].data_ptr()))
-        self.A, self.B = self.B, self.A
-
-    def _filter0_partitioned(self):
-        """Axis-0 filter of the stage-4 output Pb -> slab1, rows split over
-        the ranks (wd_dist_filter0: three local phases, two all_gathers)."""
-        lib, comm = self.lib, self.comm
-        n0, n1, n2 = self.dims
-        P = comm.P
-        R = len(self.ctxs)
-        self._sync()
-        comm.halo(self.Pb, self.slabs[0])
-        self._sync()
-
-        def phase(ph, mine):
-            for r in range(R):
-                nat.check(lib.wd_dist_filter0(
-                    self.ctxs[r].ptr, ph, self.Pb[r].data_ptr(), self.slab1[r].data_ptr(), n0,
-                    n1, n2, self.G, P, self.slabs[r].rank, self.gathA[r].data_ptr(),
-                    self.gathB[r].data_ptr(), mine[r].data_ptr()))
-        phase(1, self.mineA)
-        self._sync()
-        comm.allgather(self.gathA, self.mineA)
-        self._sync()
-        phase(2, self.mineB)
-        self._sync()
-        comm.allgather(self.gathB, self.mineB)
-        self._sync()
-        phase(3, self.mineB)
-
-    def _filter0_transpose(self, streams):
-        """Axis-0 filter on pencils (n0, n1/P, n2): pack, all_to_all, sweep,
-        all_to_all back, unpack -> slab1 (bit-identical to one GPU)."""
-        lib, comm = self.lib, self.comm
-        n0, n1, n2 = self.dims
-        P, nl = comm.P, self.nl
-        m1 = n1 // P
-        R = len(self.ctxs)
-        for r in range(R):
-            x = self._interior(self.Pb[r])
-            nat.check(lib.wd_dist_pack(x.data_ptr(), self.send[r].data_ptr(), nl, n1, n2, P,
-                                       streams[r]))
-        self._sync()
-        comm.alltoall(self.pen, self.send)
-        self._sync()
-        for r in range(R):
-            nat.check(lib.wd_dist_filter(self.ctxs[r].ptr, 0, self.pen[r].data_ptr(),
-                                         self.pen2[r].data_ptr(), n0, m1, n2, 1, None))
-        self._sync()
-        comm.alltoall(self.back, self.pen2)
-        self._sync()
-        for r in range(R):
-            nat.check(lib.wd_dist_unpack(self.back[r].data_ptr(), self.slab1[r].data_ptr(), nl,
-                                         n1, n2, P, streams[r]))
-
-    def _sync(self):
-        """Simulated ranks use one stream per logical rank: order them
-        around the device-copy transfers.  With one rank per process all work
-        shares the solver stream and needs no host synchronisation."""
-        if isinstance(self.comm, LocalComm):
-            self.torch.cuda.synchronize()
-
-    def status(self, r=0):
+    def status(self):
         st = nat.Status()
-        nat.check(self.lib.wd_read_status(self.ctxs[r].ptr, ctypes.byref(st)))
+        nat.check(self.lib.wd_dist_read_status(self.ptr, ctypes.byref(st)))
         return st
 
-    def history(self, r=0):
-        st = self.status(r)
-        return self.hists[r][:st.iters].cpu().numpy()
+    def finish(self):
+        """The rank's slab holding the latest state (a CUDA tensor)."""
+        nat.check(self.lib.wd_dist_finish(self.ptr))
+        return self.phi
+
+    def history(self):
+        return self.hist[:self.status().iters].cpu().numpy().copy()
+
+    def stream(self):
+        return self.torch.cuda.ExternalStream(self.lib.wd_dist_stream(self.ptr))
+
+    def gather(self):
+        """Global field (every rank): all_gather of the slabs."""
+        flat = self.comm.allgather(self.finish().reshape(-1))
+        return flat.view(tuple(self.grid.dims))
 
     def close(self):
-        for c in self.ctxs:
-            c.close()
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            self.lib.wd_dist_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

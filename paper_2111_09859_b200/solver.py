@@ -202,16 +202,23 @@ def _chunk_sizes(n_nodes: int):
 
 
 def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, exact=None,
-                 *, device_result: bool = False, chunk: int | None = None) -> SolveReport:
+                 *, device_result: bool = False, chunk: int | None = None,
+                 comm=None) -> SolveReport:
     """March to the steady wall-distance field (solver.py:221-286).
 
     Stops when max |phi - phi_old| / Lref <= tol over non-mask nodes, or at
     max_iters (converged=False).  Raises DivergenceError like the reference.
     ``device_result=True`` (extension) keeps ``report.phi`` as a CUDA tensor.
+    ``comm`` (extension): a communicator of
+    :mod:`paper_2111_09859_b200.dist` -- the solve is decomposed into slabs of
+    the periodic axis 0 over its ranks (one process per GPU); every rank
+    passes the same global ``grid`` / ``phi0`` and gets the global field back.
     """
     import torch
     if not boundary.has_wall():
         raise ValueError("boundary spec pins no wall nodes (no Dirichlet anchor)")
+    if comm is not None:
+        return _solve_steady_dist(grid, boundary, config, phi0, exact, device_result, chunk, comm)
     fc = config.formulation
     ctx = NativeSolver(grid, boundary.faces, boundary.solid_mask, config.scheme, fc,
                        config.filter_config if config.uses_filter() else None, config.cfl,
@@ -282,6 +289,67 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
         return report
     finally:
         ctx.close()
+
+
+def _solve_steady_dist(grid, boundary, config, phi0, exact, device_result, chunk, comm):
+    """solve_steady on the slabs of ``comm`` (dist.DistributedSolve): the same
+    loop, the stop decision taken in-device from all-reduced maxima, so every
+    rank leaves it at the same iteration."""
+    import torch
+    from .dist import DistributedSolve
+    fc = config.formulation
+    if exact is not None and config.l2_every > 0:
+        raise NotImplementedError("l2 sampling against an exact field is a single-GPU diagnostic")
+    ds = DistributedSolve(grid, boundary.faces, config, comm, boundary.solid_mask)
+    try:
+        lo, hi = ds.slab.lo, ds.slab.hi
+        local = None
+        if phi0 is not None:
+            local = phi0[lo:hi] if isinstance(phi0, torch.Tensor) else np.asarray(phi0)[lo:hi]
+        ds.bind(local)
+        stream = ds.stream()
+        k, kmax = _chunk_sizes(int(np.prod(ds.local_dims)))
+        if chunk is not None:
+            k = kmax = int(chunk)
+        seconds, elapsed, done = [], 0.0, 0
+        while True:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ds.steps(k)
+            e1.record(stream)
+            st = ds.status()
+            ran = st.iters - done
+            dt_chunk = e0.elapsed_time(e1) / 1e3
+            for j in range(ran):
+                seconds.append(elapsed + dt_chunk * (j + 1) / max(ran, 1))
+            elapsed += dt_chunk
+            done = st.iters
+            if st.state != nat.STATE_RUNNING:
+                break
+            k = min(2 * k, kmax)
+        if st.state == nat.STATE_DIVERGED:
+            limit = 1e6 * grid.ref_length
+            raise DivergenceError(
+                f"pseudo-time iteration diverged (max |phi| > {limit:g}) at iteration "
+                f"{st.diverged_iter}")
+        phi = ds.gather()
+        iters = st.iters
+        report = SolveReport(phi=phi if device_result else nat.to_host(phi), iters=iters,
+                             residual_history=ds.history(),
+                             wall_seconds=np.asarray(seconds[:iters]),
+                             converged=st.state == nat.STATE_CONVERGED, l2_history=None)
+        if fc.kind == "poisson":
+            # the post-map's axis-0 derivatives are collective (pencils)
+            out = torch.empty_like(ds.phi)
+            nat.check(ds.lib.wd_poisson_post(ds.lib.wd_dist_context(ds.ptr), ds.phi.data_ptr(),
+                                             out.data_ptr()))
+            full = comm.allgather(out.reshape(-1)).view(tuple(grid.dims))
+            report.phi_prime = report.phi
+            report.phi = full if device_result else nat.to_host(full)
+        return report
+    finally:
+        ds.close()
 
 
 def _l2_norm(ctx, phi, exact_t, grid, config):

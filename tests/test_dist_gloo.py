@@ -1,8 +1,9 @@
-"""The slab decomposition's host-side communication (dist.TorchComm) with
-world_size 2 over gloo on CPU: ghost-plane ring exchange, slab <-> pencil
-all_to_all (the axis-0 filter transpose) and the all_reduce(max) of the
-convergence words reassemble the global field exactly; the all_gather of
-the partitioned axis-0 filter's per-line carries arrives in rank order."""
+"""The slab decomposition's communication layer (dist.TorchComm) with
+world_size 2 over gloo on CPU: the four collectives of the native step
+program (include/walldist_b200.h: wd_comm_callbacks) -- ghost-plane ring
+exchange, slab <-> pencil all_to_all, per-line carry all_gather and the
+all_reduce(max) of the convergence words -- reassemble the global field
+exactly and arrive in rank order."""
 import os
 import socket
 
@@ -27,40 +28,44 @@ def _worker(rank, world, port, dims, q):
     try:
         from paper_2111_09859_b200 import dist
         n0, n1, n2 = dims
+        G = dist.GHOST
         glob = np.arange(n0 * n1 * n2, dtype=float).reshape(dims)
         slab = dist.Slab(n0, world, rank)
-        slab.check(n1)
-        G, nl = slab.G, slab.nl
-        t = torch.from_numpy(dist.split_global(glob, world)[rank])
+        slab.check()
+        nl = slab.nl
+        interior = dist.split_global(glob, world)[rank]
+        ghosted = np.zeros((nl + 2 * G, n1 * n2))
+        ghosted[G:G + nl] = interior.reshape(nl, -1)
+        t = torch.from_numpy(ghosted)
         comm = dist.TorchComm()
-        comm.halo([t], slab)
-        lo_expect = np.take(glob, range(slab.lo - G, slab.lo), axis=0, mode="wrap")
-        hi_expect = np.take(glob, range(slab.lo + nl, slab.lo + nl + G), axis=0, mode="wrap")
+        assert (comm.P, comm.rank) == (world, rank)
+        comm._halo(t, nl, G)
+        flat = glob.reshape(n0, -1)
+        lo_expect = np.take(flat, range(slab.lo - G, slab.lo), axis=0, mode="wrap")
+        hi_expect = np.take(flat, range(slab.hi, slab.hi + G), axis=0, mode="wrap")
         ok_halo = np.array_equal(t[:G].numpy(), lo_expect) and \
             np.array_equal(t[nl + G:].numpy(), hi_expect)
-        # slab (nl, n1, n2) -> (P, nl, n1/P, n2) as wd_dist_pack, all_to_all -> pencil
+        # slab (nl, n1, n2) -> (P, nl, n1/P, n2) as k_pack_slab, all_to_all -> pencil
         m1 = n1 // world
-        interior = t[G:G + nl].numpy()
         packed = interior.reshape(nl, world, m1, n2).transpose(1, 0, 2, 3).copy()
         send = torch.from_numpy(packed.ravel())
         recv = torch.empty_like(send)
-        comm.alltoall([recv], [send])
+        comm._alltoall(send, recv)
         pencil = recv.numpy().reshape(n0, m1, n2)
         ok_pencil = np.array_equal(pencil, glob[:, rank * m1:(rank + 1) * m1, :])
-        # back: pencil as P chunks along i -> (P, nl, m1, n2) -> unpack
         back = torch.empty_like(send)
-        comm.alltoall([back], [torch.from_numpy(pencil.ravel().copy())])
+        comm._alltoall(torch.from_numpy(pencil.ravel().copy()), back)
         unpacked = back.numpy().reshape(world, nl, m1, n2).transpose(1, 0, 2, 3).reshape(nl, n1, n2)
         ok_back = np.array_equal(unpacked, interior)
-        # per-line carries of the partitioned axis-0 filter: all_gather
         mine = torch.full((6,), float(rank + 1), dtype=torch.float64)
         gath = torch.empty(6 * world, dtype=torch.float64)
-        comm.allgather([gath], [mine])
+        comm._allgather(mine, gath)
         ok_gather = gath.view(world, 6)[:, 0].tolist() == [float(r + 1) for r in range(world)]
         stats = torch.tensor([rank * 10 + 3, 7 - rank, rank], dtype=torch.int64)
-        comm.allreduce_max([stats])
+        comm._allreduce_max(stats)
         ok_red = stats.tolist() == [(world - 1) * 10 + 3, 7, world - 1]
         q.put((rank, ok_halo, ok_pencil, ok_back, ok_red, ok_gather))
+        comm.close()
     finally:
         tdist.destroy_process_group()
 
@@ -84,8 +89,10 @@ def test_torchcomm_gloo_world2(dims):
 def test_slab_partition_bookkeeping():
     from paper_2111_09859_b200 import dist
     s = dist.Slab(64, 4, 3)
-    assert (s.nl, s.lo, s.left, s.right) == (16, 48, 2, 0)
+    assert (s.nl, s.lo, s.hi, s.left, s.right) == (16, 48, 64, 2, 0)
     parts = dist.split_global(np.arange(64 * 4 * 2, dtype=float).reshape(64, 4, 2), 4)
-    assert len(parts) == 4 and parts[0].shape == (16 + 2 * s.G, 4, 2)
+    assert len(parts) == 4 and parts[0].shape == (16, 4, 2)
     with pytest.raises(ValueError):
-        dist.Slab(64, 4, 0, G=20).check(4)
+        dist.Slab(30, 4, 0).check()
+    with pytest.raises(ValueError):
+        dist.split_global(np.zeros((30, 4)), 4)

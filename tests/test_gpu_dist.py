@@ -1,7 +1,9 @@
-"""Slab-decomposed solve (dist.py) with P logical ranks on one GPU against
-the single-GPU fused solve: bit-identical state and residual history with
-the transposed axis-0 filter; round-off-level agreement with the
-partitioned one (fast arithmetic)."""
+"""Slab-decomposed solve (dist.py, csrc/wd_dist.cuh) against the single-GPU
+solve.  P logical ranks run on one GPU, one host thread each (LocalGroup:
+device copies stand in for NVLink, every wait is a host barrier); the native
+step program is the one the NCCL communicator runs.  Transposed axis-0
+operators: bit-identical state and residual history; partitioned axis-0
+filter (fast arithmetic): round-off level, tolerance written below."""
 import numpy as np
 import pytest
 
@@ -20,76 +22,320 @@ def _need_gpu():
 
 FACES = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "wall",
          "kmin": "periodic", "kmax": "periodic"}
+CYL = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield",
+       "kmin": "periodic", "kmax": "periodic"}
+RING = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield"}
 
 
-def _run(P, arith, filter0, n0=32, overlap=True):
+def _dist_solve(P, grid, faces, cfg, phi0, steps, filter0=None, overlap=True, mask=None,
+                extra=0, comm_factory=None):
+    """Run `steps` (+ `extra` beyond the stop) on P logical ranks; returns
+    (global field, history, info of rank 0)."""
     from paper_2111_09859_b200 import dist
+    group = dist.LocalGroup(P)
+    slabs = dist.split_global(phi0, P)
+
+    def work(r):
+        ds = dist.DistributedSolve(grid, faces, cfg, group.comms[r], solid_mask=mask,
+                                   filter0=filter0, overlap=overlap)
+        try:
+            ds.bind(slabs[r])
+            for _ in range(steps + extra):
+                ds.steps(1)
+            out = ds.finish().cpu().numpy().copy()
+            return out, ds.history(), (ds.fused, ds.filter0, ds.graph, ds.status().iters)
+        finally:
+            ds.close()
+
+    res = group.run(work)
+    for c in group.comms:
+        c.close()
+    got = np.concatenate([r[0] for r in res], axis=0)
+    for r in res[1:]:
+        assert same(r[1], res[0][1])  # every rank holds the same history
+    return got, res[0][1], res[0][2]
+
+
+def _channel(n0=32, arith="exact", steps=6):
     dims = (n0, 48, 64)
-    sp = (1.0 / n0, 1.0 / 47, 1.0 / 64)
     g = W.build_cartesian(*dims, Lx=1.0, Ly=1.0, Lz=1.0, periodic=(True, False, True))
-    fc = W.FormulationConfig(kind="hj")
-    filt = W.FilterConfig(0.49)
-    steps = 6
-    cfg = W.SolveConfig(formulation=fc, scheme="E6", filter_config=filt, tol=1e-15,
-                        max_iters=steps, arith=arith)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E6",
+                        filter_config=W.FilterConfig(0.49), tol=1e-15, max_iters=steps,
+                        arith=arith)
     rng = np.random.default_rng(5)
     y = np.linspace(0.0, 1.0, dims[1])
     phi0 = np.broadcast_to(np.minimum(y, 1 - y)[None, :, None], dims).copy()
     phi0 += 1e-3 * rng.standard_normal(dims)
-    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
-    comm = dist.LocalComm(P)
-    ds = dist.DistributedSolve(dims, sp, FACES, "E6", fc, filt, 0.5, 1e-15, steps, arith, comm,
-                               list(range(P)), filter0=filter0, overlap=overlap)
-    assert ds.overlap == (overlap and n0 // P >= 22)
-    n = dims[0] // P
-    # the single-GPU path applies the BCs to phi0 first; mirror it
-    import torch
-    phi_bc = phi0.copy()
-    phi_bc[:, 0, :] = 0.0
-    phi_bc[:, -1, :] = 0.0
-    ds.set_state([phi_bc[r * n:(r + 1) * n] for r in range(P)])
-    for _ in range(steps):
-        ds.step()
-    got = np.concatenate([s.cpu().numpy() for s in ds.state()], axis=0)
-    hist = ds.history(0)
-    ds.close()
-    return got, hist, ref
+    return g, cfg, phi0
 
 
 @pytest.mark.parametrize("P,arith", [(1, "exact"), (2, "exact"), (4, "exact"), (2, "fast")])
-def test_decomposed_equals_single(P, arith):
-    got, hist, ref = _run(P, arith, "transpose")
+def test_fused_transposed_equals_single(P, arith):
+    g, cfg, phi0 = _channel(arith=arith)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    got, hist, info = _dist_solve(P, g, FACES, cfg, phi0, 6, filter0="transpose")
+    assert info[0] and info[1] == "transpose"
     assert same(hist, ref.residual_history)
     assert same(got, ref.phi)
 
 
-@pytest.mark.parametrize("P", [1, 2, 4])
-def test_partitioned_axis0_filter(P):
-    """Fast arithmetic with the axis-0 filter solved across the ranks
-    (two per-line carry all_gathers instead of two slab transposes)."""
-    got, hist, ref = _run(P, "fast", "partitioned")
+@pytest.mark.parametrize("P,n0", [(1, 32), (2, 32), (4, 32), (2, 128), (4, 64), (1, 256), (8, 64),
+                                  (2, 40), (2, 44)])
+def test_fused_partitioned_axis0_filter(P, n0):
+    """Fast arithmetic, axis-0 filter solved across the ranks (one local scan
+    kernel, one all_gather of 3 doubles per line, one fix-up): every segment
+    shape (4, 8, 16 rows x 16 / 32 segments, generic) is hit by the sizes."""
+    g, cfg, phi0 = _channel(n0=n0, arith="fast", steps=4)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    got, hist, info = _dist_solve(P, g, FACES, cfg, phi0, 4, filter0="partitioned")
+    assert info[0] and info[1] == "partitioned"
     scale = float(np.max(np.abs(ref.phi)))
     assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale
     assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
 
 
-def test_slab_checks():
-    from paper_2111_09859_b200 import dist
-    with pytest.raises(ValueError):
-        dist.Slab(30, 4, 0).check(48)
-    with pytest.raises(ValueError):
-        dist.Slab(32, 4, 0).check(30)
-
-
 @pytest.mark.parametrize("P,arith,filter0", [(2, "exact", "transpose"), (2, "fast", "transpose"),
-                                             (4, "fast", "partitioned")])
+                                             (4, "fast", "partitioned"), (2, "fast", "partitioned")])
 def test_overlapped_ghost_exchange(P, arith, filter0):
-    """Stage kernels split into ghost-free interior planes (launched while
-    the ghost planes are in flight) and the boundary planes: same results."""
-    got, hist, ref = _run(P, arith, filter0, n0=32 * P)
+    """Stage kernels split into the ghost-free interior planes (launched while
+    the ghost planes are in flight on the communication stream) and the
+    boundary planes: same results."""
+    g, cfg, phi0 = _channel(n0=32 * P, arith=arith, steps=4)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    from paper_2111_09859_b200 import dist
+    got, hist, info = _dist_solve(P, g, FACES, cfg, phi0, 4, filter0=filter0, overlap=True)
+    got2, hist2, _ = _dist_solve(P, g, FACES, cfg, phi0, 4, filter0=filter0, overlap=False)
+    assert same(got, got2) and same(hist, hist2)
     if filter0 == "transpose":
         assert same(hist, ref.residual_history)
         assert same(got, ref.phi)
     else:
         scale = float(np.max(np.abs(ref.phi)))
         assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale
+
+
+def test_solo_rank_stays_finite():
+    """The benchmarking communicator (one rank of P alone, graph-captured,
+    overlapped): a slab of the channel wrapped onto itself is the channel of
+    that length, so the rank's state must match the single-GPU solve on the
+    (nl, n1, n2) periodic box."""
+    from paper_2111_09859_b200 import dist
+    P = 2
+    g, cfg, phi0 = _channel(n0=64, arith="fast", steps=6)
+    gl = W.build_cartesian(32, 48, 64, Lx=0.5, Ly=1.0, Lz=1.0, periodic=(True, False, True))
+    ref = W.solve_steady(gl, W.BoundarySpec(FACES), cfg, phi0=phi0[:32])
+    comm = dist.SoloComm(P, 0)
+    ds = dist.DistributedSolve(g, FACES, cfg, comm)
+    try:
+        assert ds.overlap and ds.graph
+        ds.bind(phi0[:32])
+        ds.steps(2)
+        ds.steps(4)
+        assert ds.status().iters == 6
+        got = ds.finish().cpu().numpy()
+        assert np.max(np.abs(got - ref.phi)) <= 1e-12 * float(np.max(np.abs(ref.phi)))
+    finally:
+        ds.close()
+        comm.close()
+
+
+def test_steps_past_the_stop_keep_the_state():
+    """stepping a stopped solve must not move the reported state
+    (buffer parity follows the completed-step count, not the enqueued one)."""
+    g, cfg, phi0 = _channel(arith="fast", steps=5)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    for extra in (1, 2, 3):
+        got, hist, info = _dist_solve(2, g, FACES, cfg, phi0, 5, filter0="transpose", extra=extra)
+        assert info[3] == 5 and len(hist) == 5
+        assert same(got, ref.phi)
+
+
+def _cylinder(kind, arith, steps, dims=(32, 16, 12), scheme="C6", alpha=0.48):
+    g = W.build_cylinder(*dims, scheme=scheme)
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme=scheme,
+                        filter_config=W.FilterConfig(alpha) if alpha else None, tol=1e-15,
+                        max_iters=steps, arith=arith)
+    c = g.coords
+    phi0 = np.sqrt(c[0] ** 2 + c[1] ** 2) - 0.5
+    phi0 = phi0 + 1e-3 * np.random.default_rng(3).standard_normal(dims) * (phi0 > 0)
+    return g, cfg, phi0
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
+def test_generic_cylinder_c6_exact_equals_single(P, kind):
+    """BASELINE config 5's formulation: compact C6 on all axes, the theta
+    axis decomposed, its line solves on pencils between all_to_all
+    transposes -> bit-identical to one GPU (post-map included)."""
+    g, cfg, phi0 = _cylinder(kind, "exact", 4)
+    if kind == "poisson":
+        phi0 = np.zeros_like(phi0)
+    ref = W.solve_steady(g, W.BoundarySpec(CYL), cfg, phi0=phi0)
+    got, hist, info = _dist_solve(P, g, CYL, cfg, phi0, 4)
+    assert not info[0]
+    assert same(hist, ref.residual_history)
+    assert same(got, ref.phi_prime if kind == "poisson" else ref.phi)
+
+
+def test_generic_cylinder_c6_fast_equals_single():
+    g, cfg, phi0 = _cylinder("hj_curvature", "fast", 4)
+    ref = W.solve_steady(g, W.BoundarySpec(CYL), cfg, phi0=phi0)
+    got, hist, info = _dist_solve(2, g, CYL, cfg, phi0, 4)
+    scale = float(np.max(np.abs(ref.phi)))
+    assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale
+    assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("kind,scheme,alpha", [("hj", "UW", None), ("hj_lad", "E4", 0.49),
+                                               ("eikonal", "E2", 0.45), ("hj", "C4", 0.48)])
+def test_generic_channel_schemes_equal_single(kind, scheme, alpha):
+    """One-sided differences (UW), the LAD 4th derivative, explicit and
+    compact schemes along the decomposed axis, with a solid mask."""
+    dims = (20, 14, 12)
+    g = W.build_cartesian(*dims, Lx=1.0, Ly=1.0, Lz=1.0, periodic=(True, False, True))
+    mask = np.zeros(dims, dtype=bool)
+    mask[3:7, 5:8, 2:6] = True
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme=scheme,
+                        filter_config=W.FilterConfig(alpha) if alpha else None, tol=1e-15,
+                        max_iters=5, arith="exact")
+    y = np.linspace(0.0, 1.0, dims[1])
+    phi0 = np.broadcast_to(np.minimum(y, 1 - y)[None, :, None], dims).copy()
+    phi0 += 1e-3 * np.random.default_rng(11).standard_normal(dims)
+    import os
+    os.environ["WD_DISABLE_FUSED"] = "1"
+    try:
+        ref = W.solve_steady(g, W.BoundarySpec(FACES, solid_mask=mask), cfg, phi0=phi0)
+        got, hist, info = _dist_solve(2, g, FACES, cfg, phi0, 5, mask=mask)
+    finally:
+        del os.environ["WD_DISABLE_FUSED"]
+    assert not info[0]
+    assert same(hist, ref.residual_history)
+    assert same(got, ref.phi)
+
+
+def test_generic_annulus_2d_equals_single():
+    g = W.build_annulus(32, 16, scheme="C6")
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj_curvature"), scheme="C6",
+                        filter_config=W.FilterConfig(0.48), tol=1e-15, max_iters=6)
+    c = g.coords
+    phi0 = np.sqrt(c[0] ** 2 + c[1] ** 2) - 0.5
+    ref = W.solve_steady(g, W.BoundarySpec(RING), cfg, phi0=phi0)
+    got, hist, _ = _dist_solve(2, g, RING, cfg, phi0, 6)
+    assert same(hist, ref.residual_history)
+    assert same(got, ref.phi)
+
+
+def test_solve_steady_with_comm_converges_like_single():
+    """solve_steady(..., comm=) on 2 logical ranks: stops at the same
+    iteration (tolerance set between two entries of the single-GPU history)
+    with the same history and field (exact arithmetic, transposes)."""
+    from paper_2111_09859_b200 import dist
+    import dataclasses
+    g, cfg, phi0 = _channel(n0=16, arith="exact", steps=40)
+    probe = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    h = probe.residual_history
+    tol = float(0.5 * (h[24] + h[25]))
+    cfg = dataclasses.replace(cfg, tol=tol)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    assert ref.converged and 1 < ref.iters < 40
+    group = dist.LocalGroup(2)
+    reps = group.run(lambda r: W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0,
+                                              comm=group.comms[r]))
+    for rep in reps:
+        assert rep.converged and rep.iters == ref.iters
+        assert same(rep.residual_history, ref.residual_history)
+        assert same(rep.phi, ref.phi)
+
+
+def test_nccl_comm_single_rank_graph():
+    """The product communicator (NCCL inside the library; one rank here):
+    k steps replayed as one CUDA graph, partitioned filter, vs single GPU."""
+    from paper_2111_09859_b200 import dist
+    g, cfg, phi0 = _channel(n0=64, arith="fast", steps=8)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    comm = dist.NcclComm(0, 1)
+    ds = dist.DistributedSolve(g, FACES, cfg, comm)
+    try:
+        assert ds.fused and ds.graph and ds.filter0 == "partitioned"
+        ds.bind(phi0)
+        ds.steps(4)
+        ds.steps(4)
+        ds.steps(4)  # frozen at max_iters
+        assert ds.status().iters == 8
+        got = ds.finish().cpu().numpy()
+        scale = float(np.max(np.abs(ref.phi)))
+        assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale
+        rep = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0, comm=comm)
+        assert np.max(np.abs(rep.phi - ref.phi)) <= 1e-12 * scale
+    finally:
+        ds.close()
+        comm.close()
+
+
+def test_slab_checks():
+    from paper_2111_09859_b200 import dist
+    with pytest.raises(ValueError):
+        dist.Slab(30, 4, 0).check()
+    g, cfg, phi0 = _channel()
+    bad = dict(FACES, imin="wall", imax="wall")
+    gw = W.build_cartesian(32, 48, 64, periodic=(False, False, True))
+    with pytest.raises(ValueError):
+        dist.DistributedSolve(gw, bad, cfg, dist.NcclComm(0, 1))
+
+
+# ------------------------------------------------- two processes, one GPU
+def _proc(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2111_09859_b200 import dist
+        out = {}
+        comm = dist.TorchComm()
+        # fused program, partitioned filter
+        g, cfg, phi0 = _channel(n0=32, arith="fast", steps=4)
+        rep = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0, comm=comm)
+        out["fused"] = (rep.phi, rep.residual_history)
+        # generic program (compact C6 cylinder), transposes
+        g2, cfg2, p2 = _cylinder("hj_curvature", "exact", 3)
+        rep2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2, comm=comm)
+        out["generic"] = (rep2.phi, rep2.residual_history)
+        q.put((rank, out))
+        comm.close()
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_processes_torchcomm_gloo():
+    """DistributedSolve with a real multi-process communicator: two
+    processes share GPU 0, torch.distributed/gloo moves the ghost planes,
+    carries and pencils through the host (no kernel waits on a kernel)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proc, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    g, cfg, phi0 = _channel(n0=32, arith="fast", steps=4)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    g2, cfg2, p2 = _cylinder("hj_curvature", "exact", 3)
+    ref2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2)
+    for r in (0, 1):
+        phi, hist = res[r]["fused"]
+        assert np.max(np.abs(phi - ref.phi)) <= 1e-12 * float(np.max(np.abs(ref.phi)))
+        assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
+        phi, hist = res[r]["generic"]
+        assert same(hist, ref2.residual_history)
+        assert same(phi, ref2.phi)
