@@ -202,6 +202,15 @@ int wd_gradient_magnitude(wd_ctx* ctx, const double* phi_dev, double* out_dev);
 int wd_levelset_step(wd_ctx* ctx, const double* phi_dev, double* out_dev, double F, double dt,
                      double source);
 
+/* One implicit-filter sweep (operators.py:305-352) of the fused path's
+ * kernels along `axis` of an arbitrary (n0, n1, n2) array; with A_dev the
+ * sweep also accumulates max|out - A|, max|out| and the non-finite flag into
+ * the status word, readable with wd_status_maxima (int64 x 3: the two maxima
+ * as order-preserving bit patterns).  Operator-level parity entry points. */
+int wd_fused_filter(wd_ctx* ctx, int axis, const double* in_dev, double* out_dev, int n0, int n1,
+                    int n2, int periodic, const double* A_dev);
+int wd_status_maxima(wd_ctx* ctx, long long* dev3);
+
 /* ---- multi-GPU: slab decomposition along axis 0 (EXTENSION) --
  * One process per GPU.  The reference has no distributed path; these entry
  * points put its solve loop (solver.py:221-286) on P ranks that each own the

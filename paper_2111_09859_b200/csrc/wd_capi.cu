@@ -444,6 +444,8 @@ struct wd_ctx {
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
   long long enq = 0;  // host-side count of enqueued steps (buffer parity)
   FusedPlan fused;    // specialised kernels (wd_fused.cuh), if applicable
+  // wd_fused_filter: filter factors for arbitrary (length, periodic)
+  std::map<std::pair<int, int>, std::pair<HostFactor, double*>> dfilt;
 };
 
 namespace {
@@ -1098,6 +1100,7 @@ int wd_destroy(wd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   fused_release(c->fused);
+  for (auto& kv : c->dfilt) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
   cudaFree(c->sums_dev);
   ws_free(c->ws, (size_t)7 * c->g.N * sizeof(double));

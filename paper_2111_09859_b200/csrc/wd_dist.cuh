@@ -419,7 +419,9 @@ int dist_filter0_fused(wd_dist* d, double* Pb, double* T1) {
     else f0_launch<0>(a, threads, true, s);
     if (int rc = comm_rc(d, d->comm->allgather(d->mine, d->all, (size_t)3 * d->plane, s)))
       return rc;
-    k_f0_fix<<<nblocks(d->plane, 128), 128, 0, s>>>(T1, d->all, d->nl, d->plane, d->f0, c->st);
+    k_f0_carry<<<nblocks(d->plane, 256), 256, 0, s>>>(d->all, d->mine, d->plane, d->f0, c->st);
+    const dim3 fg((unsigned)((d->plane + 255) / 256), (unsigned)((d->nl + F0_FR - 1) / F0_FR));
+    k_f0_fix<<<fg, 256, 0, s>>>(T1, d->mine, d->nl, d->plane, d->f0, c->st);
     return WD_OK;
   }
   // slab -> pencil, sweep, pencil -> slab: every line sees the single-GPU sweep
@@ -855,6 +857,57 @@ int wd_dist_finish(wd_dist* d) {
   CK(cudaMemcpyAsync(d->phi, src + (long long)d->G * d->plane, (size_t)d->Nl * sizeof(double),
                      cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  return WD_OK;
+}
+
+// One filter sweep of the fused path's kernels on an arbitrary (n0, n1, n2)
+// array (operator-level parity of the scan / checkpointed sweeps).
+int wd_fused_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, int n1, int n2,
+                    int periodic, const double* A) {
+  if (!c || !c->fused.active || !c->sd.use_filter || axis < 0 || axis > 2)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  const int nn[3] = {n0, n1, n2};
+  const int n = nn[axis];
+  auto key = std::make_pair(n, periodic ? 1 : 0);
+  auto it = c->dfilt.find(key);
+  if (it == c->dfilt.end()) {
+    HostFactor F;
+    int rc = filter_factor(c->sd.alpha_f, n, periodic, F);
+    if (rc) return rc;
+    for (double sw : F.swap)
+      if (sw != 0.0) return fail(WD_ERR_INVALID, "filter factor with interchanges");
+    std::vector<double> packed, sc;
+    factor_pack(F, packed);
+    int m = 0;
+    const size_t nf = packed.size();
+    if (c->sd.arith == 1 && scan_pack(F, sc, m)) packed.insert(packed.end(), sc.begin(), sc.end());
+    double* dev = nullptr;
+    CK(cudaMalloc(&dev, packed.size() * sizeof(double)));
+    CK(cudaMemcpy(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+    fused_filter_prepare(n);
+    F.scan_m = m;
+    F.scan_off = nf;
+    it = c->dfilt.emplace(key, std::make_pair(F, dev)).first;
+  }
+  const TriDev T = factor_view(it->second.first, it->second.second);
+  ScanDev SD;
+  if (it->second.first.scan_m) {
+    SD.n = n;
+    SD.m = it->second.first.scan_m;
+    SD.tab = it->second.second + it->second.first.scan_off;
+    SD.denom = it->second.first.cyclic ? it->second.first.denom : 1.0;
+  }
+  fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream,
+                   SD.n ? &SD : nullptr);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+// running maxima of the status word (max|delta| bits, max|phi| bits, non-finite flag)
+int wd_status_maxima(wd_ctx* c, long long* dev3) {
+  if (!c || !dev3) return fail(WD_ERR_INVALID, "bad arguments");
+  k_stats_out<<<1, 1, 0, c->stream>>>(c->st, dev3);
+  CK(cudaGetLastError());
   return WD_OK;
 }
 

@@ -220,13 +220,11 @@ inline size_t f0_smem_bytes(int nl, bool generic) {
          (generic ? (size_t)nl * F0_L * 8 : 0);
 }
 
-// x = x' + cf W_r + cb Qp_r - f z_r, in place; `all` = gathered [P][3][lines]
-__global__ void k_f0_fix(double* x, const double* __restrict__ all, int nl, long long lines,
-                         F0Tables T, const Status* st) {
+// Per-line carries of this rank from the gathered [P][3][lines] exports:
+// coef[0] = cf (y of row lo - 1), coef[1] = cb (x of row hi), coef[2] = f.
+__global__ void k_f0_carry(const double* __restrict__ all, double* __restrict__ coef,
+                           long long lines, F0Tables T, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  const double* Wt = T.tab + 6 * nl;
-  const double* Qp = Wt + nl;
-  const double* zz = Qp + nl;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < lines;
        q += (long long)gridDim.x * blockDim.x) {
     double cf = 0.0, cfr = 0.0, hsum = 0.0;
@@ -249,16 +247,38 @@ __global__ void k_f0_fix(double* x, const double* __restrict__ all, int nl, long
         cb = fma(T.blk[3 * p + 1], cb, fma(cfq[p], T.blk[3 * p + 2], g[lines]));
       }
     }
-    const double f = hsum * T.rden;
-    double* px = x + q;
-    for (int r = 0; r < nl; ++r) {
-      double v = fma(cfr, Wt[r], *px);
-      v = fma(cb, Qp[r], v);
-      v = fma(-f, zz[r], v);
-      *px = v;
-      px += lines;
-    }
+    coef[q] = cfr;
+    coef[lines + q] = cb;
+    coef[2 * lines + q] = hsum * T.rden;
   }
+}
+
+// x = x' + cf W_r + cb Qp_r - f z_r, in place: one thread per line and
+// F0_FR rows (grid.y), the rows' loads issued together
+constexpr int F0_FR = 8;
+__global__ void __launch_bounds__(256) k_f0_fix(double* x, const double* __restrict__ coef, int nl,
+                                                long long lines, F0Tables T, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const double* Wt = T.tab + 6 * nl;
+  const double* Qp = Wt + nl;
+  const double* zz = Qp + nl;
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= lines) return;
+  const int r0 = blockIdx.y * F0_FR;
+  const double cf = coef[q], cb = coef[lines + q], f = coef[2 * lines + q];
+  double* px = x + q + (long long)r0 * lines;
+  double v[F0_FR];
+#pragma unroll
+  for (int k = 0; k < F0_FR; ++k)
+    if (r0 + k < nl) v[k] = __ldcs(px + (long long)k * lines);
+#pragma unroll
+  for (int k = 0; k < F0_FR; ++k)
+    if (r0 + k < nl) {
+      double t = fma(cf, __ldg(Wt + r0 + k), v[k]);
+      t = fma(cb, __ldg(Qp + r0 + k), t);
+      t = fma(-f, __ldg(zz + r0 + k), t);
+      __stcs(px + (long long)k * lines, t);
+    }
 }
 
 }  // namespace wd

@@ -115,14 +115,22 @@ def test_c5_cylinder_128x64x32_c6_50_steps_exact(kind):
 @pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
 def test_c5_cylinder_64x32x16_c6_converged_fast(kind):
     """Fast arithmetic (scan derivatives / scan filter) to tol 1e-8: iteration
-    count within 1 of the oracle's, field within 1e-10 * max|phi|."""
+    count within 1 of the oracle's, field within 1e-10 * max|phi|.  The
+    oracle's Poisson run is still at a change of 1.1e-4 after its 40,000
+    steps (slow diffusive convergence): there both runs stop at max_iters
+    and the fields are compared after the same 40,000 steps."""
     z = goldens.load(f"base_c5_cyl64_{kind}_C6_conv")
-    assert bool(z["converged"]), "oracle run did not converge"
     g = W.build_cylinder(64, 32, 16, scheme="C6")
-    rep, div = _solve(g, CYL, z, arith="fast", max_iters=int(z["iters"]) + 50)
-    assert rep is not None, f"diverged at {div}"
-    assert rep.converged
-    assert abs(rep.iters - int(z["iters"])) <= 1, (rep.iters, int(z["iters"]))
+    if bool(z["converged"]):
+        rep, div = _solve(g, CYL, z, arith="fast", max_iters=int(z["iters"]) + 50)
+        assert rep is not None, f"diverged at {div}"
+        assert rep.converged
+        assert abs(rep.iters - int(z["iters"])) <= 1, (rep.iters, int(z["iters"]))
+    else:
+        rep, div = _solve(g, CYL, z, arith="fast")
+        assert rep is not None, f"diverged at {div}"
+        assert not rep.converged and rep.iters == int(z["iters"])
+        assert np.allclose(rep.residual_history[-100:], z["residual_history"][-100:], rtol=1e-6)
     ref = z["phi"]
     err = float(np.max(np.abs(rep.phi - ref)))
     assert err <= 1e-10 * float(np.max(np.abs(ref))), err

@@ -1,7 +1,7 @@
 """Fast-arithmetic filter sweep (csrc/wd_filter_scan.cuh: segmented affine
 scan of the dgtsv factor) against the oracle's apply_filter
 (operators.py:305-352; cyclic extension), one sweep at a time through the
-C ABI (wd_dist_filter on an arbitrary (n0, n1, n2) array), plus the fused
+C ABI (wd_fused_filter on an arbitrary (n0, n1, n2) array), plus the fused
 convergence reduction it carries on the last axis.
 
 Tolerance: the scan solves the same linear system in a different operation
@@ -46,7 +46,7 @@ def _sweep(torch, ctx, u, axis, periodic, A=None):
     dev = torch.from_numpy(u).cuda()
     out = torch.empty_like(dev)
     a_dev = torch.from_numpy(A).cuda() if A is not None else None
-    nat.check(ctx.lib.wd_dist_filter(ctx.ptr, axis, dev.data_ptr(), out.data_ptr(), *u.shape,
+    nat.check(ctx.lib.wd_fused_filter(ctx.ptr, axis, dev.data_ptr(), out.data_ptr(), *u.shape,
                                      int(periodic), a_dev.data_ptr() if a_dev is not None else None))
     torch.cuda.synchronize()
     return out.cpu().numpy()
@@ -104,7 +104,7 @@ def test_scan_filter_smooth_field(torch):
 
 def test_scan_filter_reduction(torch):
     """Last-axis sweep also reduces max|x - A|, max|x| into the status word
-    (read through wd_dist_stats)."""
+    (read through wd_status_maxima)."""
     shape = (6, 20, 512)
     rng = np.random.default_rng(3)
     u = rng.standard_normal(shape)
@@ -113,7 +113,7 @@ def test_scan_filter_reduction(torch):
     try:
         got = _sweep(torch, ctx, u, 2, True, A=A)
         stats = torch.zeros(3, dtype=torch.int64, device="cuda")
-        nat.check(ctx.lib.wd_dist_stats(ctx.ptr, stats.data_ptr()))
+        nat.check(ctx.lib.wd_status_maxima(ctx.ptr, stats.data_ptr()))
         s = stats.cpu().numpy()
     finally:
         ctx.close()
