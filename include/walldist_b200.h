@@ -202,6 +202,16 @@ int wd_gradient_magnitude(wd_ctx* ctx, const double* phi_dev, double* out_dev);
 int wd_levelset_step(wd_ctx* ctx, const double* phi_dev, double* out_dev, double F, double dt,
                      double source);
 
+/* levelset.py:214-318 extract_isolines, the per-cell part: marching-squares
+ * segments of a 2-D (n0, n1) field at `level`, coords (2, n0 n1).  Per cell
+ * c = i (n1 - 1) + j: count[c] in 0..2 segments; ids[4 c + 2 s + e] the cell
+ * edge of endpoint e of segment s (2 * node + 0: edge towards i + 1, + 1:
+ * towards j + 1); pts[8 c + 4 s + 2 e ..] its interpolated (x, y).  The host
+ * chains segments through shared edge ids.                                */
+int wd_iso_segments(const double* field_dev, const double* coords_dev, int n0, int n1,
+                    double level, int* count_dev, long long* ids_dev, double* pts_dev,
+                    void* stream);
+
 /* One implicit-filter sweep (operators.py:305-352) of the fused path's
  * kernels along `axis` of an arbitrary (n0, n1, n2) array; with A_dev the
  * sweep also accumulates max|out - A|, max|out| and the non-finite flag into

@@ -133,6 +133,7 @@ SIGNATURES = {
     "wd_fused_active": (_I, [_P]),
     "wd_time_kernel": (_I, [_P, _I, _I, _DP]),
     "wd_kernel_words": (_I, [_P, _I]),
+    "wd_iso_segments": (_I, [_P, _P, _I, _I, _D, _P, _P, _P, _P]),
     "wd_fused_filter": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _P]),
     "wd_status_maxima": (_I, [_P, _P]),
     "wd_comm_unique_id": (_I, [_P]),

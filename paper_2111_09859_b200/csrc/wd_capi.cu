@@ -410,6 +410,9 @@ struct wd_dist;
 
 struct wd_ctx {
   wd_dist* dist = nullptr;  // GENERIC slab-decomposed program (wd_dist.cuh): axis-0 hooks
+  bool nopool = true;       // parked for reuse only when fully built and unmodified
+  int device = 0;
+  std::string env_sig;      // A/B environment knobs the plan was built under
   wd_grid_desc gd;
   wd_solver_desc sd;
   Geom g;
@@ -494,6 +497,10 @@ void line_solve_prepare() {
                        (int)kLineSolveMaxSmem);
   cudaFuncSetAttribute(k_line_solve_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kLineSolveMaxSmem);
+  cudaFuncSetAttribute(k_line_few<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
+  cudaFuncSetAttribute(k_line_few<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
   done = true;
 }
 template <int JOB>
@@ -503,6 +510,20 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
                        const Status* st, cudaStream_t s) {
   const int n = g.n[axis];
   const long long L = g.N / n;
+  // few long lines (2-D grids): one chain thread per line out of shared
+  // memory, right-hand side and epilogue in the same launch
+  if (L <= 148LL * 2 * LF_MAXL && !getenv("WD_NO_LINE_FEW")) {
+    int fl = (int)((L + 147) / 148);
+    if (fl > LF_MAXL) fl = LF_MAXL;
+    if (fl < 1) fl = 1;
+    const size_t sm = line_few_smem(n, fl);
+    if (sm <= kLineSolveMaxSmem) {
+      const int blocks = (int)((L + fl - 1) / fl);
+      k_line_few<JOB><<<blocks, LF_T, sm, s>>>(in, out, g, axis, n, g.s[axis], per, off, scheme, T,
+                                               e, fc, pin, use_geom_pin, fl, st);
+      return;
+    }
+  }
   if (g.s[axis] >= 32 && !getenv("WD_NO_RHS_SEG")) {
     const long long segs = L * ((n + RS_ROWS - 1) / RS_ROWS);
     k_line_rhs_seg<JOB><<<nblocks(segs, kThreads), kThreads, 0, s>>>(
@@ -918,6 +939,52 @@ int validate(const wd_grid_desc* gd, const wd_solver_desc* sd) {
 
 }  // namespace
 
+// Parked contexts.  A solve_steady() call builds a context, runs, and
+// destroys it; for the same grid and scheme the next call would redo the
+// factorisation, ~10 small cudaMalloc / cudaFree (each a device-wide
+// synchronisation), the stream and event creation, the tile-list uploads and
+// the CUDA-graph instantiation -- 10-140 ms of jitter on a 0.15-0.4 s
+// one-shot solve.  Contexts whose descriptors hold no
+// caller-owned device pointers (uniform grid, no solid mask) are parked on
+// wd_destroy (at most kCtxPoolMax, oldest evicted) and handed back by
+// wd_create for an equal descriptor; tol / max_iters may differ (they only
+// invalidate the captured graphs).  WD_NO_CTX_POOL disables it.
+namespace {
+constexpr size_t kCtxPoolMax = 2;
+std::mutex g_pool_mu;
+std::vector<wd_ctx*> g_ctx_pool;
+
+std::string env_signature() {
+  static const char* knobs[] = {"WD_DISABLE_FUSED", "WD_NO_FAST3", "WD_FILTER_ORDER", "WD_NO_DSCAN",
+                                "WD_SCAN_GENERIC", "WD_NO_GEN_SCANF", "WD_NO_ZERO_SKIP",
+                                "WD_NO_ASM_EXTRA", "WD_NO_RHS_SEG", "WD_NO_TILED_FEW"};
+  std::string sig;
+  for (const char* k : knobs) {
+    const char* v = getenv(k);
+    sig += v ? v : "-";
+    sig += '|';
+  }
+  return sig;
+}
+bool ctx_poolable(const wd_grid_desc& gd) {
+  static const bool off = getenv("WD_NO_CTX_POOL") != nullptr;
+  return !off && gd.uniform && gd.metrics_dev == nullptr && gd.solid_mask_dev == nullptr;
+}
+bool same_desc(const wd_ctx* c, const wd_grid_desc& gd, const wd_solver_desc& sd, bool use_filter) {
+  const wd_grid_desc& a = c->gd;
+  if (a.ndim != gd.ndim || a.uniform != gd.uniform || a.ref_length != gd.ref_length) return false;
+  for (int k = 0; k < 3; ++k)
+    if (k < gd.ndim && (a.dims[k] != gd.dims[k] || a.inv_spacing[k] != gd.inv_spacing[k]))
+      return false;
+  for (int k = 0; k < 2 * gd.ndim; ++k)
+    if (a.face[k] != gd.face[k]) return false;
+  const wd_solver_desc& b = c->sd;
+  return b.scheme == sd.scheme && b.kind == sd.kind && b.epsilon == sd.epsilon &&
+         b.lad_c == sd.lad_c && b.eps0 == sd.eps0 && (b.use_filter != 0) == use_filter &&
+         (!use_filter || b.alpha_f == sd.alpha_f) && b.cfl == sd.cfl && b.arith == sd.arith;
+}
+}  // namespace
+
 extern "C" {
 
 int wd_version(void) { return 100; }
@@ -935,7 +1002,31 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   if (!gd || !sd || !out) return fail(WD_ERR_INVALID, "null argument");
   int rc = validate(gd, sd);
   if (rc) return rc;
+  if (ctx_poolable(*gd)) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    const int dev = ws_device();
+    const bool uf = sd->use_filter && sd->scheme != WD_UW;
+    for (size_t i = g_ctx_pool.size(); i-- > 0;) {
+      wd_ctx* p = g_ctx_pool[i];
+      if (p->device != dev || !same_desc(p, *gd, *sd, uf) || p->env_sig != env_signature())
+        continue;
+      g_ctx_pool.erase(g_ctx_pool.begin() + i);
+      if (p->sd.tol != sd->tol || p->sd.max_iters != sd->max_iters) {
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);  // tol is a graph argument
+        p->graphs.clear();
+        p->sd.tol = sd->tol;
+        p->sd.max_iters = sd->max_iters;
+      }
+      p->fused.i_lo = p->fused.i_hi = 0;
+      p->enq = 0;
+      p->nopool = false;
+      *out = p;
+      return WD_OK;
+    }
+  }
   wd_ctx* c = new wd_ctx();
+  c->device = ws_device();
+  c->env_sig = env_signature();
   c->gd = *gd;
   c->sd = *sd;
   c->sd.use_filter = sd->use_filter && sd->scheme != WD_UW;
@@ -1091,6 +1182,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
     wd_destroy(c);
     return fail(WD_ERR_CUDA, "context setup failed");
   }
+  c->nopool = false;
   *out = c;
   return WD_OK;
 }
@@ -1098,6 +1190,20 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
 int wd_destroy(wd_ctx* c) {
   if (!c) return WD_OK;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->stream && c->ws && c->st && !c->nopool && !c->dist && ctx_poolable(c->gd)) {
+    wd_ctx* evict = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      g_ctx_pool.push_back(c);
+      if (g_ctx_pool.size() > kCtxPoolMax) {
+        evict = g_ctx_pool.front();
+        g_ctx_pool.erase(g_ctx_pool.begin());
+      }
+    }
+    if (!evict) return WD_OK;
+    c = evict;
+    c->nopool = true;  // really destroy the evicted one
+  }
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   fused_release(c->fused);
   for (auto& kv : c->dfilt) cudaFree(kv.second.second);

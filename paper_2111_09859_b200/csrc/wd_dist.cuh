@@ -735,6 +735,7 @@ int wd_dist_create(wd_comm* cm, const wd_grid_desc* gd, const wd_solver_desc* sd
     return code;
   };
   if (d->fused && !c->fused.active) return bail(fail(WD_ERR_INVALID, "configuration is not on the fused 3-D path"));
+  if (!d->fused) c->nopool = true;  // fused plan released / axis-0 hooks: not reusable
   if (!d->fused && c->fused.active) fused_release(c->fused);
   if (cudaMalloc(&d->stats, 16 * sizeof(long long)) != cudaSuccess)
     return bail(fail(WD_ERR_CUDA, "allocation failed"));
@@ -899,6 +900,19 @@ int wd_fused_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, 
   }
   fused_filter_any(c->fused, axis, in, out, n0, n1, n2, periodic, T, A, c->st, c->stream,
                    SD.n ? &SD : nullptr);
+  CK(cudaGetLastError());
+  return WD_OK;
+}
+
+// Marching-squares segments of a 2-D field (levelset.py:214-318): per cell
+// (n0 - 1)(n1 - 1): count, 4 edge ids, 4 points (wd_metrics.cuh).
+int wd_iso_segments(const double* field, const double* coords, int n0, int n1, double level,
+                    int* count, long long* ids, double* pts, void* stream) {
+  if (!field || !coords || !count || !ids || !pts || n0 < 2 || n1 < 2)
+    return fail(WD_ERR_INVALID, "bad arguments");
+  const long long cells = (long long)(n0 - 1) * (n1 - 1);
+  k_iso_segments<<<nblocks(cells, kThreads), kThreads, 0, (cudaStream_t)stream>>>(
+      field, coords, coords + (long long)n0 * n1, n0, n1, level, count, ids, pts);
   CK(cudaGetLastError());
   return WD_OK;
 }

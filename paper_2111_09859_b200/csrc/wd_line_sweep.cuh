@@ -407,6 +407,168 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, LS_MINB)
   }
 }
 
+// ---------------------------------------------------------------------
+// FEW LONG LINES (2-D grids: BASELINE configs 1-3 have 101-1025 lines of
+// 101-1025 rows).  The dgtsv recurrences are one dependency chain per line,
+// and the warp-per-32-lines kernels above leave all but a handful of warps
+// of the GPU empty while every step of the chain waits on a global or
+// transposed-tile access (C3's axis-0 filter: 384 us for 513 lines).  Here a
+// CTA owns FL lines: all its threads evaluate the right-hand sides into
+// shared memory (field reads hit L2), then ONE thread per line -- lane 0 of
+// its own warp, so the chains of a CTA sit on different schedulers -- runs
+// the forward / backward recurrences out of shared memory with the factor
+// rows prefetched in batches (off the chain), then all threads apply the
+// cyclic correction, the epilogue / pinned-node restore and store.  Same
+// expressions in the same order as k_line_rhs + k_line_solve (bitwise
+// equal; tests/test_gpu_parity.py), one launch instead of two.
+constexpr int LF_T = 128;   // threads per CTA
+constexpr int LF_MAXL = 4;  // lines per CTA (one chain thread per warp)
+constexpr int LF_U = 8;     // chain steps per prefetched batch
+
+template <int JOB, class L>
+__device__ __forceinline__ double line_rhs_at(const L& w, int i, int n, int scheme, int per,
+                                              const FilterCoef& fc) {
+  if (JOB == 0) return compact_rhs_at(w, i, n, scheme, per);
+  const int h = per ? 5 : ((i == 0 || i == n - 1) ? 0 : min(min(i, n - 1 - i), 5));
+  if (h == 0) return w(i);
+  const double* c = fc.hc + h * 6;
+  double r = c[0] * w(i);
+  for (int k = 1; k <= h; ++k) r = r + c[k] * (w(i + k) + w(i - k));
+  return r;
+}
+
+template <int JOB>
+static __global__ void __launch_bounds__(LF_T)
+    k_line_few(const double* __restrict__ in, double* out, Geom g, int axis, int n, long long sa,
+               int per, double off, int scheme, TriDev T, Epi epi, FilterCoef fc,
+               const uint8_t* pin, int use_geom_pin, int fl, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  extern __shared__ double lf_s[];  // [fl][n] right-hand sides -> y -> x, then hs[fl]
+  const long long L = g.N / n;
+  const long long q0 = (long long)blockIdx.x * fl;
+  const int nl = (int)min((long long)fl, L - q0);
+  double* fcors = lf_s + (size_t)fl * n;
+  // ---- A. right-hand sides (all threads; consecutive threads -> consecutive
+  // rows when the axis is contiguous, consecutive lines otherwise)
+  const int total = nl * n;
+  for (int t = threadIdx.x; t < total; t += LF_T) {
+    const int ll = sa == 1 ? t / n : t % nl;
+    const int i = sa == 1 ? t - ll * n : t / nl;
+    const long long base = line_base(g, axis, q0 + ll);
+    Line w{in + base, sa, n, per, off};
+    lf_s[(size_t)ll * n + i] = line_rhs_at<JOB>(w, i, n, scheme, per, fc);
+  }
+  __syncthreads();
+  // ---- B. one chain per line: lane 0 of warp ll
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0 && wib < nl) {
+    double* x = lf_s + (size_t)wib * n;
+    if (n == 1) {
+      x[0] = x[0] / T.d[0];
+      fcors[wib] = 0.0;
+    } else {
+      double carry = x[0];
+      double hs = 0.0;
+      if (T.cyclic) hs = hs + T.h[0] * carry;
+      int i = 0;
+      for (; i + LF_U <= n - 1; i += LF_U) {
+        double b[LF_U], f[LF_U], sw[LF_U], hv[LF_U];
+#pragma unroll
+        for (int u = 0; u < LF_U; ++u) {
+          b[u] = x[i + u + 1];
+          f[u] = __ldg(T.fact + i + u);
+          sw[u] = __ldg(T.swap + i + u);
+          hv[u] = T.cyclic ? __ldg(T.h + i + u + 1) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < LF_U; ++u) {
+          double yv;
+          if (sw[u] != 0.0) {
+            yv = b[u];
+            carry = carry - f[u] * b[u];
+          } else {
+            yv = carry;
+            carry = b[u] - f[u] * carry;
+          }
+          if (T.cyclic) hs = hs + hv[u] * b[u];
+          x[i + u] = yv;
+        }
+      }
+      for (; i < n - 1; ++i) {
+        const double bv = x[i + 1], f = T.fact[i];
+        double yv;
+        if (T.swap[i] != 0.0) {
+          yv = bv;
+          carry = carry - f * bv;
+        } else {
+          yv = carry;
+          carry = bv - f * carry;
+        }
+        if (T.cyclic) hs = hs + T.h[i + 1] * bv;
+        x[i] = yv;
+      }
+      fcors[wib] = T.cyclic ? hs / T.denom : 0.0;
+      double x1 = ls_div(carry, T.d[n - 1], T.rinv[n - 1]);
+      x[n - 1] = x1;
+      double x2 = x1;
+      x1 = ls_div(x[n - 2] - T.du[n - 2] * x2, T.d[n - 2], T.rinv[n - 2]);
+      x[n - 2] = x1;
+      int r = n - 3;
+      for (; r - LF_U + 1 >= 0; r -= LF_U) {
+        double yv[LF_U], du[LF_U], du2[LF_U], dd[LF_U], ri[LF_U];
+#pragma unroll
+        for (int u = 0; u < LF_U; ++u) {
+          yv[u] = x[r - u];
+          du[u] = __ldg(T.du + r - u);
+          du2[u] = __ldg(T.du2 + r - u);
+          dd[u] = __ldg(T.d + r - u);
+          ri[u] = __ldg(T.rinv + r - u);
+        }
+#pragma unroll
+        for (int u = 0; u < LF_U; ++u) {
+          const double xv = ls_div((yv[u] - du[u] * x1) - du2[u] * x2, dd[u], ri[u]);
+          x2 = x1;
+          x1 = xv;
+          x[r - u] = xv;
+        }
+      }
+      for (; r >= 0; --r) {
+        const double xv = ls_div((x[r] - T.du[r] * x1) - T.du2[r] * x2, T.d[r], T.rinv[r]);
+        x2 = x1;
+        x1 = xv;
+        x[r] = xv;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- C. cyclic correction, epilogue / pinned-node restore, store
+  for (int t = threadIdx.x; t < total; t += LF_T) {
+    const int ll = sa == 1 ? t / n : t % nl;
+    const int i = sa == 1 ? t - ll * n : t / nl;
+    const long long base = line_base(g, axis, q0 + ll);
+    const long long idx = base + (long long)i * sa;
+    const double xs = lf_s[(size_t)ll * n + i];
+    const double xv = T.cyclic ? xs - fcors[ll] * T.z[i] : xs;
+    if (JOB == 0) {
+      out[idx] = epi.apply(xv, idx);
+    } else {
+      bool p;
+      if (use_geom_pin) {
+        int c[kMaxDim];
+        node_coords(g, idx, c);
+        p = is_pinned(g, idx, c);
+      } else {
+        p = pin != nullptr && pin[idx] != 0;
+      }
+      out[idx] = p ? in[idx] : xv;
+    }
+  }
+}
+
+__host__ __forceinline__ size_t line_few_smem(int n, int fl) {
+  return ((size_t)fl * n + LF_MAXL) * sizeof(double);
+}
+
 __host__ __forceinline__ size_t line_solve_smem(int n) {
   return (size_t)8 * n * sizeof(double) + (size_t)((n + LS_U - 1) / LS_U) * sizeof(int);
 }

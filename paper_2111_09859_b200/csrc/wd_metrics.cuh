@@ -126,3 +126,97 @@ __global__ void k_fill(double* __restrict__ out, double v, long long N) {
 }
 
 }  // namespace wd
+
+namespace wd {
+
+// Marching-squares segment extraction (reference levelset.py:214-318 keeps
+// this on the host; here every cell is one thread).  Cell (i, j) of an
+// (n0, n1) field: corner bits 1 = (i, j), 2 = (i+1, j), 4 = (i+1, j+1),
+// 8 = (i, j+1) set where f - level > 0 (exact zeros count as +1e-30, the
+// reference's tie rule); each crossed cell edge carries the linearly
+// interpolated point (1 - t) x_a + t x_b, t = h_a / (h_a - h_b); the two
+// saddle codes connect around the corner pair whose sign differs from the
+// sign of the corner sum.  Output per cell: count (0..2) and per segment two
+// edge identities (2 * node + 0 for the edge towards i+1, + 1 towards j+1,
+// node = i * n1 + j) with their (x, y) points -- chained on the host.
+struct IsoEdge {
+  long long id;
+  double x, y;
+};
+
+__device__ __forceinline__ IsoEdge iso_edge(const double* f, const double* cx, const double* cy,
+                                            double level, int n1, int i, int j, int towards_j) {
+  const long long a = (long long)i * n1 + j;
+  const long long b = towards_j ? a + 1 : a + n1;
+  double ha = f[a] - level, hb = f[b] - level;
+  if (ha == 0.0) ha = 1e-30;
+  if (hb == 0.0) hb = 1e-30;
+  const double t = ha / (ha - hb);
+  IsoEdge e;
+  e.id = 2 * a + towards_j;
+  e.x = (1.0 - t) * cx[a] + t * cx[b];
+  e.y = (1.0 - t) * cy[a] + t * cy[b];
+  return e;
+}
+
+static __global__ void k_iso_segments(const double* __restrict__ f, const double* __restrict__ cx,
+                                      const double* __restrict__ cy, int n0, int n1, double level,
+                                      int* __restrict__ count, long long* __restrict__ ids,
+                                      double* __restrict__ pts) {
+  const long long cells = (long long)(n0 - 1) * (n1 - 1);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < cells;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(c / (n1 - 1)), j = (int)(c % (n1 - 1));
+    double h[4];
+    const long long a = (long long)i * n1 + j;
+    h[0] = f[a] - level;
+    h[1] = f[a + n1] - level;
+    h[2] = f[a + n1 + 1] - level;
+    h[3] = f[a + 1] - level;
+    int code = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (h[q] == 0.0) h[q] = 1e-30;
+      if (h[q] > 0.0) code |= 1 << q;
+    }
+    // the four cell edges: 0 bottom (j), 1 right (i+1), 2 top (j+1), 3 left (i)
+    // crossed edge pairs per code, two bits per edge, up to two segments
+    int ns = 0, e[4] = {0, 0, 0, 0};
+    auto seg = [&](int p, int q) {
+      e[2 * ns] = p;
+      e[2 * ns + 1] = q;
+      ++ns;
+    };
+    const bool mid_up = ((h[0] + h[1]) + h[2]) + h[3] > 0.0;
+    switch (code) {
+      case 1: case 14: seg(3, 0); break;
+      case 2: case 13: seg(0, 1); break;
+      case 3: case 12: seg(3, 1); break;
+      case 4: case 11: seg(1, 2); break;
+      case 6: case 9: seg(0, 2); break;
+      case 7: case 8: seg(3, 2); break;
+      case 5:
+        if (mid_up) { seg(3, 2); seg(0, 1); } else { seg(3, 0); seg(1, 2); }
+        break;
+      case 10:
+        if (mid_up) { seg(3, 0); seg(1, 2); } else { seg(0, 1); seg(2, 3); }
+        break;
+      default: break;
+    }
+    count[c] = ns;
+    for (int s = 0; s < 2 * ns; ++s) {
+      IsoEdge g;
+      switch (e[s]) {
+        case 0: g = iso_edge(f, cx, cy, level, n1, i, j, 0); break;       // (i,j)-(i+1,j)
+        case 1: g = iso_edge(f, cx, cy, level, n1, i + 1, j, 1); break;   // (i+1,j)-(i+1,j+1)
+        case 2: g = iso_edge(f, cx, cy, level, n1, i, j + 1, 0); break;   // (i,j+1)-(i+1,j+1)
+        default: g = iso_edge(f, cx, cy, level, n1, i, j, 1); break;      // (i,j)-(i,j+1)
+      }
+      ids[4 * c + s] = g.id;
+      pts[8 * c + 2 * s] = g.x;
+      pts[8 * c + 2 * s + 1] = g.y;
+    }
+  }
+}
+
+}  // namespace wd

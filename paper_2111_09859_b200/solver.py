@@ -228,7 +228,9 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
         if phi0 is None:
             phi = torch.zeros(tuple(grid.dims), dtype=torch.float64, device="cuda")
         else:
-            phi = ctx.field(phi0).clone()
+            phi = ctx.field(phi0)
+            if isinstance(phi0, torch.Tensor) and phi.data_ptr() == phi0.data_ptr():
+                phi = phi.clone()  # the caller's device tensor is not to be overwritten
         hist = torch.zeros(max(config.max_iters, 1), dtype=torch.float64, device="cuda")
         nat.check(lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
         stream = ctx.stream()
