@@ -21,6 +21,7 @@
 #include "wd_metrics.cuh"
 #include "wd_dist_filter0.cuh"
 #include "wd_deriv_scan.cuh"
+#include "wd_stage_explicit.cuh"
 
 using namespace wd;
 
@@ -769,7 +770,8 @@ void enqueue_timestep(wd_ctx* c, const double* p, double* dt, const Status* st) 
 
 // filter all axes + BC: x (BC'd RK4 output, clobbered) -> out
 // (solver.py:208-212)
-void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
+void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st,
+                       const double* change_vs = nullptr) {
   const Geom& g = c->g;
   double* cur = x;
   double* bufs[2] = {c->tmp2, x};
@@ -804,7 +806,11 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st) {
     }
     cur = nxt;
   }
-  k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
+  if (change_vs)  // the step's convergence reduction rides on the BC pass
+    k_bc_change<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, change_vs, g,
+                                                                    const_cast<Status*>(st));
+  else
+    k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
 }
 
 void rk_stage(int nd, int nb, cudaStream_t s, int stage, const double* phi, const double* dt,
@@ -815,7 +821,7 @@ void rk_stage(int nd, int nb, cudaStream_t s, int stage, const double* phi, cons
 
 // one RK4 step A -> B given dt already in c->dt (solver.py:183-212)
 void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
-                 bool dt_fresh = false) {
+                 bool dt_fresh = false, bool fuse_change = false) {
   const Geom& g = c->g;
   const int nb = nblocks(g.N, kThreads);
   // stage 1 evaluates the tendency at A, where enqueue_timestep just left
@@ -829,7 +835,7 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
   enqueue_tendency(c, c->p, c->k, st);
   if (c->sd.use_filter) {
     rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, c->p, g, st);
-    enqueue_filter_bc(c, c->p, B, st);
+    enqueue_filter_bc(c, c->p, B, st, fuse_change ? A : nullptr);
   } else {
     rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, B, g, st);
   }
@@ -885,15 +891,79 @@ int ensure_generic(wd_ctx* c) {
   return WD_OK;
 }
 
+// 2-D explicit central schemes, Eikonal / HJ: two kernels per RK stage
+// (wd_stage_explicit.cuh), bit-identical to the multi-kernel sequence below
+bool explicit_stage_ok(const wd_ctx* c) {
+  const int sc = c->sd.scheme;
+  return c->g.nd == 2 && (sc == WD_E2 || sc == WD_E4 || sc == WD_E6) &&
+         (c->sd.kind == WD_EIKONAL || c->sd.kind == WD_HJ) && !c->dist &&
+         !getenv("WD_NO_STAGE_EXPLICIT");
+}
+
+void enqueue_step_explicit(wd_ctx* c, const double* A, double* B) {
+  ExArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.A = A;
+  a.dt = c->dt;
+  a.acc = c->acc;
+  a.g = c->g;
+  a.M = c->M;
+  for (int t = 0; t < c->g.nd * c->g.nd; ++t)
+    if (c->M.m == nullptr || c->mterm[t]) a.nzm |= 1u << t;
+  a.scheme = c->sd.scheme;
+  a.kind = c->sd.kind;
+  a.eps = c->sd.epsilon;
+  a.cfl = c->sd.cfl;
+  a.sumS = c->sums_dev;
+  a.sumS_c = c->sumS_c;
+  a.cflms = c->sums_dev ? c->sums_dev + c->g.N : nullptr;
+  a.cflms_c = c->cflms_c;
+  a.st = c->st;
+  a.U[0] = c->U[0];
+  a.U[1] = c->U[1];
+  a.adv = c->advf;
+  const int nb = nblocks(c->g.N, 256);
+  double* last = c->sd.use_filter ? c->k : B;
+  a.p = A;
+  a.out = c->p;
+  k_ex_grad<2, true><<<nb, 256, 0, c->stream>>>(a);
+  k_ex_update<2, 1><<<nb, 256, 0, c->stream>>>(a);
+  a.p = c->p;
+  a.out = c->k;
+  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
+  k_ex_update<2, 2><<<nb, 256, 0, c->stream>>>(a);
+  a.p = c->k;
+  a.out = c->p;
+  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
+  k_ex_update<2, 3><<<nb, 256, 0, c->stream>>>(a);
+  a.p = c->p;
+  a.out = last;
+  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
+  k_ex_update<2, 4><<<nb, 256, 0, c->stream>>>(a);
+  if (c->sd.use_filter)
+    enqueue_filter_bc(c, c->k, B, c->st, A);
+  else
+    k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
+                                                                     c->g.N);
+  k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
+}
+
 void enqueue_step(wd_ctx* c, const double* A, double* B) {
   if (c->fused.active) {
     fused_step(c->fused, A, B, c->st, c->hist, c->stream);
     return;
   }
+  if (explicit_stage_ok(c)) {
+    enqueue_step_explicit(c, A, B);
+    return;
+  }
   enqueue_timestep(c, A, c->dt, c->st);
-  enqueue_rk4(c, A, B, c->st, true);
-  k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
-                                                                   c->g.N);
+  // filtered steps end with a BC pass: the convergence reduction rides on it
+  const bool fuse = c->sd.use_filter && !getenv("WD_NO_BC_CHANGE");
+  enqueue_rk4(c, A, B, c->st, true, fuse);
+  if (!fuse)
+    k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
+                                                                     c->g.N);
   if (c->dist) dist_reduce_status(c);
   k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
 }

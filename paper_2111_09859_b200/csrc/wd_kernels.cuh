@@ -614,6 +614,51 @@ static __global__ void k_change(const double* __restrict__ nw, const double* __r
   }
 }
 
+// k_bc + k_change in one pass: out = BC(in), and the running maxima of
+// |out - old| (unmasked nodes), |out| and the non-finite flag.
+static __global__ void k_bc_change(const double* __restrict__ in, double* out,
+                                   const double* __restrict__ old, Geom g, Status* st) {
+  if (st->state != WD_STATE_RUNNING) return;
+  double md = 0.0, ma = 0.0;
+  int bad = 0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int c[kMaxDim];
+    node_coords(g, idx, c);
+    const double v = is_pinned(g, idx, c) ? 0.0 : in[bc_source(g, idx, c)];
+    out[idx] = v;
+    if (!isfinite(v)) bad = 1;
+    ma = fmax(ma, fabs(v));
+    if (g.mask == nullptr || g.mask[idx] == 0) md = fmax(md, fabs(v - old[idx]));
+  }
+  md = warp_max(md);
+  ma = warp_max(ma);
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ double smd[32], sma[32];
+  __shared__ int sbad[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    smd[wid] = md;
+    sma[wid] = ma;
+    sbad[wid] = bad;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw_ = blockDim.x >> 5;
+    md = lane < nw_ ? smd[lane] : 0.0;
+    ma = lane < nw_ ? sma[lane] : 0.0;
+    bad = lane < nw_ ? sbad[lane] : 0;
+    md = warp_max(md);
+    ma = warp_max(ma);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      atomicMax(&st->max_delta_bits, (unsigned long long)__double_as_longlong(md));
+      atomicMax(&st->max_abs_bits, (unsigned long long)__double_as_longlong(ma));
+      if (bad) atomicOr(&st->nonfinite, 1);
+    }
+  }
+}
+
 // Stop test + history (solver.py:253-272).
 static __global__ void k_finalize(Status* st, double* hist, double lref, double tol, double limit) {
   if (st->state == WD_STATE_RUNNING) {

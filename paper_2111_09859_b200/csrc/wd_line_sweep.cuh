@@ -443,11 +443,29 @@ static __global__ void __launch_bounds__(LF_T)
                int per, double off, int scheme, TriDev T, Epi epi, FilterCoef fc,
                const uint8_t* pin, int use_geom_pin, int fl, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
-  extern __shared__ double lf_s[];  // [fl][n] right-hand sides -> y -> x, then hs[fl]
+  extern __shared__ double lf_s[];  // [fl][n] right-hand sides -> y -> x, hs[LF_MAXL], factor rows
   const long long L = g.N / n;
   const long long q0 = (long long)blockIdx.x * fl;
   const int nl = (int)min((long long)fl, L - q0);
   double* fcors = lf_s + (size_t)fl * n;
+  // factor rows in shared memory: every operand of the chains is then an
+  // LDS issued a batch ahead (global / L1 latency per batch was the bound)
+  double* sfact = fcors + LF_MAXL;
+  double* sswap = sfact + n;
+  double* sdu = sswap + n;
+  double* sdu2 = sdu + n;
+  double* sd = sdu2 + n;
+  double* srinv = sd + n;
+  double* sh = srinv + n;
+  for (int t = threadIdx.x; t < n; t += LF_T) {
+    sfact[t] = t < n - 1 ? T.fact[t] : 0.0;
+    sswap[t] = t < n - 1 ? T.swap[t] : 0.0;
+    sdu[t] = t < n - 1 ? T.du[t] : 0.0;
+    sdu2[t] = t < n - 2 ? T.du2[t] : 0.0;
+    sd[t] = T.d[t];
+    srinv[t] = T.rinv[t];
+    sh[t] = T.cyclic ? T.h[t] : 0.0;
+  }
   // ---- A. right-hand sides (all threads; consecutive threads -> consecutive
   // rows when the axis is contiguous, consecutive lines otherwise)
   const int total = nl * n;
@@ -467,18 +485,37 @@ static __global__ void __launch_bounds__(LF_T)
       x[0] = x[0] / T.d[0];
       fcors[wib] = 0.0;
     } else {
+      const bool cyc = T.cyclic != 0;
       double carry = x[0];
       double hs = 0.0;
-      if (T.cyclic) hs = hs + T.h[0] * carry;
-      int i = 0;
-      for (; i + LF_U <= n - 1; i += LF_U) {
-        double b[LF_U], f[LF_U], sw[LF_U], hv[LF_U];
+      if (cyc) hs = hs + sh[0] * carry;
+      // forward elimination, software pipelined: batch k + 1 is loaded
+      // before the recurrence of batch k runs
+      const int nf = (n - 1) / LF_U;
+      auto fload = [&](int k, double (&b)[LF_U], double (&f)[LF_U], double (&sw)[LF_U],
+                       double (&hv)[LF_U]) {
 #pragma unroll
         for (int u = 0; u < LF_U; ++u) {
-          b[u] = x[i + u + 1];
-          f[u] = __ldg(T.fact + i + u);
-          sw[u] = __ldg(T.swap + i + u);
-          hv[u] = T.cyclic ? __ldg(T.h + i + u + 1) : 0.0;
+          const int i = k * LF_U + u;
+          b[u] = x[i + 1];
+          f[u] = sfact[i];
+          sw[u] = sswap[i];
+          hv[u] = cyc ? sh[i + 1] : 0.0;
+        }
+      };
+      auto fproc = [&](int k, const double (&b)[LF_U], const double (&f)[LF_U],
+                       const double (&sw)[LF_U], const double (&hv)[LF_U]) {
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < LF_U; ++u) any |= sw[u] != 0.0;
+        if (!any) {  // no row interchange in the batch: branch-free chain
+#pragma unroll
+          for (int u = 0; u < LF_U; ++u) {
+            x[k * LF_U + u] = carry;
+            carry = b[u] - f[u] * carry;
+            if (cyc) hs = hs + hv[u] * b[u];
+          }
+          return;
         }
 #pragma unroll
         for (int u = 0; u < LF_U; ++u) {
@@ -490,50 +527,79 @@ static __global__ void __launch_bounds__(LF_T)
             yv = carry;
             carry = b[u] - f[u] * carry;
           }
-          if (T.cyclic) hs = hs + hv[u] * b[u];
-          x[i + u] = yv;
+          if (cyc) hs = hs + hv[u] * b[u];
+          x[k * LF_U + u] = yv;
+        }
+      };
+      {
+        double bA[LF_U], fA[LF_U], sA[LF_U], hA[LF_U], bB[LF_U], fB[LF_U], sB[LF_U], hB[LF_U];
+        if (nf > 0) fload(0, bA, fA, sA, hA);
+        for (int k = 0; k < nf; k += 2) {
+          if (k + 1 < nf) fload(k + 1, bB, fB, sB, hB);
+          fproc(k, bA, fA, sA, hA);
+          if (k + 1 >= nf) break;
+          if (k + 2 < nf) fload(k + 2, bA, fA, sA, hA);
+          fproc(k + 1, bB, fB, sB, hB);
         }
       }
-      for (; i < n - 1; ++i) {
-        const double bv = x[i + 1], f = T.fact[i];
+      for (int i = nf * LF_U; i < n - 1; ++i) {
+        const double bv = x[i + 1], f = sfact[i];
         double yv;
-        if (T.swap[i] != 0.0) {
+        if (sswap[i] != 0.0) {
           yv = bv;
           carry = carry - f * bv;
         } else {
           yv = carry;
           carry = bv - f * carry;
         }
-        if (T.cyclic) hs = hs + T.h[i + 1] * bv;
+        if (cyc) hs = hs + sh[i + 1] * bv;
         x[i] = yv;
       }
-      fcors[wib] = T.cyclic ? hs / T.denom : 0.0;
-      double x1 = ls_div(carry, T.d[n - 1], T.rinv[n - 1]);
+      fcors[wib] = cyc ? hs / T.denom : 0.0;
+      double x1 = ls_div(carry, sd[n - 1], srinv[n - 1]);
       x[n - 1] = x1;
       double x2 = x1;
-      x1 = ls_div(x[n - 2] - T.du[n - 2] * x2, T.d[n - 2], T.rinv[n - 2]);
+      x1 = ls_div(x[n - 2] - sdu[n - 2] * x2, sd[n - 2], srinv[n - 2]);
       x[n - 2] = x1;
-      int r = n - 3;
-      for (; r - LF_U + 1 >= 0; r -= LF_U) {
-        double yv[LF_U], du[LF_U], du2[LF_U], dd[LF_U], ri[LF_U];
+      // back substitution: rows n-3 .. 0, batch k covers rows n-3-kU .. n-3-kU-U+1
+      const int nbk = (n - 2) / LF_U;
+      auto bload = [&](int k, double (&yv)[LF_U], double (&du)[LF_U], double (&du2)[LF_U],
+                       double (&dd)[LF_U], double (&ri)[LF_U]) {
 #pragma unroll
         for (int u = 0; u < LF_U; ++u) {
-          yv[u] = x[r - u];
-          du[u] = __ldg(T.du + r - u);
-          du2[u] = __ldg(T.du2 + r - u);
-          dd[u] = __ldg(T.d + r - u);
-          ri[u] = __ldg(T.rinv + r - u);
+          const int r = n - 3 - k * LF_U - u;
+          yv[u] = x[r];
+          du[u] = sdu[r];
+          du2[u] = sdu2[r];
+          dd[u] = sd[r];
+          ri[u] = srinv[r];
         }
+      };
+      auto bproc = [&](int k, const double (&yv)[LF_U], const double (&du)[LF_U],
+                       const double (&du2)[LF_U], const double (&dd)[LF_U],
+                       const double (&ri)[LF_U]) {
 #pragma unroll
         for (int u = 0; u < LF_U; ++u) {
           const double xv = ls_div((yv[u] - du[u] * x1) - du2[u] * x2, dd[u], ri[u]);
           x2 = x1;
           x1 = xv;
-          x[r - u] = xv;
+          x[n - 3 - k * LF_U - u] = xv;
+        }
+      };
+      {
+        double yA[LF_U], aA[LF_U], cA[LF_U], dA[LF_U], rA[LF_U];
+        double yB[LF_U], aB[LF_U], cB[LF_U], dB[LF_U], rB[LF_U];
+        if (nbk > 0) bload(0, yA, aA, cA, dA, rA);
+        for (int k = 0; k < nbk; k += 2) {
+          if (k + 1 < nbk) bload(k + 1, yB, aB, cB, dB, rB);
+          bproc(k, yA, aA, cA, dA, rA);
+          if (k + 1 >= nbk) break;
+          if (k + 2 < nbk) bload(k + 2, yA, aA, cA, dA, rA);
+          bproc(k + 1, yB, aB, cB, dB, rB);
         }
       }
-      for (; r >= 0; --r) {
-        const double xv = ls_div((x[r] - T.du[r] * x1) - T.du2[r] * x2, T.d[r], T.rinv[r]);
+      for (int r = n - 3 - nbk * LF_U; r >= 0; --r) {
+        const double xv = ls_div((x[r] - sdu[r] * x1) - sdu2[r] * x2, sd[r], srinv[r]);
         x2 = x1;
         x1 = xv;
         x[r] = xv;
@@ -566,7 +632,7 @@ static __global__ void __launch_bounds__(LF_T)
 }
 
 __host__ __forceinline__ size_t line_few_smem(int n, int fl) {
-  return ((size_t)fl * n + LF_MAXL) * sizeof(double);
+  return ((size_t)fl * n + LF_MAXL + (size_t)7 * n) * sizeof(double);
 }
 
 __host__ __forceinline__ size_t line_solve_smem(int n) {
