@@ -37,10 +37,62 @@
 // rest go back into the tile behind the window (rows no other thread reads).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the encoder is resolved at run time, no libcuda link)
+
 #include "wd_filter_sweep.cuh"
 #include "wd_fused.cuh"
 
 namespace wd {
+
+// Tensor maps of the sweep's input for the TMA tile loads (strided axes,
+// full-segment tiles): `main` moves n / 2 rows x 16 lines per copy, `ghost`
+// the 5 wrapped rows of a periodic line.
+struct ScanTma {
+  CUtensorMap main, ghost;
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WD_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra WD_MBAR_DONE;\n"
+      "bra WD_MBAR_WAIT;\n"
+      "WD_MBAR_DONE:\n"
+      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2-D / 3-D tile loads: box of the tensor map at (c0, c1[, c2]) -> dst,
+// completion (bytes) signalled on `bar`
+__device__ __forceinline__ void tma_load_2d(double* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
 
 struct ScanArgs {
   const double* in;
@@ -101,7 +153,13 @@ __device__ __forceinline__ double fs_rhsh(const double* w, int h, const double* 
 // MM > 0: every segment has exactly MM rows (n = 16 MM); MM = 0: any n <= 512.
 // RED: fused convergence reduction against a.A (separate instantiation, so
 // the plain sweeps carry no predicated reduction code).
-template <bool AX2, int MM, bool RED>
+// TMA (strided axes, full-segment tiles, inner length a multiple of 16): the
+// tile is loaded by one elected thread with cp.async.bulk.tensor (two copies
+// of n / 2 rows x 128 bytes + the wrapped ghost rows) completing on two
+// mbarriers, one per half of the rows, so the segments of the first half
+// start their right-hand sides while the second half is still in flight;
+// the other instantiations stage with per-thread cp.async.
+template <bool AX2, int MM, bool RED, bool TMA>
 #ifndef WD_SCAN_TG
 #define WD_SCAN_TG 0  // 1: factor tables read from global memory (L1) instead of shared
 #endif
@@ -113,9 +171,12 @@ template <bool AX2, int MM, bool RED>
 #ifndef WD_SCAN_MINB
 #define WD_SCAN_MINB 2
 #endif
-__global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) {
+__global__ void __launch_bounds__(FS_T, WD_SCAN_MINB)
+    k_filter_scan(ScanArgs a, const __grid_constant__ ScanTma tm) {
   if (a.st->state != WD_STATE_RUNNING) return;
-  extern __shared__ double fs_smem[];
+  extern __shared__ __align__(128) double fs_smem[];
+  constexpr bool kTma = TMA && !AX2 && MM > 0;
+  __shared__ __align__(8) unsigned long long tbar[2];
   const int n = a.T.n, m = a.T.m, per = a.per;
   // tables: T1 (fm, h), T2 (P, g), T4 (Q, z) as double2; T3 rinv
   const double* tb = WD_SCAN_TG ? a.T.tab : fs_smem;
@@ -125,7 +186,7 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
   const double* T3 = tb + 6 * n;
   constexpr int tabn = WD_SCAN_TG ? 0 : 1;  // tables in shared memory?
   double* shc = fs_smem + tabn * 7 * n;  // FilterCoef (dynamic h: generic path)
-  double* tile = fs_smem + ((tabn * 7 * n + 36 + 3) & ~3);  // 32-byte aligned (16-byte cp.async)
+  double* tile = fs_smem + ((tabn * 7 * n + 36 + 15) & ~15);  // 128-byte aligned (TMA / cp.async)
   const int NR = n + 2 * FS_G;
   const int LS = NR | 1;  // AX2 line stride (odd)
   const int tsz = AX2 ? FS_L * LS : NR * FS_L;
@@ -157,9 +218,13 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
   const double rden = 1.0 / a.T.denom;
   const bool vec16 = !AX2 && (rstride % 2 == 0);  // 16-byte rows (base parity per tile)
 
+  long long t_outer = 0;  // tile coordinates of the last tile_of (TMA)
+  int t_inner0 = 0;
   auto tile_of = [&](long long q, long long& base, int& nl) {
     const long long outer = q / nb;
     const int inner0 = (int)(q - outer * nb) * FS_L;
+    t_outer = outer;
+    t_inner0 = inner0;
     nl = min(FS_L, inner_n - inner0);
     if (a.axis == 0) base = outer * a.n2 + inner0;
     else if (a.axis == 1) base = outer * a.s0 + inner0;
@@ -221,6 +286,40 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
+  // TMA: thread 0 arms the two mbarriers with the bytes of their half and
+  // issues the copies; tile rows [0, 5) / [n + 5, n + 10) are the ghosts
+  auto load_tma = [&]() {
+    if (tid != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // tile last written by threads
+    const unsigned half = (unsigned)(n / 2) * FS_L * 8u, gh = per ? FS_G * FS_L * 8u : 0u;
+    mbar_expect_tx(&tbar[0], half + gh);
+    mbar_expect_tx(&tbar[1], half + gh);
+    if (a.axis == 0) {
+      const int c0 = (int)(t_outer * a.n2 + t_inner0);
+      if (per) tma_load_2d(tile, &tm.ghost, c0, n - FS_G, &tbar[0]);
+      tma_load_2d(tile + FS_G * FS_L, &tm.main, c0, 0, &tbar[0]);
+      tma_load_2d(tile + (FS_G + n / 2) * FS_L, &tm.main, c0, n / 2, &tbar[1]);
+      if (per) tma_load_2d(tile + (FS_G + n) * FS_L, &tm.ghost, c0, 0, &tbar[1]);
+    } else {
+      const int c2 = (int)t_outer;
+      if (per) tma_load_3d(tile, &tm.ghost, t_inner0, n - FS_G, c2, &tbar[0]);
+      tma_load_3d(tile + FS_G * FS_L, &tm.main, t_inner0, 0, c2, &tbar[0]);
+      tma_load_3d(tile + (FS_G + n / 2) * FS_L, &tm.main, t_inner0, n / 2, c2, &tbar[1]);
+      if (per) tma_load_3d(tile + (FS_G + n) * FS_L, &tm.ghost, t_inner0, 0, c2, &tbar[1]);
+    }
+  };
+  if (kTma) {
+    if (tid == 0) {
+      mbar_init(&tbar[0], 1);
+      mbar_init(&tbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (!per)  // wall lines: zero ghosts, written once (no copy ever lands there)
+      for (int t = tid; t < 2 * FS_G * FS_L; t += FS_T)
+        tile[(t < FS_G * FS_L ? 0 : n * FS_L) + t] = 0.0;
+    __syncthreads();
+  }
+  unsigned tphase = 0;
   double md = 0.0, ma = 0.0;
   int bad = 0;
   long long q = blockIdx.x;
@@ -228,13 +327,22 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
   int nl = 0;
   if (q < groups) {
     tile_of(q, base, nl);
-    load(base, nl);
+    if (kTma) load_tma();
+    else load(base, nl);
   }
   const int RS = AX2 ? 1 : FS_L;
   double* tl = tile + (AX2 ? l * LS : l) + (r0 + FS_G) * RS;  // row r0 of my line
   for (; q < groups; q += gridDim.x) {
-    cp_async_wait_all();
-    __syncthreads();
+    if (kTma) {
+      // a segment's window spans tile rows [r0, r0 + m + 10): wait for the
+      // half (or halves) it touches only
+      if (r0 < n / 2 + FS_G) mbar_wait(&tbar[0], tphase);
+      if (r0 + m + 2 * FS_G > n / 2 + FS_G) mbar_wait(&tbar[1], tphase);
+      tphase ^= 1u;
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+    }
 #if WD_SCAN_PF
     // full-segment tiles: pull the convergence operand of this tile and the
     // input rows of the next one into L2 while this tile is solved, so the
@@ -394,9 +502,13 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
         base = nbase;
         nl = nnl;
       } else if (q + gridDim.x < groups) {
+        // the threads' writes into the tile (y', x') are ordered before the
+        // next copy of the async proxy
+        if (kTma) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();  // every thread done with the tile
         tile_of(q + gridDim.x, base, nl);
-        load(base, nl);
+        if (kTma) load_tma();
+        else load(base, nl);
       }
     } else {
       if constexpr (MM > 0) {
@@ -481,7 +593,7 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB) k_filter_scan(ScanArgs a) 
 inline size_t scan_smem(int n) {
   const int NR = n + 2 * FS_G;
   const size_t tile = (size_t)FS_L * (size_t)(NR | 1);  // >= NR * FS_L
-  return ((((size_t)(WD_SCAN_TG ? 0 : 7) * n + 36 + 3) & ~(size_t)3) + tile + 3 * FS_T) *
+  return ((((size_t)(WD_SCAN_TG ? 0 : 7) * n + 36 + 15) & ~(size_t)15) + tile + 3 * FS_T) *
          sizeof(double);
 }
 

@@ -81,23 +81,90 @@ void launch_sweep(const SweepArgs& w, cudaStream_t s) {
     k_filter_sweep<false><<<(int)ctas, 128, sweep_smem(w.n), s>>>(w);
 }
 
+// Tensor maps for the TMA tile loads of a strided sweep (wd_filter_scan.cuh).
+// cuTensorMapEncodeTiled is resolved through the runtime (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
+            cudaSuccess && qr == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+bool scan_tma_maps(const ScanArgs& a, ScanTma& tm) {
+  // opt-in: measured slower than the per-thread cp.async staging on this
+  // tile shape (128-byte rows, 522 row requests per tile through the SM's one
+  // TMA unit): i / j sweeps 0.547 / 0.518 ms vs 0.499 / 0.460 ms at 512^3
+  // (profiles/r02k_tma_ab.json); kept for wider-row tilings
+  static const bool off = getenv("WD_TMA") == nullptr;
+  EncodeTiledFn enc = encode_tiled();
+  const int n = a.T.n;
+  if (off || !enc || a.axis == 2 || (a.n2 % FS_L) != 0 || n / 2 > 256 || (n & 1) ||
+      ((uintptr_t)a.in & 15))
+    return false;
+  const cuuint32_t es[3] = {1, 1, 1};
+  void* base = const_cast<double*>(a.in);
+  auto make = [&](CUtensorMap* m, int rows) {
+    if (a.axis == 0) {  // (n0 rows) x (n1 n2 contiguous)
+      const cuuint64_t dims[2] = {(cuuint64_t)a.n1 * a.n2, (cuuint64_t)a.n0};
+      const cuuint64_t strides[1] = {(cuuint64_t)a.s0 * 8};
+      const cuuint32_t box[2] = {(cuuint32_t)FS_L, (cuuint32_t)rows};
+      return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)a.n2, (cuuint64_t)a.n1, (cuuint64_t)a.n0};
+    const cuuint64_t strides[2] = {(cuuint64_t)a.n2 * 8, (cuuint64_t)a.s0 * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)FS_L, (cuuint32_t)rows, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  return make(&tm.main, n / 2) == CUDA_SUCCESS && make(&tm.ghost, FS_G) == CUDA_SUCCESS;
+}
+
 // fast arithmetic: segmented-scan filter (wd_filter_scan.cuh), persistent
 // grid of resident CTAs
-template <bool AX2, int MM, bool RED>
-void scan_one(const ScanArgs& a, long long groups, cudaStream_t s) {
+template <bool AX2, int MM, bool RED, bool TMA>
+void scan_launch(const ScanArgs& a, const ScanTma& tm, long long groups, cudaStream_t s) {
   static int ctas = 0;
   const size_t smax = scan_smem(FS_NMAX);
   if (!ctas) {
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_filter_scan<AX2, MM, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smax);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<AX2, MM, RED>, FS_T, smax);
+    cudaFuncSetAttribute(k_filter_scan<AX2, MM, RED, TMA>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_scan<AX2, MM, RED, TMA>, FS_T,
+                                                  smax);
     ctas = sms * (occ > 0 ? occ : 1);
   }
   const long long c = ctas < groups ? ctas : groups;
-  k_filter_scan<AX2, MM, RED><<<(int)c, FS_T, scan_smem(a.T.n), s>>>(a);
+  k_filter_scan<AX2, MM, RED, TMA><<<(int)c, FS_T, scan_smem(a.T.n), s>>>(a, tm);
+}
+
+template <bool AX2, int MM, bool RED>
+void scan_one(const ScanArgs& a, long long groups, cudaStream_t s) {
+  ScanTma tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if constexpr (!AX2 && MM > 0) {
+    if (scan_tma_maps(a, tm)) {
+      scan_launch<AX2, MM, RED, true>(a, tm, groups, s);
+      return;
+    }
+  }
+  scan_launch<AX2, MM, RED, false>(a, tm, groups, s);
 }
 
 template <bool AX2, bool RED>
