@@ -26,6 +26,8 @@
 // (collectives included) with the in-device freeze-on-stop.
 #pragma once
 
+#include <unistd.h>
+
 #include "wd_comm.cuh"
 
 struct wd_dist {
@@ -50,6 +52,13 @@ struct wd_dist {
   ScanDev scan0, cscan0;
   double* fac0_dev = nullptr;
   long long* stats = nullptr;
+  // peer-memory ghost push (p2p = 1): neighbours' images of c->ws and of the
+  // barrier flags, opened through CUDA IPC (same-process ranks: the pointers)
+  int p2p = 0;
+  double *peer_ws_l = nullptr, *peer_ws_r = nullptr;
+  unsigned long long* xflags = nullptr;  // [0] written by the left rank, [1] by the right, [2] epoch
+  unsigned long long *xflag_l = nullptr, *xflag_r = nullptr;  // my slots in the neighbours
+  void* ipc_open[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t cs = nullptr;  // communication stream (ghost planes)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* phi = nullptr;      // caller's (nl, n1, n2) state
@@ -136,6 +145,41 @@ __global__ void k_stats_in(Status* st, const long long* in) {
   st->max_delta_bits = (unsigned long long)in[0];
   st->max_abs_bits = (unsigned long long)in[1];
   st->nonfinite = (int)in[2];
+}
+
+// Neighbour barrier of the peer-memory path: every rank runs the same
+// sequence of these, so a per-rank epoch counter names the barrier.  Thread 0
+// publishes the epoch into both neighbours' flag slots (release, system
+// scope: the stage kernel's ghost-plane stores precede it in stream order)
+// and spins until both of its own slots have reached the epoch (acquire).
+__global__ void k_xbar(unsigned long long* mine, unsigned long long* at_left,
+                       unsigned long long* at_right) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long e = mine[2] + 1;
+  mine[2] = e;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(at_left + 1), "l"(e) : "memory");
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(at_right), "l"(e) : "memory");
+  for (int side = 0; side < 2; ++side) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine + side) : "memory");
+    } while (v < e);
+  }
+}
+
+// All neighbours' ghost pushes of the kernels enqueued so far have landed
+// (and theirs into mine): device flags with NCCL ranks, a host barrier with
+// the callback communicators (tests), nothing for a rank running alone.
+int dist_xbar(wd_dist* d) {
+  wd_ctx* c = d->c;
+  if (d->comm->kind == 2 || d->P == 1) return WD_OK;
+  if (d->comm->kind == 1) {
+    DCK(d, cudaStreamSynchronize(c->stream));
+    return comm_rc(d, d->comm->allreduce_max(d->stats + 8, 1, c->stream));
+  }
+  k_xbar<<<1, 32, 0, c->stream>>>(d->xflags, d->xflag_l, d->xflag_r);
+  return WD_OK;
 }
 
 // ---- transposes -------------------------------------------------------
@@ -398,8 +442,12 @@ void f0_launch(const F0Args& a, int threads, bool generic, cudaStream_t s) {
 int dist_filter0_fused(wd_dist* d, double* Pb, double* T1) {
   wd_ctx* c = d->c;
   cudaStream_t s = c->stream;
+  if (d->p2p) {
+    if (int rc = dist_xbar(d)) return rc;  // stage 4 pushed Pb's ghost planes
+  }
   if (d->filter0 == 0) {
-    if (int rc = comm_rc(d, d->comm->halo(Pb, d->plane, d->nl, d->G, s))) return rc;
+    if (!d->p2p)
+      if (int rc = comm_rc(d, d->comm->halo(Pb, d->plane, d->nl, d->G, s))) return rc;
     F0Args a;
     a.in = Pb;
     a.out = T1;
@@ -446,6 +494,13 @@ int dist_step_fused(wd_dist* d, double* X, double* Y) {
   double* ins[4] = {X, Pa, Pb, Pa};
   double* outs[4] = {Pa, Pb, Pa, Pb};
   for (int st = 0; st < 4; ++st) {
+    if (d->p2p && st > 0) {
+      // the previous stage pushed its boundary planes into the neighbours'
+      // ghost planes as it wrote them: no exchange, one neighbour barrier
+      if (int rc = dist_xbar(d)) return rc;
+      dist_stage_range(d, st + 1, X, ins[st], outs[st], G, G + nl);
+      continue;
+    }
     if (d->overlap) {
       // planes [2G, nl): every stencil reach (<= G planes) stays inside the
       // rank's own planes, so they run while the ghost planes are in flight
@@ -487,6 +542,78 @@ int dist_enqueue(wd_dist* d, int k, int parity) {
       if (d->rc) return d->rc;
     }
   }
+  return WD_OK;
+}
+
+// Peer-memory setup: every rank publishes (pid, raw pointers, IPC handles) of
+// its workspace and flag allocations; each opens its two neighbours'.
+int dist_p2p_setup(wd_dist* d) {
+  wd_ctx* c = d->c;
+  wd_comm* cm = d->comm;
+  if (cudaMalloc(&d->xflags, 64) != cudaSuccess) return fail(WD_ERR_CUDA, "flag allocation failed");
+  CK(cudaMemset(d->xflags, 0, 64));
+  if (cm->kind == 2 || d->P == 1) {  // alone: the slab wraps onto itself
+    d->peer_ws_l = d->peer_ws_r = c->ws;
+    d->xflag_l = d->xflag_r = d->xflags;
+  } else {
+    constexpr int W = 20;  // doubles per rank: pid, ws ptr, flag ptr, 2 x 64-byte handles
+    struct Pub {
+      long long pid;
+      unsigned long long ws, fl;
+      cudaIpcMemHandle_t hws, hfl;
+    } me, *all;
+    static_assert(sizeof(Pub) <= W * sizeof(double), "Pub does not fit");
+    std::memset(&me, 0, sizeof(me));
+    me.pid = (long long)getpid();
+    me.ws = (unsigned long long)(uintptr_t)c->ws;
+    me.fl = (unsigned long long)(uintptr_t)d->xflags;
+    CK(cudaIpcGetMemHandle(&me.hws, c->ws));
+    CK(cudaIpcGetMemHandle(&me.hfl, d->xflags));
+    double *dm = nullptr, *da = nullptr;
+    CK(cudaMalloc(&dm, W * sizeof(double)));
+    CK(cudaMalloc(&da, (size_t)W * d->P * sizeof(double)));
+    std::vector<double> hostm(W, 0.0), hosta((size_t)W * d->P);
+    std::memcpy(hostm.data(), &me, sizeof(me));
+    CK(cudaMemcpy(dm, hostm.data(), W * sizeof(double), cudaMemcpyHostToDevice));
+    int rc = cm->allgather(dm, da, W, c->stream);
+    if (rc == WD_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = WD_ERR_CUDA;
+    if (rc == WD_OK)
+      CK(cudaMemcpy(hosta.data(), da, hosta.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(dm);
+    cudaFree(da);
+    if (rc) return fail(rc, "peer handle exchange failed: " + cm->err);
+    auto open = [&](int q, int slot, double** ws, unsigned long long** fl) -> int {
+      std::memcpy(&me, hosta.data() + (size_t)q * W, sizeof(me));  // reuse as scratch
+      all = &me;
+      if (all->pid == (long long)getpid()) {  // a logical rank of this process
+        *ws = (double*)(uintptr_t)all->ws;
+        *fl = (unsigned long long*)(uintptr_t)all->fl;
+        return WD_OK;
+      }
+      void *pw = nullptr, *pf = nullptr;
+      CK(cudaIpcOpenMemHandle(&pw, all->hws, cudaIpcMemLazyEnablePeerAccess));
+      CK(cudaIpcOpenMemHandle(&pf, all->hfl, cudaIpcMemLazyEnablePeerAccess));
+      d->ipc_open[2 * slot] = pw;
+      d->ipc_open[2 * slot + 1] = pf;
+      *ws = (double*)pw;
+      *fl = (unsigned long long*)pf;
+      return WD_OK;
+    };
+    if (int r2 = open(cm->left(), 0, &d->peer_ws_l, &d->xflag_l)) return r2;
+    if (cm->right() == cm->left()) {  // two ranks: one neighbour on both sides
+      d->peer_ws_r = d->peer_ws_l;
+      d->xflag_r = d->xflag_l;
+    } else if (int r3 = open(cm->right(), 1, &d->peer_ws_r, &d->xflag_r)) {
+      return r3;
+    }
+  }
+  c->fused.ws_base = c->ws;
+  c->fused.peer_ws_l = d->peer_ws_l;
+  c->fused.peer_ws_r = d->peer_ws_r;
+  c->fused.push_nl = d->nl;
+  c->fused.push_G = d->G;
+  c->nopool = true;  // the plan now points into other ranks' memory
+  d->p2p = 1;
   return WD_OK;
 }
 
@@ -643,6 +770,9 @@ int wd_dist_destroy(wd_dist* d) {
     d->c->dist = nullptr;
     wd_destroy(d->c);
   }
+  for (void* p : d->ipc_open)
+    if (p) cudaIpcCloseMemHandle(p);
+  cudaFree(d->xflags);
   ws_free(d->A, (size_t)d->Ng * sizeof(double));
   cudaFree(d->mine);
   cudaFree(d->all);
@@ -750,6 +880,8 @@ int wd_dist_create(wd_comm* cm, const wd_grid_desc* gd, const wd_solver_desc* sd
         return bail(fail(WD_ERR_CUDA, "carry buffer allocation failed"));
       if ((rc = dist_f0_tables(d))) return bail(rc);
     }
+    if (getenv("WD_DIST_P2P") && fused_can_push(c->fused))
+      if ((rc = dist_p2p_setup(d))) return bail(rc);
     if (cudaStreamCreateWithFlags(&d->cs, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming) != cudaSuccess)
@@ -936,7 +1068,7 @@ int wd_dist_info(wd_dist* d, int* out8) {
   out8[2] = d->fused;
   out8[3] = d->filter0;
   out8[4] = d->overlap;
-  out8[5] = d->comm->capturable() && !getenv("WD_DIST_NO_GRAPH");
+  out8[5] = (d->comm->capturable() && !getenv("WD_DIST_NO_GRAPH")) | (d->p2p << 1);
   out8[6] = d->P;
   out8[7] = d->rank;
   return WD_OK;

@@ -489,11 +489,23 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
   const bool eik = sd.kind == WD_EIKONAL;
   a.p = p;
   a.out = out;
+  if (fp.peer_ws_l && fp.peer_ws_r && fast3_ok(fp, a) && !fp.n_exact) {
+    const long long off = out - fp.ws_base;
+    a.peer_l = fp.peer_ws_l + off;
+    a.peer_r = fp.peer_ws_r + off;
+    a.push_shift = (long long)fp.push_nl * a.s0;
+    a.push_l_end = 2 * fp.push_G;
+    a.push_r_beg = fp.push_nl;
+  }
   if (fp.fast_tiles) {
     stage_tiles(fp, stage, a, chunks, R, eik, s);
   } else {
     stage_dispatch(R, eik, stage, a, chunks * all_tiles, nullptr, false, s);
   }
+}
+
+bool fused_can_push(const FusedPlan& fp) {
+  return fp.active && fp.use_fast3 && fp.fast_tiles != nullptr && fp.n_exact == 0;
 }
 
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,

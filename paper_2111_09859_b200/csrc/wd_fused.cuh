@@ -53,6 +53,12 @@ struct FusedPlan {
   int use_scan = 0;        // fast arithmetic: segmented-scan filter sweeps
   int use_fast3 = 0;       // fast arithmetic, E6: cp.async-pipelined stage kernel
   int filt_order[3] = {0, 1, 2};  // axis of each filter sweep (reference order 0, 1, 2)
+  // peer-memory ghost push of the fast E6 stage kernels (wd_dist.cuh): the
+  // neighbours' images of this rank's workspace; 0 = off
+  const double* ws_base = nullptr;
+  double* peer_ws_l = nullptr;
+  double* peer_ws_r = nullptr;
+  int push_nl = 0, push_G = 0;
 };
 
 // Decide whether a specialised path applies; fills fp (fp.active = 1).
@@ -71,6 +77,8 @@ void fused_launch(const FusedPlan& fp, int kid, const double* A, double* B, Stat
 // an arbitrary (n0, n1, n2) array with factor T (SweepArgs semantics).
 void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const double* p,
                       double* out, Status* st, cudaStream_t s);
+// the stage kernels of this plan can push ghost planes to peer memory
+bool fused_can_push(const FusedPlan& fp);
 void fused_filter_prepare(int n);  // opt in to the sweep's shared memory for length n
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
                       int n1, int n2, int per, const TriDev& T, const double* A, Status* st,

@@ -46,6 +46,14 @@ struct F3Args {
   int i_lo, i_hi;        // planes to update (ghosted slabs: interior only)
   int tiles_k, tiles_j;
   const Status* st;
+  // slab decomposition with peer memory (wd_dist.cuh): the planes
+  // [i_lo, push_l_end) of `out` also go to the left neighbour's high ghost
+  // planes (index + push_shift) and the planes [push_r_beg, i_hi) to the right
+  // neighbour's low ghost planes (index - push_shift), as stores over NVLink
+  double* peer_l = nullptr;
+  double* peer_r = nullptr;
+  long long push_shift = 0;
+  int push_l_end = 0, push_r_beg = 0;
   // fast mode: central coefficients c[r] (r = 1..3) and the composite
   // (D o D) 13-point coefficients e[m] (m = 0..6), squared metrics
   double cr[4];

@@ -413,6 +413,16 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         if (S3_LS ? STAGE == 2 : STAGE <= 3)
           __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
         __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
+        // slab decomposition: boundary planes also land in the neighbours'
+        // ghost planes (peer memory, NVLink stores; plane-uniform branch)
+        if (a.peer_l != nullptr) {
+          if (i < a.push_l_end)
+            __stcs(reinterpret_cast<double2*>(a.peer_l + (idx + a.push_shift)),
+                   make_double2(o[0], o[1]));
+          if (i >= a.push_r_beg)
+            __stcs(reinterpret_cast<double2*>(a.peer_r + (idx - a.push_shift)),
+                   make_double2(o[0], o[1]));
+        }
       }
     }
     sb = sb + 1 == S3_SLOTS ? 0 : sb + 1;

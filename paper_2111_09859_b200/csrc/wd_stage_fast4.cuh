@@ -247,6 +247,14 @@ __global__ void __launch_bounds__(128, WD_S4_MINB) k_f3_fast4(F3Args a, const in
           if (STAGE == 1) __stcs(reinterpret_cast<double2*>(a.dt + idx), make_double2(dtn[0], dtn[1]));
           if (STAGE == 2) __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
           __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
+          if (a.peer_l != nullptr) {  // ghost push to the neighbours (wd_stage_fast.cuh)
+            if (i < a.push_l_end)
+              __stcs(reinterpret_cast<double2*>(a.peer_l + (idx + a.push_shift)),
+                     make_double2(o[0], o[1]));
+            if (i >= a.push_r_beg)
+              __stcs(reinterpret_cast<double2*>(a.peer_r + (idx - a.push_shift)),
+                     make_double2(o[0], o[1]));
+          }
         }
       }
     }

@@ -451,7 +451,8 @@ class DistributedSolve:
         info = (ctypes.c_int * 8)()
         nat.check(lib.wd_dist_info(ptr, info))
         self.nl, self.G = info[0], info[1]
-        self.fused, self.overlap, self.graph = bool(info[2]), bool(info[4]), bool(info[5])
+        self.fused, self.overlap = bool(info[2]), bool(info[4])
+        self.graph, self.p2p = bool(info[5] & 1), bool(info[5] & 2)
         self.filter0 = ("partitioned", "transpose")[info[3]] if self.fused else "transpose"
         self.local_dims = (self.nl,) + tuple(grid.dims[1:])
         self.phi = torch.zeros(self.local_dims, dtype=torch.float64, device="cuda")

@@ -139,6 +139,45 @@ def test_solo_rank_stays_finite():
         comm.close()
 
 
+@pytest.mark.parametrize("P,filter0", [(2, "partitioned"), (4, "partitioned"), (2, "transpose")])
+def test_peer_memory_ghost_push(P, filter0, monkeypatch):
+    """WD_DIST_P2P: the fast stage kernels store their boundary planes straight
+    into the neighbours' ghost planes (peer pointers; here logical ranks of
+    one process) instead of four of the five ghost exchanges per step.  Same
+    arithmetic on the same operands as the exchanged-ghost program."""
+    monkeypatch.setenv("WD_DIST_P2P", "1")
+    g, cfg, phi0 = _channel(n0=32 * P, arith="fast", steps=5)
+    got, hist, info = _dist_solve(P, g, FACES, cfg, phi0, 5, filter0=filter0)
+    monkeypatch.delenv("WD_DIST_P2P")
+    base, hist0, _ = _dist_solve(P, g, FACES, cfg, phi0, 5, filter0=filter0)
+    assert same(got, base) and same(hist, hist0)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    assert np.max(np.abs(got - ref.phi)) <= 1e-12 * float(np.max(np.abs(ref.phi)))
+
+
+def test_peer_memory_push_solo_graph(monkeypatch):
+    """The pushed-ghost program captured in a CUDA graph (solo rank: the slab
+    is its own neighbour on both sides)."""
+    from paper_2111_09859_b200 import dist
+    monkeypatch.setenv("WD_DIST_P2P", "1")
+    g, cfg, phi0 = _channel(n0=64, arith="fast", steps=6)
+    gl = W.build_cartesian(32, 48, 64, Lx=0.5, Ly=1.0, Lz=1.0, periodic=(True, False, True))
+    ref = W.solve_steady(gl, W.BoundarySpec(FACES), cfg, phi0=phi0[:32])
+    comm = dist.SoloComm(2, 0)
+    ds = dist.DistributedSolve(g, FACES, cfg, comm)
+    try:
+        assert ds.p2p and ds.graph
+        ds.bind(phi0[:32])
+        ds.steps(3)
+        ds.steps(3)
+        assert ds.status().iters == 6
+        got = ds.finish().cpu().numpy()
+        assert np.max(np.abs(got - ref.phi)) <= 1e-12 * float(np.max(np.abs(ref.phi)))
+    finally:
+        ds.close()
+        comm.close()
+
+
 def test_steps_past_the_stop_keep_the_state():
     """stepping a stopped solve must not move the reported state
     (buffer parity follows the completed-step count, not the enqueued one)."""
@@ -300,6 +339,11 @@ def _proc(rank, world, port, q):
         g, cfg, phi0 = _channel(n0=32, arith="fast", steps=4)
         rep = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0, comm=comm)
         out["fused"] = (rep.phi, rep.residual_history)
+        # the same with the ghost planes pushed through CUDA IPC peer pointers
+        os.environ["WD_DIST_P2P"] = "1"
+        rep = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0, comm=comm)
+        del os.environ["WD_DIST_P2P"]
+        out["p2p"] = (rep.phi, rep.residual_history)
         # generic program (compact C6 cylinder), transposes
         g2, cfg2, p2 = _cylinder("hj_curvature", "exact", 3)
         rep2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2, comm=comm)
@@ -336,6 +380,8 @@ def test_two_processes_torchcomm_gloo():
         phi, hist = res[r]["fused"]
         assert np.max(np.abs(phi - ref.phi)) <= 1e-12 * float(np.max(np.abs(ref.phi)))
         assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
+        assert same(res[r]["p2p"][0], res[r]["fused"][0])
+        assert same(res[r]["p2p"][1], res[r]["fused"][1])
         phi, hist = res[r]["generic"]
         assert same(hist, ref2.residual_history)
         assert same(phi, ref2.phi)
