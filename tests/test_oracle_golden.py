@@ -77,3 +77,18 @@ def test_c1_prefix_golden():
     z = goldens.load("solve_c1_plate_hj_E4")
     rep = _run(z, iters=300)
     assert same(rep.residual_history, z["residual_history"][:300])
+
+
+def test_c2_converged_golden_matches_exact_distance_near_wall():
+    """BASELINE config 2 run to tol 1e-8 by the oracle (5,078 iterations):
+    the field is the wall distance d = r - 0.5 to 1e-4 within two wall units
+    (the far-field outer boundary bends the HJ solution further out)."""
+    import goldens
+    from oracle import wd
+    z = goldens.load("base_c2_annulus_curv_C6_full")
+    assert bool(z["converged"]) and int(z["iters"]) == 5078
+    g = wd.annulus(257, 129, scheme="C6")
+    d = np.sqrt(g.coords[0] ** 2 + g.coords[1] ** 2) - 0.5
+    near = (d > 0) & (d <= 2.0)
+    assert np.max(np.abs(z["phi"] - d)[near]) <= 1e-4
+    assert np.max(np.abs(z["phi"] - d)[(d > 0) & (d <= 1.0)]) <= 1e-5
