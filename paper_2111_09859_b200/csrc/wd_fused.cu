@@ -505,7 +505,8 @@ void fused_stage_ptrs(const FusedPlan& fp, int stage, const double* A, const dou
 }
 
 bool fused_can_push(const FusedPlan& fp) {
-  return fp.active && fp.use_fast3 && fp.fast_tiles != nullptr && fp.n_exact == 0;
+  return fp.active && fp.use_fast3 && fp.fast_tiles != nullptr && fp.n_exact == 0 &&
+         fp.in.sd->kind == WD_HJ;
 }
 
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,

@@ -72,37 +72,71 @@ bool fast3_prepare() {
          set((const void*)k_f3_fast3<3, EIK, 3, true>) && set((const void*)k_f3_fast3<3, EIK, 4, true>);
 }
 
-template <bool EIK>
-void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s,
-                  bool jb) {
+template <bool EIK, bool PUSH>
+void launch_fast3_impl(int stage, F3Args a, int ntiles, const int* tiles, int chunks,
+                       cudaStream_t s, bool jb) {
   const int ni = a.i_hi - a.i_lo;
   a.chunk = (ni + chunks - 1) / chunks;
   const int blocks = chunks * ntiles;
   const size_t sm = S3Layout<3>::SMEM;
   if (jb) {
     switch (stage) {
-      case 1: k_f3_fast3<3, EIK, 1, true><<<blocks, 256, sm, s>>>(a, tiles); break;
-      case 2: k_f3_fast3<3, EIK, 2, true><<<blocks, 256, sm, s>>>(a, tiles); break;
-      case 3: k_f3_fast3<3, EIK, 3, true><<<blocks, 256, sm, s>>>(a, tiles); break;
-      default: k_f3_fast3<3, EIK, 4, true><<<blocks, 256, sm, s>>>(a, tiles); break;
+      case 1: k_f3_fast3<3, EIK, 1, true, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+      case 2: k_f3_fast3<3, EIK, 2, true, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+      case 3: k_f3_fast3<3, EIK, 3, true, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+      default: k_f3_fast3<3, EIK, 4, true, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
     }
     return;
   }
   if ((WD_S4 >> (stage - 1)) & 1) {
     switch (stage) {
-      case 1: k_f3_fast4<3, EIK, 1><<<blocks, 128, sm, s>>>(a, tiles); break;
-      case 2: k_f3_fast4<3, EIK, 2><<<blocks, 128, sm, s>>>(a, tiles); break;
-      case 3: k_f3_fast4<3, EIK, 3><<<blocks, 128, sm, s>>>(a, tiles); break;
-      default: k_f3_fast4<3, EIK, 4><<<blocks, 128, sm, s>>>(a, tiles); break;
+      case 1: k_f3_fast4<3, EIK, 1, PUSH><<<blocks, 128, sm, s>>>(a, tiles); break;
+      case 2: k_f3_fast4<3, EIK, 2, PUSH><<<blocks, 128, sm, s>>>(a, tiles); break;
+      case 3: k_f3_fast4<3, EIK, 3, PUSH><<<blocks, 128, sm, s>>>(a, tiles); break;
+      default: k_f3_fast4<3, EIK, 4, PUSH><<<blocks, 128, sm, s>>>(a, tiles); break;
     }
     return;
   }
   switch (stage) {
-    case 1: k_f3_fast3<3, EIK, 1, false><<<blocks, 256, sm, s>>>(a, tiles); break;
-    case 2: k_f3_fast3<3, EIK, 2, false><<<blocks, 256, sm, s>>>(a, tiles); break;
-    case 3: k_f3_fast3<3, EIK, 3, false><<<blocks, 256, sm, s>>>(a, tiles); break;
-    default: k_f3_fast3<3, EIK, 4, false><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 1: k_f3_fast3<3, EIK, 1, false, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 2: k_f3_fast3<3, EIK, 2, false, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+    case 3: k_f3_fast3<3, EIK, 3, false, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
+    default: k_f3_fast3<3, EIK, 4, false, PUSH><<<blocks, 256, sm, s>>>(a, tiles); break;
   }
+}
+
+// the peer-memory (PUSH) instantiations exist for HJ only
+template <bool EIK>
+void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks, cudaStream_t s,
+                  bool jb) {
+  if constexpr (!EIK) {
+    if (a.peer_l != nullptr) {
+      static const bool prepared = [] {
+        const int sm = (int)S3Layout<3>::SMEM;
+        auto set = [&](const void* f) {
+          return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+                 cudaSuccess;
+        };
+        return set((const void*)k_f3_fast3<3, false, 1, false, true>) &&
+               set((const void*)k_f3_fast3<3, false, 2, false, true>) &&
+               set((const void*)k_f3_fast3<3, false, 3, false, true>) &&
+               set((const void*)k_f3_fast3<3, false, 4, false, true>) &&
+               set((const void*)k_f3_fast3<3, false, 1, true, true>) &&
+               set((const void*)k_f3_fast3<3, false, 2, true, true>) &&
+               set((const void*)k_f3_fast3<3, false, 3, true, true>) &&
+               set((const void*)k_f3_fast3<3, false, 4, true, true>) &&
+               set((const void*)k_f3_fast4<3, false, 1, true>) &&
+               set((const void*)k_f3_fast4<3, false, 2, true>) &&
+               set((const void*)k_f3_fast4<3, false, 3, true>) &&
+               set((const void*)k_f3_fast4<3, false, 4, true>);
+      }();
+      (void)prepared;
+      launch_fast3_impl<false, true>(stage, a, ntiles, tiles, chunks, s, jb);
+      return;
+    }
+  }
+  a.peer_l = a.peer_r = nullptr;
+  launch_fast3_impl<EIK, false>(stage, a, ntiles, tiles, chunks, s, jb);
 }
 
 // i-chunks for the fast3 grid: few partial waves over 2 CTAs / SM, long

@@ -115,7 +115,10 @@ __device__ __forceinline__ double2 s3_ldcg2(const double* p) {
 __constant__ double c_jbG[12][12];  // rows 0-5: low wall, 6-11: high wall (cols from base)
 __constant__ double c_jbM[12][12];
 
-template <int R, bool EIK, int STAGE, bool JB>
+// PUSH: slab decomposition with peer memory -- the boundary planes are also
+// stored into the neighbours' ghost planes (a separate instantiation, so the
+// single-GPU kernels carry neither the code nor the registers)
+template <int R, bool EIK, int STAGE, bool JB, bool PUSH = false>
 __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles) {
   using LY = S3Layout<R>;
   constexpr int H = LY::H;
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(256, 2) k_f3_fast3(F3Args a, const int* tiles)
         __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
         // slab decomposition: boundary planes also land in the neighbours'
         // ghost planes (peer memory, NVLink stores; plane-uniform branch)
-        if (a.peer_l != nullptr) {
+        if (PUSH) {
           if (i < a.push_l_end)
             __stcs(reinterpret_cast<double2*>(a.peer_l + (idx + a.push_shift)),
                    make_double2(o[0], o[1]));

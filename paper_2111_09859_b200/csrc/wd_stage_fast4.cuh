@@ -18,7 +18,7 @@ namespace wd {
 #ifndef WD_S4_MINB
 #define WD_S4_MINB 2
 #endif
-template <int R, bool EIK, int STAGE>
+template <int R, bool EIK, int STAGE, bool PUSH = false>
 __global__ void __launch_bounds__(128, WD_S4_MINB) k_f3_fast4(F3Args a, const int* tiles) {
   static_assert(S3_LS && !S3_REG, "k_f3_fast4 implements the low-storage, shared-memory variant");
   using LY = S3Layout<R>;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(128, WD_S4_MINB) k_f3_fast4(F3Args a, const in
           if (STAGE == 1) __stcs(reinterpret_cast<double2*>(a.dt + idx), make_double2(dtn[0], dtn[1]));
           if (STAGE == 2) __stcs(reinterpret_cast<double2*>(a.acc + idx), make_double2(ac[0], ac[1]));
           __stcs(reinterpret_cast<double2*>(a.out + idx), make_double2(o[0], o[1]));
-          if (a.peer_l != nullptr) {  // ghost push to the neighbours (wd_stage_fast.cuh)
+          if (PUSH) {  // ghost push to the neighbours (wd_stage_fast.cuh)
             if (i < a.push_l_end)
               __stcs(reinterpret_cast<double2*>(a.peer_l + (idx + a.push_shift)),
                      make_double2(o[0], o[1]));
