@@ -116,3 +116,62 @@ class NativeSolver:
 
     def empty(self):
         return self.torch.empty(tuple(self.grid.dims), dtype=self.torch.float64, device="cuda")
+
+
+# ---------------------------------------------------------------------------
+# Operator-level calls (tendency, local_timestep, rk4_step, gradient_magnitude,
+# poisson_postprocess ...) each need a context for (grid, scheme, formulation);
+# building and destroying one per call costs a workspace allocation, the host
+# factorisation and a device synchronisation.  A few
+# contexts are kept, keyed by the grid OBJECT (held alive by the entry, its
+# device metrics tensor checked for identity) and the configuration; grids
+# above _CACHE_MAX_NODES and calls with a solid mask build a private context.
+from collections import OrderedDict  # noqa: E402
+import dataclasses  # noqa: E402
+
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_SLOTS = 4
+_CACHE_MAX_NODES = 4_000_000
+
+
+def acquire(grid, faces=None, solid_mask=None, scheme="E2", formulation=None,
+            filter_config=None, cfl=0.5, tol=1e-5, max_iters=1, arith="exact", key_extra=None):
+    """(context, cached): a context for this configuration; release() it."""
+    n_nodes = int(np.prod(grid.dims))
+    if solid_mask is not None or n_nodes > _CACHE_MAX_NODES:
+        return NativeSolver(grid, faces, solid_mask, scheme, formulation, filter_config, cfl,
+                            tol, max_iters, arith=arith), False
+    fc = dataclasses.astuple(formulation) if formulation is not None else None
+    gkey = key_extra if key_extra is not None else id(grid)
+    key = (gkey, tuple(sorted((faces or {}).items())), scheme, fc,
+           None if filter_config is None else float(filter_config.alpha_f), float(cfl),
+           float(tol), int(max_iters), arith)
+    ent = _CACHE.get(key)
+    if ent is not None:
+        ctx, kept_grid, met = ent
+        same_grid = key_extra is not None or kept_grid is grid
+        same_met = grid.is_uniform or grid.device_metrics() is met
+        if same_grid and same_met and ctx.ptr is not None:
+            _CACHE.move_to_end(key)
+            return ctx, True
+        _CACHE.pop(key)
+        ctx.close()
+    ctx = NativeSolver(grid, faces, None, scheme, formulation, filter_config, cfl, tol,
+                       max_iters, arith=arith)
+    _CACHE[key] = (ctx, grid, None if grid.is_uniform else grid.device_metrics())
+    while len(_CACHE) > _CACHE_SLOTS:
+        _, (old, _g, _m) = _CACHE.popitem(last=False)
+        old.close()
+    return ctx, True
+
+
+def release(ctx, cached):
+    if not cached:
+        ctx.close()
+
+
+def drop_cached():
+    """Close every cached context (tests, interpreter shutdown)."""
+    while _CACHE:
+        _, (ctx, _g, _m) = _CACHE.popitem()
+        ctx.close()

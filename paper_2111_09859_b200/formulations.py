@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from ._context import NativeSolver
+from . import _context
 
 FORMULATIONS = ("eikonal", "hj", "hj_lad", "hj_curvature", "poisson")
 
@@ -44,14 +44,14 @@ def _as_out(values, t):
 
 def tendency(phi, grid, scheme: str, config: FormulationConfig):
     """Pseudo-time derivative d(phi)/dt* (formulations.py:244-252)."""
-    ctx = NativeSolver(grid, None, None, scheme, config)
+    ctx, cached = _context.acquire(grid, scheme=scheme, formulation=config)
     try:
         p = ctx.field(phi)
         k = ctx.empty()
         nat.check(ctx.lib.wd_tendency(ctx.ptr, p.data_ptr(), k.data_ptr()))
         return _as_out(phi, k)
     finally:
-        ctx.close()
+        _context.release(ctx, cached)
 
 
 def residual(phi, grid, scheme: str, config: FormulationConfig):
@@ -88,11 +88,12 @@ def gamma_standard(phi, epsilon: float):
 
 def poisson_postprocess(phi_prime, grid, scheme: str):
     """phi = -|grad phi'| + sqrt(|grad phi'|^2 + 2 phi') (formulations.py:255-270)."""
-    ctx = NativeSolver(grid, None, None, scheme, FormulationConfig(kind="poisson"))
+    ctx, cached = _context.acquire(grid, scheme=scheme,
+                                   formulation=FormulationConfig(kind="poisson"))
     try:
         p = ctx.field(phi_prime)
         out = ctx.empty()
         nat.check(ctx.lib.wd_poisson_post(ctx.ptr, p.data_ptr(), out.data_ptr()))
         return _as_out(phi_prime, out)
     finally:
-        ctx.close()
+        _context.release(ctx, cached)

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from ._context import NativeSolver
+from . import _context
 from .errors import TooFewIterationsError
 from .formulations import FormulationConfig
 
@@ -123,14 +123,15 @@ def gradient_magnitude(phi, grid, scheme: str):
     """|grad phi| (metrics.py:121-124): sqrt(sum_m U_m^2), U from the scheme's
     derivatives and the grid metrics, on the GPU."""
     torch = _torch()
-    ctx = NativeSolver(grid, None, None, scheme, FormulationConfig(kind="eikonal"))
+    ctx, cached = _context.acquire(grid, scheme=scheme,
+                                   formulation=FormulationConfig(kind="eikonal"))
     try:
         p = ctx.field(phi)
         out = ctx.empty()
         nat.check(ctx.lib.wd_gradient_magnitude(ctx.ptr, p.data_ptr(), out.data_ptr()))
         return out if isinstance(phi, torch.Tensor) else out.cpu().numpy()
     finally:
-        ctx.close()
+        _context.release(ctx, cached)
 
 
 def timing_probe(report) -> float:

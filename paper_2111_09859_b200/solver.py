@@ -19,6 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from . import _context
 from ._context import FACE_NAMES, NativeSolver
 from .errors import DivergenceError
 from .formulations import FormulationConfig
@@ -143,8 +144,9 @@ def apply_boundary_conditions(phi, boundary: BoundarySpec):
     is_t = isinstance(phi, torch.Tensor)
     dims = tuple(phi.shape)
     per = tuple(boundary.faces.get(_FACE_NAMES[2 * a]) == PERIODIC for a in range(len(dims)))
-    ctx = NativeSolver(_GridShim(dims, per), boundary.faces, boundary.solid_mask, "E2",
-                       FormulationConfig(kind="eikonal"))
+    ctx, cached = _context.acquire(_GridShim(dims, per), boundary.faces, boundary.solid_mask,
+                                   "E2", FormulationConfig(kind="eikonal"),
+                                   key_extra=("shim", dims, per))
     try:
         t = ctx.field(phi) if not is_t else phi
         if is_t and (t.dtype != torch.float64 or not t.is_contiguous() or not t.is_cuda):
@@ -154,12 +156,12 @@ def apply_boundary_conditions(phi, boundary: BoundarySpec):
             phi[...] = t.cpu().numpy()
         return phi
     finally:
-        ctx.close()
+        _context.release(ctx, cached)
 
 
 def local_timestep(phi, grid, config: FormulationConfig, cfl: float, scheme: str = "E2"):
     """Per-node pseudo time step (solver.py:160-180)."""
-    ctx = NativeSolver(grid, None, None, scheme, config, cfl=cfl)
+    ctx, cached = _context.acquire(grid, scheme=scheme, formulation=config, cfl=cfl)
     try:
         p = ctx.field(phi)
         dt = ctx.empty()
@@ -167,14 +169,15 @@ def local_timestep(phi, grid, config: FormulationConfig, cfl: float, scheme: str
         import torch
         return dt if isinstance(phi, torch.Tensor) else dt.cpu().numpy()
     finally:
-        ctx.close()
+        _context.release(ctx, cached)
 
 
 def rk4_step(phi, grid, config: SolveConfig, dt_field, boundary: BoundarySpec):
     """One classical RK4 step + filter + BCs + divergence check
     (solver.py:183-218)."""
-    ctx = NativeSolver(grid, boundary.faces, boundary.solid_mask, config.scheme,
-                       config.formulation, config.filter_config, config.cfl, config.tol)
+    ctx, cached = _context.acquire(grid, boundary.faces, boundary.solid_mask, config.scheme,
+                                   config.formulation, config.filter_config, config.cfl,
+                                   config.tol)
     try:
         p = ctx.field(phi)
         dt = ctx.field(dt_field)
@@ -188,7 +191,7 @@ def rk4_step(phi, grid, config: SolveConfig, dt_field, boundary: BoundarySpec):
         import torch
         return out if isinstance(phi, torch.Tensor) else out.cpu().numpy()
     finally:
-        ctx.close()
+        _context.release(ctx, cached)
 
 
 def _chunk_sizes(n_nodes: int):
