@@ -677,7 +677,7 @@ void launch_gamma_lad(wd_ctx* c, const double* p, const Status* st) {
 // the same pseudo-iteration computed them from the same field with the same
 // kernels, so recomputing would reproduce them bit for bit.
 void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
-                      bool fresh = false) {
+                      bool fresh = false, ResidualArgs* defer = nullptr) {
   const int kind = c->sd.kind, scheme = c->sd.scheme, nd = c->g.nd;
   const int csch = scheme == WD_UW ? WD_E2 : scheme;
   ResidualArgs a;
@@ -739,6 +739,10 @@ void enqueue_tendency(wd_ctx* c, const double* p, double* k, const Status* st,
       }
     }
   }
+  if (defer) {  // the caller fuses the residual into its own kernel (k_tend_rk)
+    *defer = a;
+    return;
+  }
   k_tendency<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(a, k, c->g.N, st);
 }
 
@@ -783,17 +787,21 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st,
       cur = nxt;
       continue;
     }
-    // arith="fast", 3-D, no solid mask: the segmented-scan sweep
+    // arith="fast", no solid mask, lines of 12..512 rows: the segmented-scan sweep
     // (wd_filter_scan.cuh).  It does not restore pinned nodes, which is
     // exact here: the input is BC'd (walls are 0), a wall of this axis is a
     // line end (identity row) and a wall of another axis holds whole lines
     // of zeros, which the linear sweep maps to zeros.
-    if (st && c->sd.arith == 1 && g.nd == 3 && g.mask == nullptr && c->scan[a].tab &&
+    if (st && c->sd.arith == 1 && g.mask == nullptr && c->scan[a].tab &&
         !getenv("WD_NO_GEN_SCANF")) {
       FusedPlan fp;
       fp.in.fcoef = c->fcoef;
-      fused_filter_any(fp, a, cur, nxt, g.n[0], g.n[1], g.n[2], g.per[a], c->filt[a], nullptr,
-                       const_cast<Status*>(st), c->stream, &c->scan[a]);
+      if (g.nd == 3)
+        fused_filter_any(fp, a, cur, nxt, g.n[0], g.n[1], g.n[2], g.per[a], c->filt[a], nullptr,
+                         const_cast<Status*>(st), c->stream, &c->scan[a]);
+      else  // 2-D (n0, n1) swept as the (1, n0, n1) array: axes 0, 1 -> 1, 2
+        fused_filter_any(fp, a + 1, cur, nxt, 1, g.n[0], g.n[1], g.per[a], c->filt[a], nullptr,
+                         const_cast<Status*>(st), c->stream, &c->scan[a]);
       cur = nxt;
       continue;
     }
@@ -825,19 +833,26 @@ void enqueue_rk4(wd_ctx* c, const double* A, double* B, const Status* st,
   const Geom& g = c->g;
   const int nb = nblocks(g.N, kThreads);
   // stage 1 evaluates the tendency at A, where enqueue_timestep just left
-  // dphi / U / Uh (/ gamma) -- except for Poisson, whose time step is static
-  enqueue_tendency(c, A, c->acc, st, dt_fresh && c->sd.kind != WD_POISSON);
-  rk_stage(c->g.nd, nb, c->stream, 1, A, c->dt, c->acc, c->acc, c->p, g, st);
-  enqueue_tendency(c, c->p, c->k, st);
-  rk_stage(c->g.nd, nb, c->stream, 2, A, c->dt, c->k, c->acc, c->p, g, st);
-  enqueue_tendency(c, c->p, c->k, st);
-  rk_stage(c->g.nd, nb, c->stream, 3, A, c->dt, c->k, c->acc, c->p, g, st);
-  enqueue_tendency(c, c->p, c->k, st);
+  // dphi / U / Uh (/ gamma) -- except for Poisson, whose time step is static.
+  // The residual itself is evaluated inside the stage update (k_tend_rk).
+  // Stage fields ping-pong p -> k -> p -> k: the update reads the stage input
+  // (eps phi in the residual) at its source node, so it cannot be in place.
+  auto stage = [&](int sidx, const double* pin, double* outp, bool fresh) {
+    ResidualArgs ra;
+    enqueue_tendency(c, pin, nullptr, st, fresh, &ra);
+    if (c->g.nd == 3)
+      k_tend_rk<3><<<nb, kThreads, 0, c->stream>>>(sidx, ra, A, c->dt, c->acc, outp, g, st);
+    else
+      k_tend_rk<2><<<nb, kThreads, 0, c->stream>>>(sidx, ra, A, c->dt, c->acc, outp, g, st);
+  };
+  stage(1, A, c->p, dt_fresh && c->sd.kind != WD_POISSON);
+  stage(2, c->p, c->k, false);
+  stage(3, c->k, c->p, false);
   if (c->sd.use_filter) {
-    rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, c->p, g, st);
-    enqueue_filter_bc(c, c->p, B, st, fuse_change ? A : nullptr);
+    stage(4, c->p, c->k, false);
+    enqueue_filter_bc(c, c->k, B, st, fuse_change ? A : nullptr);
   } else {
-    rk_stage(c->g.nd, nb, c->stream, 4, A, c->dt, c->k, c->acc, B, g, st);
+    stage(4, c->p, B, false);
   }
 }
 

@@ -394,58 +394,59 @@ struct ResidualArgs {
   Vec3 U, Uh, dphi, B, F;
 };
 
-// Tendency (formulations.py:153-252).  UW advection: flux_from_bf
-// (operators.py:216-219); central: Uhat . dphi.
+// Tendency (formulations.py:153-252) at one node.  UW advection:
+// flux_from_bf (operators.py:216-219); central: Uhat . dphi.
+__device__ __forceinline__ double residual_at(const ResidualArgs& a, long long idx) {
+  if (a.kind == WD_POISSON) {
+    const double r = -1.0 - a.lap[idx];
+    return -r;
+  }
+  double adv = 0.0;
+#pragma unroll
+  for (int l = 0; l < kMaxDim; ++l) {
+    if (l >= a.nd || a.adv) break;
+    const double uh = a.Uh.p[l][idx];
+    double t;
+    if (a.scheme == WD_UW) {
+      const double au = fabs(uh);
+      t = 0.5 * ((uh + au) * a.B.p[l][idx] + (uh - au) * a.F.p[l][idx]);
+    } else {
+      t = uh * a.dphi.p[l][idx];
+    }
+    adv = l == 0 ? t : adv + t;
+  }
+  if (a.adv) adv = a.adv[idx];
+  if (a.kind == WD_EIKONAL) return 1.0 - adv;
+  if (a.kind == WD_HJ || a.kind == WD_HJ_LAD) {
+    const double gam = a.kind == WD_HJ ? a.eps * a.p[idx] : a.gam[idx];
+    return 1.0 + gam * a.lap[idx] - adv;
+  }
+  // WD_HJ_CURVATURE
+  double gm;
+  if (a.gm) {
+    gm = a.gm[idx];
+  } else {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < kMaxDim; ++m) {
+      if (m >= a.nd) break;
+      const double u = a.U.p[m][idx];
+      s = m == 0 ? u * u : s + u * u;
+    }
+    gm = sqrt(s);
+  }
+  const double om = 1.0 - gm;
+  const double nu = 0.001 * (om * om);
+  const double gam = a.eps * a.p[idx] + nu;
+  const double corr = a.lap[idx] - np_max(0.0, gm * a.kappa[idx]);
+  return 1.0 + gam * corr - adv;
+}
+
 static __global__ void k_tendency(ResidualArgs a, double* k, long long N, const Status* st) {
   if (st && st->state != WD_STATE_RUNNING) return;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
-       idx += (long long)gridDim.x * blockDim.x) {
-    if (a.kind == WD_POISSON) {
-      const double r = -1.0 - a.lap[idx];
-      k[idx] = -r;
-      continue;
-    }
-    double adv = 0.0;
-#pragma unroll
-    for (int l = 0; l < kMaxDim; ++l) {
-      if (l >= a.nd || a.adv) break;
-      const double uh = a.Uh.p[l][idx];
-      double t;
-      if (a.scheme == WD_UW) {
-        const double au = fabs(uh);
-        t = 0.5 * ((uh + au) * a.B.p[l][idx] + (uh - au) * a.F.p[l][idx]);
-      } else {
-        t = uh * a.dphi.p[l][idx];
-      }
-      adv = l == 0 ? t : adv + t;
-    }
-    if (a.adv) adv = a.adv[idx];
-    if (a.kind == WD_EIKONAL) {
-      k[idx] = 1.0 - adv;
-    } else if (a.kind == WD_HJ || a.kind == WD_HJ_LAD) {
-      const double gam = a.kind == WD_HJ ? a.eps * a.p[idx] : a.gam[idx];
-      k[idx] = 1.0 + gam * a.lap[idx] - adv;
-    } else {  // WD_HJ_CURVATURE
-      double gm;
-      if (a.gm) {
-        gm = a.gm[idx];
-      } else {
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < kMaxDim; ++m) {
-          if (m >= a.nd) break;
-          const double u = a.U.p[m][idx];
-          s = m == 0 ? u * u : s + u * u;
-        }
-        gm = sqrt(s);
-      }
-      const double om = 1.0 - gm;
-      const double nu = 0.001 * (om * om);
-      const double gam = a.eps * a.p[idx] + nu;
-      const double corr = a.lap[idx] - np_max(0.0, gm * a.kappa[idx]);
-      k[idx] = 1.0 + gam * corr - adv;
-    }
-  }
+       idx += (long long)gridDim.x * blockDim.x)
+    k[idx] = residual_at(a, idx);
 }
 
 struct DtArgs {
@@ -553,6 +554,49 @@ static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
     // stages 2/3 read acc nowhere else, so the accumulation rides along
     // (k[idx] is k[s] or its neighbour: one DRAM pass over k)
     if (stage == 2 || stage == 3) acc[idx] = acc[idx] + 2.0 * k[idx];
+  }
+}
+
+// k_tendency + k_rk_stage in one pass (the solve loop's generic path): the
+// residual is pointwise in the assembled fields, so the stage update
+// evaluates it at its source node (and at the node itself for the running
+// sum acc) instead of reading a stored k.  Same expressions, bit-identical.
+template <int ND>
+static __global__ void k_tend_rk(int stage, ResidualArgs a, const double* __restrict__ phi,
+                                 const double* __restrict__ dt, double* acc, double* out, Geom g,
+                                 const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int c[kMaxDim];
+    node_coords_nd<ND>(g, idx, c);
+    long long s = idx;
+    bool pinned = false;
+#pragma unroll
+    for (int ax = 0; ax < ND; ++ax) {
+      if (c[ax] == 0) {
+        if (g.face[2 * ax] == WD_FACE_FARFIELD) s += g.s[ax];
+        if (g.face[2 * ax] == WD_FACE_WALL) pinned = true;
+      }
+      if (c[ax] == g.n[ax] - 1) {
+        if (g.face[2 * ax + 1] == WD_FACE_FARFIELD) s -= g.s[ax];
+        if (g.face[2 * ax + 1] == WD_FACE_WALL) pinned = true;
+      }
+    }
+    if (g.mask != nullptr && g.mask[idx] != 0) pinned = true;
+    const bool moved = s != idx;
+    const double k_me = (stage != 4 || !moved) ? residual_at(a, idx) : 0.0;
+    const double k_s = moved ? residual_at(a, s) : k_me;
+    double v;
+    if (stage == 4) {
+      v = phi[s] + (dt[s] / 6.0) * (acc[s] + k_s);
+    } else {
+      const double cdt = stage == 3 ? dt[s] : 0.5 * dt[s];
+      v = phi[s] + cdt * k_s;
+    }
+    out[idx] = pinned ? 0.0 : v;
+    if (stage == 1) acc[idx] = k_me;
+    if (stage == 2 || stage == 3) acc[idx] = acc[idx] + 2.0 * k_me;
   }
 }
 

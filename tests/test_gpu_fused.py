@@ -153,3 +153,20 @@ def test_c4_strip_fast_converged(ny):
     prof = z["profile"]
     err = np.max(np.abs(rep.phi - prof[None, :, None])) / np.max(prof)
     assert err <= 1e-10, err
+
+
+def test_c1_plate_fast_converges_like_the_reference():
+    """BASELINE config 1 in fast arithmetic (2-D: the exact stage kernels,
+    the scan filter sweeps): iteration count within 1 of the reference's
+    18,440 and the converged field within 1e-10 * max|phi| (north_star)."""
+    import goldens
+    z = goldens.load("solve_c1_plate_hj_E4")
+    g = W.build_cartesian(201, 101, Lx=2.0, Ly=1.0)
+    faces = {"imin": "farfield", "imax": "farfield", "jmin": "wall", "jmax": "farfield"}
+    cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E4",
+                        filter_config=W.FilterConfig(0.49), tol=1e-8, max_iters=30000,
+                        arith="fast")
+    rep = W.solve_steady(g, W.BoundarySpec(faces), cfg)
+    assert rep.converged and abs(rep.iters - int(z["iters"])) <= 1, rep.iters
+    ref = z["phi"]
+    assert np.max(np.abs(rep.phi - ref)) <= 1e-10 * float(np.max(np.abs(ref)))
