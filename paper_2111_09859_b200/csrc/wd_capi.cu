@@ -50,6 +50,28 @@ int nblocks(long long work, int threads) {
   return (int)std::min<long long>(b, 148LL * 32);
 }
 
+// Launch with programmatic stream serialization (PDL, wd_common.cuh) when
+// WD_PDL is set, else a plain launch.  Measured on the 2-D step (C1, 12 small
+// kernels per step, CUDA-graph replay): 0.144 -> 0.177 ms per step WITH the
+// programmatic edges (C3: 0.415 -> 0.428), i.e. slower than the plain
+// kernel-to-kernel edges of the graph, so it is opt-in.
+template <class... P, class... A>
+void launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  static const bool off = getenv("WD_PDL") == nullptr;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<P>(args)...);
+}
+
 int min_line(int scheme) {
   switch (scheme) {
     case WD_UW: return 3;
@@ -520,8 +542,8 @@ void launch_line_solve(const double* in, double* scratch, double* out, const Geo
     const size_t sm = line_few_smem(n, fl);
     if (sm <= kLineSolveMaxSmem) {
       const int blocks = (int)((L + fl - 1) / fl);
-      k_line_few<JOB><<<blocks, LF_T, sm, s>>>(in, out, g, axis, n, g.s[axis], per, off, scheme, T,
-                                               e, fc, pin, use_geom_pin, fl, st);
+      launch_pdl(k_line_few<JOB>, dim3(blocks), dim3(LF_T), sm, s, in, out, g, axis, n, g.s[axis],
+                 per, off, scheme, T, e, fc, pin, use_geom_pin, fl, st);
       return;
     }
   }
@@ -815,8 +837,8 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st,
     cur = nxt;
   }
   if (change_vs)  // the step's convergence reduction rides on the BC pass
-    k_bc_change<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, change_vs, g,
-                                                                    const_cast<Status*>(st));
+    launch_pdl(k_bc_change, dim3(nblocks(g.N, kThreads)), dim3(kThreads), 0, c->stream, cur, out,
+               change_vs, g, const_cast<Status*>(st));
   else
     k_bc<<<nblocks(g.N, kThreads), kThreads, 0, c->stream>>>(cur, out, g, st);
 }
@@ -941,26 +963,27 @@ void enqueue_step_explicit(wd_ctx* c, const double* A, double* B) {
   double* last = c->sd.use_filter ? c->k : B;
   a.p = A;
   a.out = c->p;
-  k_ex_grad<2, true><<<nb, 256, 0, c->stream>>>(a);
-  k_ex_update<2, 1><<<nb, 256, 0, c->stream>>>(a);
+  launch_pdl(k_ex_grad<2, true>, dim3(nb), dim3(256), 0, c->stream, a);
+  launch_pdl(k_ex_update<2, 1>, dim3(nb), dim3(256), 0, c->stream, a);
   a.p = c->p;
   a.out = c->k;
-  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
-  k_ex_update<2, 2><<<nb, 256, 0, c->stream>>>(a);
+  launch_pdl(k_ex_grad<2, false>, dim3(nb), dim3(256), 0, c->stream, a);
+  launch_pdl(k_ex_update<2, 2>, dim3(nb), dim3(256), 0, c->stream, a);
   a.p = c->k;
   a.out = c->p;
-  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
-  k_ex_update<2, 3><<<nb, 256, 0, c->stream>>>(a);
+  launch_pdl(k_ex_grad<2, false>, dim3(nb), dim3(256), 0, c->stream, a);
+  launch_pdl(k_ex_update<2, 3>, dim3(nb), dim3(256), 0, c->stream, a);
   a.p = c->p;
   a.out = last;
-  k_ex_grad<2, false><<<nb, 256, 0, c->stream>>>(a);
-  k_ex_update<2, 4><<<nb, 256, 0, c->stream>>>(a);
+  launch_pdl(k_ex_grad<2, false>, dim3(nb), dim3(256), 0, c->stream, a);
+  launch_pdl(k_ex_update<2, 4>, dim3(nb), dim3(256), 0, c->stream, a);
   if (c->sd.use_filter)
     enqueue_filter_bc(c, c->k, B, c->st, A);
   else
     k_change<<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(B, A, c->g.mask, c->st,
                                                                      c->g.N);
-  k_finalize<<<1, 1, 0, c->stream>>>(c->st, c->hist, lref(c), c->sd.tol, 1e6 * lref(c));
+  launch_pdl(k_finalize, dim3(1), dim3(1), 0, c->stream, c->st, c->hist, lref(c), c->sd.tol,
+             1e6 * lref(c));
 }
 
 void enqueue_step(wd_ctx* c, const double* A, double* B) {

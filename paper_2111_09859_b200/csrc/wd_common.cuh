@@ -239,6 +239,21 @@ __device__ __forceinline__ long long bc_source(const Geom& g, long long idx,
   return src;
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may be scheduled while its predecessor
+// in the stream still runs; it must not touch anything the predecessor
+// writes (the status word included) before pdl_wait(), which returns once
+// every prerequisite grid has completed and flushed.  pdl_trigger() at the
+// top of a kernel lets ITS successor be scheduled as soon as all of this
+// grid's CTAs have started.  Both are no-ops in a normally launched grid.
+// Wired into the launch-bound 2-D step (wd_stage_explicit.cuh, WD_PDL=1);
+// inside a CUDA-graph replay it measured slower than plain edges (wd_capi.cu:
+// launch_pdl), so the default launches are plain.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Device status word shared by the step kernels (freeze-on-stop).
 struct Status {
   int state;          // WD_STATE_*

@@ -662,6 +662,8 @@ static __global__ void k_change(const double* __restrict__ nw, const double* __r
 // |out - old| (unmasked nodes), |out| and the non-finite flag.
 static __global__ void k_bc_change(const double* __restrict__ in, double* out,
                                    const double* __restrict__ old, Geom g, Status* st) {
+  pdl_trigger();
+  pdl_wait();
   if (st->state != WD_STATE_RUNNING) return;
   double md = 0.0, ma = 0.0;
   int bad = 0;
@@ -705,6 +707,8 @@ static __global__ void k_bc_change(const double* __restrict__ in, double* out,
 
 // Stop test + history (solver.py:253-272).
 static __global__ void k_finalize(Status* st, double* hist, double lref, double tol, double limit) {
+  pdl_trigger();
+  pdl_wait();
   if (st->state == WD_STATE_RUNNING) {
     const double ma = __longlong_as_double((long long)st->max_abs_bits);
     if (st->nonfinite || ma > limit) {

@@ -442,6 +442,8 @@ static __global__ void __launch_bounds__(LF_T)
     k_line_few(const double* __restrict__ in, double* out, Geom g, int axis, int n, long long sa,
                int per, double off, int scheme, TriDev T, Epi epi, FilterCoef fc,
                const uint8_t* pin, int use_geom_pin, int fl, const Status* st) {
+  pdl_trigger();
+  pdl_wait();
   if (st && st->state != WD_STATE_RUNNING) return;
   extern __shared__ double lf_s[];  // [fl][n] right-hand sides -> y -> x, hs[LF_MAXL], factor rows
   const long long L = g.N / n;

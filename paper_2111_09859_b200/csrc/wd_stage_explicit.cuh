@@ -46,6 +46,8 @@ struct ExArgs {
 
 template <int ND, bool DT>
 static __global__ void __launch_bounds__(256) k_ex_grad(ExArgs a) {
+  pdl_trigger();
+  pdl_wait();
   if (a.st && a.st->state != WD_STATE_RUNNING) return;
   const Geom& g = a.g;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
@@ -124,6 +126,8 @@ __device__ __forceinline__ double ex_tend(const ExArgs& a, long long e, const in
 
 template <int ND, int STAGE>
 static __global__ void __launch_bounds__(256) k_ex_update(ExArgs a) {
+  pdl_trigger();
+  pdl_wait();
   if (a.st && a.st->state != WD_STATE_RUNNING) return;
   const Geom& g = a.g;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;

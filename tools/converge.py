@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--c4", default=None)
     ap.add_argument("--c4-n", type=int, default=512)
     ap.add_argument("--c5-steps", type=int, default=0)
+    ap.add_argument("--c5-dims", default="1024x512x256")
     ap.add_argument("--c5-converge", type=int, default=0,
                     help="max_iters of a C5 HJ-curvature fast solve to tol 1e-8 (full size)")
     args = ap.parse_args()
@@ -94,10 +95,11 @@ def main():
 
 
     if args.c5_converge:
-        g = W.build_cylinder(1024, 512, 256, scheme="C6")
+        n5 = tuple(int(v) for v in args.c5_dims.split("x"))
+        g = W.build_cylinder(*n5, scheme="C6")
         faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield",
                  "kmin": "periodic", "kmax": "periodic"}
-        run("c5_cylinder_1024x512x256_hj_curvature_C6_F0.48", g, faces, "hj_curvature", "C6",
+        run(f"c5_cylinder_{args.c5_dims}_hj_curvature_C6_F0.48", g, faces, "hj_curvature", "C6",
             0.48, 1e-8, args.c5_converge, arith="fast",
             exact_fn=lambda gr: np.hypot(gr.x, gr.y) - 0.5, chunk=8)
 
