@@ -421,7 +421,7 @@ static __global__ void __launch_bounds__(LS_WARPS * 32, LS_MINB)
 // cyclic correction, the epilogue / pinned-node restore and store.  Same
 // expressions in the same order as k_line_rhs + k_line_solve (bitwise
 // equal; tests/test_gpu_parity.py), one launch instead of two.
-constexpr int LF_T = 128;   // threads per CTA
+constexpr int LF_T = 256;   // threads per CTA
 constexpr int LF_MAXL = 4;  // lines per CTA (one chain thread per warp)
 constexpr int LF_U = 8;     // chain steps per prefetched batch
 
@@ -468,15 +468,61 @@ static __global__ void __launch_bounds__(LF_T)
     srinv[t] = T.rinv[t];
     sh[t] = T.cyclic ? T.h[t] : 0.0;
   }
-  // ---- A. right-hand sides (all threads; consecutive threads -> consecutive
-  // rows when the axis is contiguous, consecutive lines otherwise)
+  // ---- A. right-hand sides.  Strided lines: a thread owns a run of
+  // consecutive rows of one line and slides a register window over them (one
+  // L2 load per row instead of the stencil's 5 / 11); the rows whose stencil
+  // leaves the line (closures, reduced filter orders, periodic wrap) and
+  // contiguous lines take the per-row evaluation.  Same expressions.
   const int total = nl * n;
-  for (int t = threadIdx.x; t < total; t += LF_T) {
-    const int ll = sa == 1 ? t / n : t % nl;
-    const int i = sa == 1 ? t - ll * n : t / nl;
-    const long long base = line_base(g, axis, q0 + ll);
-    Line w{in + base, sa, n, per, off};
-    lf_s[(size_t)ll * n + i] = line_rhs_at<JOB>(w, i, n, scheme, per, fc);
+  constexpr int HW = JOB == 0 ? 2 : 5;  // stencil reach
+  if (sa != 1 && n >= 4 * (2 * HW + 1)) {
+    const int tpl = LF_T / nl;                  // threads per line
+    const int ll = threadIdx.x / tpl, part = threadIdx.x - ll * tpl;
+    if (ll < nl) {
+      const int rows = (n + tpl - 1) / tpl;
+      const int i0 = part * rows, i1 = min(n, i0 + rows);
+      const long long base = line_base(g, axis, q0 + ll);
+      Line w{in + base, sa, n, per, off};
+      const double* q = in + base;
+      double* dst = lf_s + (size_t)ll * n;
+      const double* fcc = fc.hc + 30;
+      int i = i0;
+      // head rows near the line start
+      for (; i < i1 && i < HW; ++i) dst[i] = line_rhs_at<JOB>(w, i, n, scheme, per, fc);
+      if (i < i1 && i < n - HW) {
+        double win[2 * HW + 1];  // w(i - HW) .. w(i + HW)
+#pragma unroll
+        for (int k = 0; k < 2 * HW; ++k) win[k + 1] = q[(long long)(i - HW + k) * sa];
+        for (; i < i1 && i < n - HW; ++i) {
+#pragma unroll
+          for (int k = 0; k < 2 * HW; ++k) win[k] = win[k + 1];
+          win[2 * HW] = q[(long long)(i + HW) * sa];
+          double r;
+          if (JOB == 0) {
+            // compact interior rows (compact_rhs_at): C6 rows 1 / n-2 use the
+            // C4 relation on non-periodic lines
+            const double d1 = win[HW + 1] - win[HW - 1];
+            if (scheme == WD_C4) r = C4_CA * d1;
+            else if (!per && (i == 1 || i == n - 2)) r = 0.75 * d1;
+            else r = C6_CA * d1 + C6_CB * (win[HW + 2] - win[HW - 2]);
+          } else {
+            r = fcc[0] * win[HW];
+#pragma unroll
+            for (int k = 1; k <= 5; ++k) r = r + fcc[k] * (win[HW + k] + win[HW - k]);
+          }
+          dst[i] = r;
+        }
+      }
+      for (; i < i1; ++i) dst[i] = line_rhs_at<JOB>(w, i, n, scheme, per, fc);
+    }
+  } else {
+    for (int t = threadIdx.x; t < total; t += LF_T) {
+      const int ll = sa == 1 ? t / n : t % nl;
+      const int i = sa == 1 ? t - ll * n : t / nl;
+      const long long base = line_base(g, axis, q0 + ll);
+      Line w{in + base, sa, n, per, off};
+      lf_s[(size_t)ll * n + i] = line_rhs_at<JOB>(w, i, n, scheme, per, fc);
+    }
   }
   __syncthreads();
   // ---- B. one chain per line: lane 0 of warp ll
