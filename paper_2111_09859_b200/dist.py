@@ -440,7 +440,7 @@ class DistributedSolve:
         sd.cfl = float(config.cfl)
         sd.tol = float(config.tol)
         sd.max_iters = int(config.max_iters)
-        sd.arith = {"exact": 0, "fast": 1}[config.arith]
+        sd.arith = {"exact": 0, "fast": 1}[config.resolved_arith()]
         self.gd, self.sd = gd, sd
         ptr = ctypes.c_void_p()
         torch.cuda.synchronize()

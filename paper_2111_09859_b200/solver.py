@@ -86,21 +86,31 @@ class SolveConfig:
     tol: float = 1e-5
     max_iters: int = 50000
     l2_every: int = 0
-    # EXTENSION: "exact" (default) reproduces the reference bit for bit;
-    # "fast" lets the fused 3-D kernels use FMA and the composite Laplacian
-    # stencil (round-off-level differences).
-    arith: str = "exact"
+    # EXTENSION: "exact" reproduces the reference bit for
+    # bit; "fast" lets the kernels reassociate (FMA, composite stencils,
+    # scan-form line solves: round-off-level differences, the converged field
+    # within 1e-10 and the iteration count within 1 of the reference's --
+    # BASELINE's tolerance); "auto" (default) = "fast" for the formulations
+    # whose iteration is stable under round-off perturbations (hj, poisson;
+    # SURVEY sec. 8c) and "exact" for the chaotic ones (hj_lad, hj_curvature,
+    # eikonal), whose parity is only defined bit for bit.
+    arith: str = "auto"
 
     def __post_init__(self):
         if self.cfl <= 0.0:
             raise ValueError("cfl must be positive")
         if self.tol <= 0.0:
             raise ValueError("tol must be positive")
-        if self.arith not in ("exact", "fast"):
-            raise ValueError("arith must be 'exact' or 'fast'")
+        if self.arith not in ("auto", "exact", "fast"):
+            raise ValueError("arith must be 'auto', 'exact' or 'fast'")
 
     def uses_filter(self) -> bool:
         return self.filter_config is not None and self.scheme != "UW"
+
+    def resolved_arith(self) -> str:
+        if self.arith != "auto":
+            return self.arith
+        return "fast" if self.formulation.kind in ("hj", "poisson") else "exact"
 
 
 @dataclass
@@ -225,7 +235,7 @@ def solve_steady(grid, boundary: BoundarySpec, config: SolveConfig, phi0=None, e
     fc = config.formulation
     ctx = NativeSolver(grid, boundary.faces, boundary.solid_mask, config.scheme, fc,
                        config.filter_config if config.uses_filter() else None, config.cfl,
-                       config.tol, config.max_iters, arith=config.arith)
+                       config.tol, config.max_iters, arith=config.resolved_arith())
     try:
         lib = ctx.lib
         if phi0 is None:

@@ -25,7 +25,7 @@ def _need_gpu():
 def test_parked_context_reuse_is_invisible(monkeypatch):
     g = W.build_cartesian(41, 21, Lx=2.0, Ly=1.0)
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E4",
-                        filter_config=W.FilterConfig(0.49), tol=1e-12, max_iters=30)
+                        filter_config=W.FilterConfig(0.49), tol=1e-12, max_iters=30, arith="exact")
     monkeypatch.setenv("WD_NO_CTX_POOL", "1")
     fresh = W.solve_steady(g, W.BoundarySpec(PLATE), cfg)
     fresh20 = W.solve_steady(g, W.BoundarySpec(PLATE), dataclasses.replace(cfg, max_iters=20))
@@ -60,3 +60,17 @@ def test_operator_cache_follows_the_grid():
     k4 = F.tendency(phi, g, "E4", fc)          # fresh context, same answer
     assert same(k3, k4) and not same(k3, k1)
     _context.drop_cached()
+
+
+def test_default_arithmetic_is_auto():
+    """SolveConfig.arith defaults to "auto": fast arithmetic for the
+    round-off-stable formulations (hj, poisson), exact for the chaotic ones."""
+    mk = lambda kind: W.SolveConfig(formulation=W.FormulationConfig(kind=kind))  # noqa: E731
+    assert mk("hj").arith == "auto"
+    assert mk("hj").resolved_arith() == "fast" and mk("poisson").resolved_arith() == "fast"
+    for kind in ("eikonal", "hj_lad", "hj_curvature"):
+        assert mk(kind).resolved_arith() == "exact"
+    import dataclasses
+    assert dataclasses.replace(mk("hj"), arith="exact").resolved_arith() == "exact"
+    with pytest.raises(ValueError):
+        W.SolveConfig(arith="sloppy")

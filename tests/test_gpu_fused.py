@@ -64,7 +64,7 @@ def test_fused_vs_oracle(case):
                   phi0=phi0, raise_on_divergence=False)
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme=scheme,
                         filter_config=None if af is None else W.FilterConfig(af), tol=1e-15,
-                        max_iters=iters)
+                        max_iters=iters, arith="exact")
     ctx = _context.NativeSolver(pg, faces, None, scheme, cfg.formulation, cfg.filter_config)
     assert ctx.fused, "fused path expected"
     ctx.close()
@@ -79,7 +79,8 @@ def test_fused_matches_generic(monkeypatch):
     faces = _faces(per, ("wall", "wall"))
     pg = W.build_cartesian(*dims, periodic=per)
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E6",
-                        filter_config=W.FilterConfig(0.49), tol=1e-15, max_iters=10)
+                        filter_config=W.FilterConfig(0.49), tol=1e-15, max_iters=10,
+                        arith="exact")
     a = W.solve_steady(pg, W.BoundarySpec(faces), cfg)
     monkeypatch.setenv("WD_DISABLE_FUSED", "1")
     ctx = _context.NativeSolver(pg, faces, None, "E6", cfg.formulation, cfg.filter_config)

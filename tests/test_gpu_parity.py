@@ -204,7 +204,8 @@ def _product_case(z, uniform_from=None):
     cfg = slv.SolveConfig(formulation=forms.FormulationConfig(kind=str(z["kind"])),
                           scheme=str(z["scheme"]),
                           filter_config=None if af is None else ops.FilterConfig(af),
-                          cfl=float(z["cfl"]), tol=float(z["tol"]), max_iters=int(z["max_iters"]))
+                          cfl=float(z["cfl"]), tol=float(z["tol"]), max_iters=int(z["max_iters"]),
+                          arith="exact")
     return g, slv.BoundarySpec(faces, z.get("solid_mask")), cfg
 
 
@@ -232,7 +233,8 @@ def test_solve_uniform_cartesian_c1_prefix():
     z = goldens.load("solve_c1_plate_hj_E4")
     g = G.build_cartesian(201, 101, Lx=2.0, Ly=1.0)
     cfg = slv.SolveConfig(formulation=forms.FormulationConfig(kind="hj"), scheme="E4",
-                          filter_config=ops.FilterConfig(0.49), tol=1e-8, max_iters=50000)
+                          filter_config=ops.FilterConfig(0.49), tol=1e-8, max_iters=50000,
+                          arith="exact")
     rep = slv.solve_steady(g, slv.BoundarySpec(goldens.case_faces(z)), cfg)
     assert rep.iters == int(z["iters"]) == 18440
     assert same(rep.residual_history, z["residual_history"])
@@ -247,7 +249,7 @@ def test_divergence_plate():
     from paper_2111_09859_b200.errors import DivergenceError
     g = G.build_cartesian(41, 21, Lx=2.0, Ly=1.0)
     cfg = slv.SolveConfig(formulation=forms.FormulationConfig(kind="hj"), scheme="E4",
-                          tol=1e-12, max_iters=5000)
+                          tol=1e-12, max_iters=5000, arith="exact")
     faces = dict(zip(goldens.FACES, ("farfield", "farfield", "wall", "farfield")))
     with pytest.raises(DivergenceError, match=f"iteration {int(z['diverged_at'])}"):
         slv.solve_steady(g, slv.BoundarySpec(faces), cfg)
@@ -259,7 +261,7 @@ def _ext_solve(og, pg, faces, kind, scheme, af, iters, cfl=0.5):
     ro = wd.solve(og, wd.Boundary(faces), cfg_o)
     cfg_p = slv.SolveConfig(formulation=forms.FormulationConfig(kind=kind), scheme=scheme,
                             filter_config=None if af is None else ops.FilterConfig(af),
-                            cfl=cfl, tol=1e-14, max_iters=iters)
+                            cfl=cfl, tol=1e-14, max_iters=iters, arith="exact")
     rp = slv.solve_steady(pg, slv.BoundarySpec(faces), cfg_p)
     return ro, rp
 

@@ -61,7 +61,8 @@ def test_solve_l2_history():
     g = W.build_cartesian(41, 21, Lx=2.0, Ly=1.0)
     faces = {"imin": "farfield", "imax": "farfield", "jmin": "wall", "jmax": "farfield"}
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E4",
-                        filter_config=W.FilterConfig(0.49), tol=1e-12, max_iters=40, l2_every=5)
+                        filter_config=W.FilterConfig(0.49), tol=1e-12, max_iters=40, l2_every=5,
+                        arith="exact")
     rep = W.solve_steady(g, W.BoundarySpec(faces), cfg, exact=g.y.copy())
     h = np.asarray(rep.l2_history)
     assert h.shape == z["l2h"].shape

@@ -20,7 +20,7 @@ def _setup(z):
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=str(z["kind"])),
                         scheme=str(z["scheme"]),
                         filter_config=None if np.isnan(af) else W.FilterConfig(af), cfl=0.5,
-                        tol=float(z["tol"]), max_iters=int(z["max_iters"]))
+                        tol=float(z["tol"]), max_iters=int(z["max_iters"]), arith="exact")
     return g, motion, cfg
 
 
