@@ -41,7 +41,8 @@ struct wd_dist {
   long long plane = 0, Nl = 0, Ng = 0;  // nodes per plane, per slab, per ghosted slab
   // fused program
   double* A = nullptr;  // ghosted state (B = c->phiY, Pa = c->p, Pb = c->k)
-  double *mine = nullptr, *all = nullptr;
+  double *mine = nullptr, *all = nullptr, *coef2 = nullptr;
+  const double* fixc = nullptr;  // this step's filtered correction planes, if fused
   wd::F0Tables f0;
   double* f0_dev = nullptr;
   // transposes / pencils
@@ -468,6 +469,26 @@ int dist_filter0_fused(wd_dist* d, double* Pb, double* T1) {
     if (int rc = comm_rc(d, d->comm->allgather(d->mine, d->all, (size_t)3 * d->plane, s)))
       return rc;
     k_f0_carry<<<nblocks(d->plane, 256), 256, 0, s>>>(d->all, d->mine, d->plane, d->f0, c->st);
+    // The correction cf W_i + cb Qp_i - f z_i is separable (per-line
+    // coefficient x per-plane factor) and the j / k sweeps are linear, so
+    // the sweeps can run on x' and the correction be added at the end with
+    // the coefficient PLANES filtered instead: two tiny sweeps over 3 planes
+    // and three L2-resident loads in the last sweep's store replace a
+    // 2-word pass over the slab.
+    // Measured at 512^3 (ncu, P = 1): the last sweep grows from 712 to 1044 us
+    // with the three coefficient loads per node, the 318 us pass goes away:
+    // no net gain, so the separate pass stays the default (WD_F0_FIX_FUSED=1
+    // selects the fused form; tests/test_gpu_dist.py runs both).
+    static const bool fusedfix = getenv("WD_F0_FIX_FUSED") != nullptr;
+    if (fusedfix && d->coef2 && c->scan[1].tab && c->scan[2].tab) {
+      fused_filter_any(c->fused, 1, d->mine, d->coef2, 3, d->n1, d->n2, c->g.per[1], c->filt[1],
+                       nullptr, c->st, s, &c->scan[1]);
+      fused_filter_any(c->fused, 2, d->coef2, d->mine, 3, d->n1, d->n2, c->g.per[2], c->filt[2],
+                       nullptr, c->st, s, &c->scan[2]);
+      d->fixc = d->mine;
+      return WD_OK;
+    }
+    d->fixc = nullptr;
     const dim3 fg((unsigned)((d->plane + 255) / 256), (unsigned)((d->nl + F0_FR - 1) / F0_FR));
     k_f0_fix<<<fg, 256, 0, s>>>(T1, d->mine, d->nl, d->plane, d->f0, c->st);
     return WD_OK;
@@ -519,12 +540,14 @@ int dist_step_fused(wd_dist* d, double* X, double* Y) {
   }
   c->fused.i_lo = G;
   c->fused.i_hi = G + nl;
+  d->fixc = nullptr;
   if (int rc = dist_filter0_fused(d, Pb, T1)) return rc;
   const long long go = (long long)G * d->plane;
   fused_filter_any(c->fused, 1, T1, T2, nl, d->n1, d->n2, c->g.per[1], c->filt[1], nullptr, c->st, s,
                    c->scan[1].tab ? &c->scan[1] : nullptr);
   fused_filter_any(c->fused, 2, T2, Y + go, nl, d->n1, d->n2, c->g.per[2], c->filt[2], X + go,
-                   c->st, s, c->scan[2].tab ? &c->scan[2] : nullptr);
+                   c->st, s, c->scan[2].tab ? &c->scan[2] : nullptr, d->fixc,
+                   d->fixc ? d->f0.tab + 6 * nl : nullptr);
   dist_reduce(d);
   k_finalize<<<1, 1, 0, s>>>(c->st, d->hist, lref(c), c->sd.tol, 1e6 * lref(c));
   DCK(d, cudaGetLastError());
@@ -775,6 +798,7 @@ int wd_dist_destroy(wd_dist* d) {
   cudaFree(d->xflags);
   ws_free(d->A, (size_t)d->Ng * sizeof(double));
   cudaFree(d->mine);
+  cudaFree(d->coef2);
   cudaFree(d->all);
   cudaFree(d->f0_dev);
   cudaFree(d->send);
@@ -875,7 +899,8 @@ int wd_dist_create(wd_comm* cm, const wd_grid_desc* gd, const wd_solver_desc* sd
     if (ws_alloc((void**)&d->A, (size_t)d->Ng * sizeof(double)) != cudaSuccess)
       return bail(fail(WD_ERR_CUDA, "slab allocation failed"));
     if (d->filter0 == 0) {
-      if (cudaMalloc(&d->mine, (size_t)3 * d->plane * sizeof(double)) != cudaSuccess ||
+      if (cudaMalloc(&d->coef2, (size_t)3 * d->plane * sizeof(double)) != cudaSuccess ||
+          cudaMalloc(&d->mine, (size_t)3 * d->plane * sizeof(double)) != cudaSuccess ||
           cudaMalloc(&d->all, (size_t)3 * P * d->plane * sizeof(double)) != cudaSuccess)
         return bail(fail(WD_ERR_CUDA, "carry buffer allocation failed"));
       if ((rc = dist_f0_tables(d))) return bail(rc);

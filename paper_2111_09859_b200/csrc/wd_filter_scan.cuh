@@ -105,6 +105,8 @@ struct ScanArgs {
   FilterCoef fc;
   const double* A;  // nullptr -> no convergence reduction
   Status* st;
+  const double* fixc;    // FIX: [3][n1 n2] coefficient planes (see SweepArgs)
+  const double* fixrow;  // FIX: [3][n0] per-plane factors
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
@@ -159,7 +161,11 @@ __device__ __forceinline__ double fs_rhsh(const double* w, int h, const double* 
 // mbarriers, one per half of the rows, so the segments of the first half
 // start their right-hand sides while the second half is still in flight;
 // the other instantiations stage with per-thread cp.async.
-template <bool AX2, int MM, bool RED, bool TMA>
+// FIX (AX2 && RED only): out = x + c0 W_i + c1 Qp_i - c2 z_i with the
+// per-line coefficients c(j, k) and the per-plane factors of plane i: the
+// correction of the slab-decomposed axis-0 filter, which commutes with the j
+// and k sweeps (all linear), applied here instead of in a pass of its own.
+template <bool AX2, int MM, bool RED, bool TMA, bool FIX = false>
 #ifndef WD_SCAN_TG
 #define WD_SCAN_TG 0  // 1: factor tables read from global memory (L1) instead of shared
 #endif
@@ -464,6 +470,24 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB)
       if (per) x = fma(-f, t4.y, x);
       return x;
     };
+    // FIX: the plane's factors and the tile's offset inside a coefficient plane
+    double fxW = 0.0, fxQ = 0.0, fxZ = 0.0;
+    long long fxoff = 0;
+    if (FIX) {
+      const long long oc = q / nb;  // plane i of this tile (axis 2: outer = i)
+      fxW = a.fixrow[oc];
+      fxQ = a.fixrow[a.n0 + oc];
+      fxZ = a.fixrow[2 * a.n0 + oc];
+      fxoff = base - oc * a.s0;
+    }
+    const long long fxN = (long long)a.n1 * a.n2;
+    auto fixed = [&](double x, long long off2) {  // off2: offset inside the plane
+      if (!FIX) return x;
+      const double* pc = a.fixc + off2;
+      x = fma(__ldg(pc), fxW, x);
+      x = fma(__ldg(pc + fxN), fxQ, x);
+      return fma(-__ldg(pc + 2 * fxN), fxZ, x);
+    };
     // ---- 4. store (+ convergence reduction against A)
     auto emit = [&](double* po, const double* pa, double x) {
       __stcs(po, x);
@@ -550,7 +574,8 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB)
               if (l0 + u < nl) {
 #pragma unroll
                 for (int k = 0; k < KK; ++k) {
-                  const double x = pt[u * LS + k * FS_T];
+                  const double x = fixed(pt[u * LS + k * FS_T],
+                                         fxoff + (l0 + u) * lstride + tid + k * FS_T);
                   __stcs(po + u * lstride + k * FS_T, x);
                   if (!isfinite(x)) bad = 1;
                   ma = fmax(ma, fabs(x));
@@ -564,7 +589,8 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB)
           }
         } else {
           for (int ll = 0; ll < nl; ++ll) {
-            for (int r = 0; r + tid < n; r += FS_T) emit(po + r, pa + r, pt[r]);
+            for (int r = 0; r + tid < n; r += FS_T)
+              emit(po + r, pa + r, fixed(pt[r], fxoff + ll * lstride + tid + r));
             po += lstride;
             if (RED) pa += lstride;
             pt += LS;

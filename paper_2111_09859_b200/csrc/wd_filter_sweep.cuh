@@ -56,6 +56,10 @@ struct SweepArgs {
   // fused convergence reduction (last axis)
   const double* A;     // nullptr -> no reduction
   Status* st;
+  // slab decomposition (scan form, last sweep): rank-separable correction of
+  // the partitioned axis-0 filter, added on the way out (wd_dist_filter0.cuh)
+  const double* fixc = nullptr;    // [3][n1 n2] filtered per-line coefficients
+  const double* fixrow = nullptr;  // [3][n0] per-plane factors W, Qp, z
 };
 
 __device__ __forceinline__ double div_rn(double s, double d, double r) {

@@ -167,9 +167,38 @@ void scan_one(const ScanArgs& a, long long groups, cudaStream_t s) {
   scan_launch<AX2, MM, RED, false>(a, tm, groups, s);
 }
 
+// last sweep of the slab-decomposed step with the axis-0 correction fused
+template <int MM>
+void scan_fix(const ScanArgs& a, long long groups, cudaStream_t s) {
+  ScanTma tm;
+  std::memset(&tm, 0, sizeof(tm));
+  static int ctas = 0;
+  const size_t smax = scan_smem(FS_NMAX);
+  if (!ctas) {
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_filter_scan<true, MM, true, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, k_filter_scan<true, MM, true, false, true>, FS_T, smax);
+    ctas = sms * (occ > 0 ? occ : 1);
+  }
+  const long long c = ctas < groups ? ctas : groups;
+  k_filter_scan<true, MM, true, false, true><<<(int)c, FS_T, scan_smem(a.T.n), s>>>(a, tm);
+}
+
 template <bool AX2, bool RED>
 void scan_mm(const ScanArgs& a, long long groups, cudaStream_t s) {
   static const bool generic = getenv("WD_SCAN_GENERIC") != nullptr;  // A/B knob
+  if constexpr (AX2 && RED) {
+    if (a.fixc) {
+      if (a.T.n == FS_S * FS_M && !generic) scan_fix<FS_M>(a, groups, s);
+      else if (a.T.n == FS_S * 16 && !generic) scan_fix<16>(a, groups, s);
+      else scan_fix<0>(a, groups, s);
+      return;
+    }
+  }
   if (a.T.n == FS_S * FS_M && !generic) scan_one<AX2, FS_M, RED>(a, groups, s);
   else if (a.T.n == FS_S * 16 && !generic) scan_one<AX2, 16, RED>(a, groups, s);
   else scan_one<AX2, 0, RED>(a, groups, s);
@@ -191,6 +220,8 @@ void launch_scan(const SweepArgs& w, const ScanDev& T, cudaStream_t s) {
   a.fc = w.fc;
   a.A = w.A;
   a.st = w.st;
+  a.fixc = w.axis == 2 && w.A ? w.fixc : nullptr;
+  a.fixrow = w.fixrow;
   const long long inner = w.axis == 2 ? w.n1 : w.n2;
   const long long outer = w.axis == 0 ? w.n1 : w.n0;
   const long long groups = outer * ((inner + FS_L - 1) / FS_L);
@@ -511,8 +542,11 @@ bool fused_can_push(const FusedPlan& fp) {
 
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
                       int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
-                      cudaStream_t s, const ScanDev* scan) {
+                      cudaStream_t s, const ScanDev* scan, const double* fixc,
+                      const double* fixrow) {
   SweepArgs w;
+  w.fixc = fixc;
+  w.fixrow = fixrow;
   w.in = in;
   w.out = out;
   const int nn[3] = {n0, n1, n2};

@@ -82,6 +82,7 @@ bool fused_can_push(const FusedPlan& fp);
 void fused_filter_prepare(int n);  // opt in to the sweep's shared memory for length n
 void fused_filter_any(const FusedPlan& fp, int axis, const double* in, double* out, int n0,
                       int n1, int n2, int per, const TriDev& T, const double* A, Status* st,
-                      cudaStream_t s, const ScanDev* scan = nullptr);
+                      cudaStream_t s, const ScanDev* scan = nullptr, const double* fixc = nullptr,
+                      const double* fixrow = nullptr);
 
 }  // namespace wd

@@ -178,6 +178,19 @@ def test_peer_memory_push_solo_graph(monkeypatch):
         comm.close()
 
 
+def test_fused_axis0_correction_matches_the_pass(monkeypatch):
+    """WD_F0_FIX_FUSED: the partitioned filter's correction added in the last
+    sweep's store (filtered coefficient planes; the sweeps are linear) instead
+    of a pass of its own: same field to round-off."""
+    g, cfg, phi0 = _channel(n0=64, arith="fast", steps=4)
+    base, hist0, _ = _dist_solve(2, g, FACES, cfg, phi0, 4, filter0="partitioned")
+    monkeypatch.setenv("WD_F0_FIX_FUSED", "1")
+    got, hist, _ = _dist_solve(2, g, FACES, cfg, phi0, 4, filter0="partitioned")
+    scale = float(np.max(np.abs(base)))
+    assert np.max(np.abs(got - base)) <= 1e-13 * scale
+    assert np.allclose(hist, hist0, rtol=1e-9, atol=1e-15)
+
+
 def test_steps_past_the_stop_keep_the_state():
     """stepping a stopped solve must not move the reported state
     (buffer parity follows the completed-step count, not the enqueued one)."""
