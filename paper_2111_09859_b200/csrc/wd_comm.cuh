@@ -133,7 +133,7 @@ struct wd_comm {
     double* lo_int = t + (size_t)G * plane;
     double* hi_int = t + (size_t)nl * plane;
     double* hi_ghost = t + (size_t)(nl + G) * plane;
-    if (P == 1 || kind == 2) {
+    if ((P == 1 && !nccl) || kind == 2) {
       if (int rc = cuda_rc(cudaMemcpyAsync(lo_ghost, hi_int, cnt * 8, cudaMemcpyDeviceToDevice, s),
                            "halo copy"))
         return rc;
@@ -160,7 +160,7 @@ struct wd_comm {
 
   // all[q * count ..] <- rank q's mine[0 .. count)
   int allgather(const double* mine, double* all, size_t count, cudaStream_t s) {
-    if (P == 1)
+    if (P == 1 && !nccl)
       return cuda_rc(cudaMemcpyAsync(all, mine, count * 8, cudaMemcpyDeviceToDevice, s),
                      "allgather copy");
     if (kind == 2) {  // every slot <- mine: the received volume of a real all_gather
@@ -182,7 +182,7 @@ struct wd_comm {
 
   // recv[q * count ..] <- rank q's send[rank * count ..]  (slab <-> pencil)
   int alltoall(const double* send, double* recv, size_t count, cudaStream_t s) {
-    if (P == 1 || kind == 2)
+    if ((P == 1 && !nccl) || kind == 2)
       return cuda_rc(cudaMemcpyAsync(recv, send, count * 8 * P, cudaMemcpyDeviceToDevice, s),
                      "alltoall copy");
     if (kind == 1) {
@@ -203,7 +203,7 @@ struct wd_comm {
 
   // element-wise max over the ranks of n int64 words, in place
   int allreduce_max(long long* buf, int n, cudaStream_t s) {
-    if (P == 1 || kind == 2) return WD_OK;
+    if ((P == 1 && !nccl) || kind == 2) return WD_OK;
     if (kind == 1) {
       if (cb.allreduce_max(cb.user, buf, n, (void*)s)) {
         err = "allreduce callback failed";

@@ -305,7 +305,7 @@ void dist_filter0_generic(wd_ctx* c, const double* cur, double* nxt, const Statu
 // local maxima of the status word -> max over the ranks (before k_finalize)
 void dist_reduce(wd_dist* d) {
   wd_ctx* c = d->c;
-  if (d->P == 1) return;
+  if (d->P == 1 && !d->comm->nccl) return;
   k_stats_out<<<1, 1, 0, c->stream>>>(c->st, d->stats);
   if (comm_rc(d, d->comm->allreduce_max(d->stats, 3, c->stream))) return;
   k_stats_in<<<1, 1, 0, c->stream>>>(c->st, d->stats);
@@ -722,8 +722,12 @@ int wd_comm_init(const void* nccl_id, int rank, int nranks, int decomposition, w
   cm->P = nranks;
   cm->kind = 0;
   cm->decomposition = decomposition;
-  if (nranks > 1) {
-    if (!nccl_id) {
+  // WD_NCCL_SELF: a one-rank communicator still goes through NCCL (self
+  // send/recv, all_gather, all_reduce inside the captured graph): exercises
+  // the loader, the ABI constants and the capture on a single GPU
+  const bool self = nranks == 1 && getenv("WD_NCCL_SELF") != nullptr;
+  if (nranks > 1 || self) {
+    if (!nccl_id && !self) {
       delete cm;
       return fail(WD_ERR_INVALID, "nccl_id is required for more than one rank");
     }
@@ -734,7 +738,16 @@ int wd_comm_init(const void* nccl_id, int rank, int nranks, int decomposition, w
       return fail(WD_ERR_CUDA, err);
     }
     NcclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
+    if (self) {
+      const int rc0 = cm->api->GetUniqueId(&id);
+      if (rc0) {
+        const std::string msg = std::string("ncclGetUniqueId: ") + cm->api->GetErrorString(rc0);
+        delete cm;
+        return fail(WD_ERR_CUDA, msg);
+      }
+    } else {
+      std::memcpy(&id, nccl_id, sizeof(id));
+    }
     const int rc = cm->api->CommInitRank(&cm->nccl, nranks, id, rank);
     if (rc) {
       const std::string msg = std::string("ncclCommInitRank: ") + cm->api->GetErrorString(rc);

@@ -324,6 +324,39 @@ def test_nccl_comm_single_rank_graph():
         comm.close()
 
 
+def test_nccl_self_communicator(monkeypatch):
+    """WD_NCCL_SELF: the one-rank communicator really goes through NCCL -- the
+    dlopen'ed library, ncclSend/Recv to self for the ghost planes,
+    ncclAllGather for the carries, ncclAllReduce(max) for the stop test, all
+    captured in the step graph -- and gives the single-GPU result."""
+    from paper_2111_09859_b200 import dist
+    monkeypatch.setenv("WD_NCCL_SELF", "1")
+    g, cfg, phi0 = _channel(n0=64, arith="fast", steps=6)
+    ref = W.solve_steady(g, W.BoundarySpec(FACES), cfg, phi0=phi0)
+    comm = dist.NcclComm(0, 1)
+    scale = float(np.max(np.abs(ref.phi)))
+    try:
+        for filter0 in ("partitioned", "transpose"):
+            ds = dist.DistributedSolve(g, FACES, cfg, comm, filter0=filter0)
+            try:
+                assert ds.graph
+                ds.bind(phi0)
+                ds.steps(3)
+                ds.steps(3)
+                assert ds.status().iters == 6
+                got = ds.finish().cpu().numpy()
+                assert np.max(np.abs(got - ref.phi)) <= 1e-12 * scale, filter0
+            finally:
+                ds.close()
+        # the generic program's all_to_all (grouped send/recv) as well
+        g2, cfg2, p2 = _cylinder("hj_curvature", "exact", 3)
+        ref2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2)
+        rep2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2, comm=comm)
+        assert same(rep2.phi, ref2.phi) and same(rep2.residual_history, ref2.residual_history)
+    finally:
+        comm.close()
+
+
 def test_slab_checks():
     from paper_2111_09859_b200 import dist
     with pytest.raises(ValueError):
