@@ -356,7 +356,7 @@ def run_b200_dist(args, world, rank, local):
             "gpu_launches": K * launches, "clocks": clk, "e2e": e2e,
             "time_to_converge": _time_to_converge(secs / K * 1e3, args.arith)}
     if rank == 0 and not args.no_cpu and world == 1:
-        line["cpu_baseline"] = cpu_sample(cfg, 3, 1)
+        line["cpu_baseline"] = cpu_sample(cfg, 9, 1)
     comm.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -523,7 +523,7 @@ def run_b200(args, world, rank, local):
             "clocks": clk, "e2e": e2e,
             "exact_mode": exact_side, "time_to_converge": ttc}
     if rank == 0 and not args.no_cpu and world == 1:
-        line["cpu_baseline"] = cpu_sample(cfg, 3, 1)
+        line["cpu_baseline"] = cpu_sample(cfg, 9, 1)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
