@@ -27,6 +27,11 @@ def main():
     ap.add_argument("--arith", default="fast")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "converge_c4.json"))
+    ap.add_argument("--comm", default=None,
+                    help="run the slab-decomposed program: 'nccl1' (one-rank NCCL communicator; "
+                         "set WD_NCCL_SELF=1 for real NCCL calls) or 'soloP' (rank 0 of a P-way "
+                         "split alone: the field is x-invariant, so its 512/P planes wrapped "
+                         "onto themselves are the same problem)")
     args = ap.parse_args()
     import torch
     import paper_2111_09859_b200 as W
@@ -38,8 +43,12 @@ def main():
     cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E6",
                         filter_config=W.FilterConfig(0.49), cfl=0.5, tol=float(gold["tol"]),
                         max_iters=int(gold["iters"]) + 20000, arith=args.arith)
+    comm = None
+    if args.comm:
+        from paper_2111_09859_b200 import dist
+        comm = dist.NcclComm(0, 1) if args.comm == "nccl1" else dist.SoloComm(int(args.comm[4:]), 0)
     t0 = time.perf_counter()
-    rep = W.solve_steady(g, W.BoundarySpec(faces), cfg, device_result=True)
+    rep = W.solve_steady(g, W.BoundarySpec(faces), cfg, device_result=True, comm=comm)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     phi = rep.phi
@@ -56,6 +65,7 @@ def main():
     out = {
         "config": f"c4_channel3d_{n}^3_hj_E6_F0.49",
         "arith": args.arith,
+        "program": args.comm or "single GPU",
         "tol": float(gold["tol"]),
         "iters": int(rep.iters),
         "converged": bool(rep.converged),
