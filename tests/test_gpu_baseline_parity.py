@@ -100,6 +100,17 @@ def test_c2_annulus_257x129_curvature_c6_outcome_exact():
     assert rep.converged and np.max(np.abs(rep.phi - d)[near]) <= 1e-4
 
 
+def test_c2_annulus_257x129_curvature_c6_fast_converges_like_the_oracle():
+    """Fast arithmetic (scan derivatives, Thomas factor) on the whole config-2
+    run: the oracle's 5,078 iterations within 1, field within 1e-10 * max."""
+    z = goldens.load("base_c2_annulus_curv_C6_full")
+    g = W.build_annulus(257, 129, scheme="C6")
+    rep, div = _solve(g, RING, z, arith="fast")
+    assert rep is not None and rep.converged
+    assert abs(rep.iters - int(z["iters"])) <= 1, rep.iters
+    assert np.max(np.abs(rep.phi - z["phi"])) <= 1e-10 * float(np.max(np.abs(z["phi"])))
+
+
 # --------------------------------------------------------------- config 3
 @pytest.mark.parametrize("kind", ["hj", "eikonal", "hj_lad"])
 def test_c3_bump_1025x513_e6_exact(kind):
