@@ -112,6 +112,12 @@ int wd_device_count(void);
  * field-independent tridiagonal factors and per-node metric sums.        */
 int wd_create(const wd_grid_desc* grid, const wd_solver_desc* solver, void* stream,
               wd_ctx** out);
+/* Contexts whose descriptors carry no caller-owned device pointers (uniform
+ * grid, no solid mask) are parked on wd_destroy (at most two per process)
+ * and handed back by wd_create for an equal descriptor, so repeated one-shot
+ * solves do not pay the factorisation, allocations and graph instantiation
+ * again (WD_NO_CTX_POOL disables it).  Not thread-safe per context; the
+ * pool itself is.                                                          */
 int wd_destroy(wd_ctx* ctx);
 /* Bind the caller's state field (in/out), the device history buffer
  * (max_iters doubles, SolveReport.residual_history) and reset the status.
