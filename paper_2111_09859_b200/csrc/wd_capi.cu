@@ -433,6 +433,7 @@ struct wd_dist;
 
 struct wd_ctx {
   wd_dist* dist = nullptr;  // GENERIC slab-decomposed program (wd_dist.cuh): axis-0 hooks
+  int concurrent = -1;      // independent line passes in one launch: -1 undecided, 0 no, 1 yes
   bool nopool = true;       // parked for reuse only when fully built and unmodified
   int device = 0;
   std::string env_sig;      // A/B environment knobs the plan was built under
@@ -618,9 +619,85 @@ void launch_deriv(wd_ctx* c, const double* in, double* out, double* scratch, int
   }
 }
 
+// Grids with few long lines (2-D configs, exact arithmetic): every compact
+// pass is one dependency chain per line, ~25-100 us regardless of how little
+// data it moves, and a tendency runs 10 of them back to back.  The passes of
+// one phase are independent (the gradient's axes; the divergence's terms,
+// which only meet in their sum), so they go into ONE launch
+// (k_line_few_multi, blockIdx.y = pass) and the divergence terms are summed
+// afterwards in the reference's order (k_div_combine): bit-identical to the
+// serial chain.  (Forked streams -- parallel graph branches -- were measured
+// 2x SLOWER than the serial launches: C2 1.23 -> 2.58 ms per step.)
+bool concurrent_passes(wd_ctx* c) {
+  if (c->concurrent >= 0) return c->concurrent != 0;
+  c->concurrent = 0;
+  const Geom& g = c->g;
+  const int sc = c->sd.scheme;
+  if ((sc != WD_C4 && sc != WD_C6) || c->dist || getenv("WD_NO_CONCURRENT")) return false;
+  if (c->sd.arith == 1) return false;  // fast arithmetic: the scan kernels
+  for (int a = 0; a < g.nd; ++a) {
+    const long long L = g.N / g.n[a];
+    if (!(L <= 148LL * 2 * LF_MAXL && line_solve_ok(g.n[a]) &&
+          line_few_smem(g.n[a], LF_MAXL) <= kLineSolveMaxSmem))
+      return false;
+  }
+  cudaFuncSetAttribute(k_line_few_multi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kLineSolveMaxSmem);
+  c->concurrent = 1;
+  return true;
+}
+
+// up to 4 compact-derivative passes (plain epilogue) per launch
+void launch_line_multi(wd_ctx* c, int count, const double* const* in, double* const* out,
+                       const int* axis, const Status* st) {
+  const Geom& g = c->g;
+  for (int q0 = 0; q0 < count; q0 += 4) {
+    LineFewJobs jobs;
+    std::memset(&jobs, 0, sizeof(jobs));
+    jobs.count = std::min(4, count - q0);
+    long long lmax = 0;
+    int nmax = 0;
+    for (int q = 0; q < jobs.count; ++q) {
+      const int a = axis[q0 + q];
+      jobs.in[q] = in[q0 + q];
+      jobs.out[q] = out[q0 + q];
+      jobs.axis[q] = a;
+      jobs.T[q] = c->comp[a];
+      lmax = std::max(lmax, g.N / g.n[a]);
+      nmax = std::max(nmax, g.n[a]);
+    }
+    int fl = (int)((lmax + 147) / 148);
+    fl = std::max(1, std::min(fl, LF_MAXL));
+    const dim3 grid((unsigned)((lmax + fl - 1) / fl), (unsigned)jobs.count);
+    k_line_few_multi<<<grid, LF_T, line_few_smem(nmax, fl), c->stream>>>(jobs, g, c->sd.scheme,
+                                                                        fl, st);
+  }
+}
+
 // lap / kappa = sum_m sum_l M[l,m] D_l(V_m)  (formulations.py:135-143)
 void launch_divergence(wd_ctx* c, double* const V[3], int csch, double* out, const Status* st) {
   const int nd = c->g.nd;
+  if (csch == c->sd.scheme && concurrent_passes(c)) {
+    DivTerms t;
+    std::memset(&t, 0, sizeof(t));
+    double* pool[9] = {c->B[0], c->B[1], c->B[2], c->F[0], c->F[1], c->F[2],
+                       c->Ue[0], c->Ue[1], c->Ue[2]};  // UW-only fields: free here
+    const double* src[9];
+    for (int m = 0; m < nd; ++m)
+      for (int l = 0; l < nd; ++l) {
+        if (c->M.m == nullptr ? l != m : !c->mterm[l * nd + m]) continue;
+        t.D[t.count] = pool[t.count];
+        src[t.count] = V[m];
+        t.l[t.count] = l;
+        t.m[t.count] = m;
+        ++t.count;
+      }
+    launch_line_multi(c, t.count, src, pool, t.l, st);
+    const int nb = nblocks(c->g.N, kThreads);
+    if (nd == 3) k_div_combine<3><<<nb, kThreads, 0, c->stream>>>(t, c->M, out, c->g.N, st);
+    else k_div_combine<2><<<nb, kThreads, 0, c->stream>>>(t, c->M, out, c->g.N, st);
+    return;
+  }
   bool first = true;
   for (int m = 0; m < nd; ++m)
     for (int l = 0; l < nd; ++l) {
@@ -663,6 +740,12 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
 
 // directional derivatives of p with the run's scheme -> dphi (+B, F for UW)
 void launch_dphi(wd_ctx* c, const double* p, const Status* st) {
+  if (c->sd.scheme != WD_UW && concurrent_passes(c)) {
+    const double* in3[3] = {p, p, p};
+    const int ax3[3] = {0, 1, 2};
+    launch_line_multi(c, c->g.nd, in3, c->dphi, ax3, st);
+    return;
+  }
   for (int l = 0; l < c->g.nd; ++l) {
     if (c->sd.scheme == WD_UW && c->dist && l == 0)
       dist_uw0(c, p, c->B[l], c->F[l], c->dphi[l], st);
@@ -1194,8 +1277,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   if (c->sd.use_filter) c->fcoef = filter_coefs(sd->alpha_f);
   if (!all.empty()) {
     if (cudaMalloc(&c->factor_dev, all.size() * sizeof(double)) != cudaSuccess ||
-        cudaMemcpy(c->factor_dev, all.data(), all.size() * sizeof(double),
-                   cudaMemcpyHostToDevice) != cudaSuccess) {
+        upload_sync(c->factor_dev, all.data(), all.size() * sizeof(double)) != cudaSuccess) {
       wd_destroy(c);
       return fail(WD_ERR_CUDA, "factor upload failed");
     }

@@ -239,6 +239,20 @@ __device__ __forceinline__ long long bc_source(const Geom& g, long long idx,
   return src;
 }
 
+// Host -> device copy that has LANDED when it returns.  A plain cudaMemcpy
+// from pageable memory returns once the bytes are staged; the DMA runs on the
+// legacy stream and is not ordered against the solver's non-blocking streams,
+// so a kernel (or a communicator callback) launched right after could still
+// read the old contents.
+inline cudaError_t upload_sync(void* dst, const void* src, size_t bytes) {
+  const cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(cudaStreamLegacy);
+}
+inline cudaError_t memset_sync(void* dst, int v, size_t bytes) {
+  const cudaError_t e = cudaMemset(dst, v, bytes);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(cudaStreamLegacy);
+}
+
 // Programmatic dependent launch (sm_90+): a kernel launched with the
 // programmatic-serialization attribute may be scheduled while its predecessor
 // in the stream still runs; it must not touch anything the predecessor

@@ -411,7 +411,7 @@ int dist_f0_tables(wd_dist* d) {
       }
   }
   CK(cudaMalloc(&d->f0_dev, tab.size() * sizeof(double)));
-  CK(cudaMemcpy(d->f0_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(upload_sync(d->f0_dev, tab.data(), tab.size() * sizeof(double)));
   d->f0.tab = d->f0_dev;
   d->f0.blk = d->f0_dev + 9 * nl;
   d->f0.P = P;
@@ -574,7 +574,7 @@ int dist_p2p_setup(wd_dist* d) {
   wd_ctx* c = d->c;
   wd_comm* cm = d->comm;
   if (cudaMalloc(&d->xflags, 64) != cudaSuccess) return fail(WD_ERR_CUDA, "flag allocation failed");
-  CK(cudaMemset(d->xflags, 0, 64));
+  CK(memset_sync(d->xflags, 0, 64));
   if (cm->kind == 2 || d->P == 1) {  // alone: the slab wraps onto itself
     d->peer_ws_l = d->peer_ws_r = c->ws;
     d->xflag_l = d->xflag_r = d->xflags;
@@ -597,7 +597,7 @@ int dist_p2p_setup(wd_dist* d) {
     CK(cudaMalloc(&da, (size_t)W * d->P * sizeof(double)));
     std::vector<double> hostm(W, 0.0), hosta((size_t)W * d->P);
     std::memcpy(hostm.data(), &me, sizeof(me));
-    CK(cudaMemcpy(dm, hostm.data(), W * sizeof(double), cudaMemcpyHostToDevice));
+    CK(upload_sync(dm, hostm.data(), W * sizeof(double)));
     int rc = cm->allgather(dm, da, W, c->stream);
     if (rc == WD_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = WD_ERR_CUDA;
     if (rc == WD_OK)
@@ -676,7 +676,7 @@ int dist_pencil_factors(wd_dist* d) {
   }
   if (all.empty()) return WD_OK;
   CK(cudaMalloc(&d->fac0_dev, all.size() * sizeof(double)));
-  CK(cudaMemcpy(d->fac0_dev, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(upload_sync(d->fac0_dev, all.data(), all.size() * sizeof(double)));
   if (d->hfilt0.n) d->filt0 = factor_view(d->hfilt0, d->fac0_dev + off_f);
   if (d->hcomp0.n) d->comp0 = factor_view(d->hcomp0, d->fac0_dev + off_c);
   if (fs_m) {
@@ -943,7 +943,7 @@ int wd_dist_create(wd_comm* cm, const wd_grid_desc* gd, const wd_solver_desc* sd
     if (c->M.m && P > 1) {
       long long hf[9] = {0};
       for (int t = 0; t < 9; ++t) hf[t] = c->mterm[t];
-      if (cudaMemcpy(d->stats, hf, sizeof(hf), cudaMemcpyHostToDevice) != cudaSuccess)
+      if (upload_sync(d->stats, hf, sizeof(hf)) != cudaSuccess)
         return bail(fail(WD_ERR_CUDA, "flag upload failed"));
       if ((rc = cm->allreduce_max(d->stats, 9, c->stream))) return bail(fail(rc, cm->err));
       if (cudaMemcpyAsync(hf, d->stats, sizeof(hf), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
@@ -1054,7 +1054,7 @@ int wd_fused_filter(wd_ctx* c, int axis, const double* in, double* out, int n0, 
     if (c->sd.arith == 1 && scan_pack(F, sc, m)) packed.insert(packed.end(), sc.begin(), sc.end());
     double* dev = nullptr;
     CK(cudaMalloc(&dev, packed.size() * sizeof(double)));
-    CK(cudaMemcpy(dev, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(upload_sync(dev, packed.data(), packed.size() * sizeof(double)));
     fused_filter_prepare(n);
     F.scan_m = m;
     F.scan_off = nf;

@@ -309,12 +309,11 @@ void fused_plan(FusedPlan& fp, const FusedInputs& in) {
     fp.n_exact = exactl[0];
     const size_t nt = fastl.size() + jbl.size() + exactl.size();
     if (cudaMalloc(&fp.tiles_dev, nt * sizeof(int)) != cudaSuccess ||
-        cudaMemcpy(fp.tiles_dev, fastl.data(), fastl.size() * sizeof(int),
-                   cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(fp.tiles_dev + fastl.size(), jbl.data(), jbl.size() * sizeof(int),
-                   cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(fp.tiles_dev + fastl.size() + jbl.size(), exactl.data(),
-                   exactl.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+        upload_sync(fp.tiles_dev, fastl.data(), fastl.size() * sizeof(int)) != cudaSuccess ||
+        upload_sync(fp.tiles_dev + fastl.size(), jbl.data(), jbl.size() * sizeof(int)) !=
+            cudaSuccess ||
+        upload_sync(fp.tiles_dev + fastl.size() + jbl.size(), exactl.data(),
+                    exactl.size() * sizeof(int)) != cudaSuccess) {
       fp.active = 0;
       return;
     }

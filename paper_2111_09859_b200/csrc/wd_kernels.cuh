@@ -557,6 +557,31 @@ static __global__ void k_rk_stage(int stage, const double* __restrict__ phi,
   }
 }
 
+// Sum of divergence terms evaluated concurrently (small grids): out =
+// sum_t M[l_t, m_t] D_t in launch_divergence's order -- c D for the first
+// term, acc + c D for the others, exactly the Epi chain of the serial path.
+struct DivTerms {
+  const double* D[9];
+  int l[9], m[9];
+  int count;
+};
+template <int ND>
+static __global__ void k_div_combine(DivTerms t, Metric M, double* out, long long N,
+                                     const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      if (q >= t.count) break;
+      const double v = mget<ND>(M, t.l[q], t.m[q], idx) * t.D[q][idx];
+      s = q == 0 ? v : s + v;
+    }
+    out[idx] = s;
+  }
+}
+
 // k_tendency + k_rk_stage in one pass (the solve loop's generic path): the
 // residual is pointwise in the assembled fields, so the stage update
 // evaluates it at its source node (and at the node itself for the running

@@ -438,16 +438,16 @@ __device__ __forceinline__ double line_rhs_at(const L& w, int i, int n, int sche
 }
 
 template <int JOB>
-static __global__ void __launch_bounds__(LF_T)
-    k_line_few(const double* __restrict__ in, double* out, Geom g, int axis, int n, long long sa,
-               int per, double off, int scheme, TriDev T, Epi epi, FilterCoef fc,
-               const uint8_t* pin, int use_geom_pin, int fl, const Status* st) {
-  pdl_trigger();
-  pdl_wait();
-  if (st && st->state != WD_STATE_RUNNING) return;
+__device__ __forceinline__ void line_few_body(const double* __restrict__ in, double* out,
+                                              const Geom& g, int axis, int n, long long sa,
+                                              int per, double off, int scheme, const TriDev& T,
+                                              const Epi& epi, const FilterCoef& fc,
+                                              const uint8_t* pin, int use_geom_pin, int fl,
+                                              int block_id) {
   extern __shared__ double lf_s[];  // [fl][n] right-hand sides -> y -> x, hs[LF_MAXL], factor rows
   const long long L = g.N / n;
-  const long long q0 = (long long)blockIdx.x * fl;
+  const long long q0 = (long long)block_id * fl;
+  if (q0 >= L) return;
   const int nl = (int)min((long long)fl, L - q0);
   double* fcors = lf_s + (size_t)fl * n;
   // factor rows in shared memory: every operand of the chains is then an
@@ -677,6 +677,42 @@ static __global__ void __launch_bounds__(LF_T)
       out[idx] = p ? in[idx] : xv;
     }
   }
+}
+
+template <int JOB>
+static __global__ void __launch_bounds__(LF_T)
+    k_line_few(const double* __restrict__ in, double* out, Geom g, int axis, int n, long long sa,
+               int per, double off, int scheme, TriDev T, Epi epi, FilterCoef fc,
+               const uint8_t* pin, int use_geom_pin, int fl, const Status* st) {
+  pdl_trigger();
+  pdl_wait();
+  if (st && st->state != WD_STATE_RUNNING) return;
+  line_few_body<JOB>(in, out, g, axis, n, sa, per, off, scheme, T, epi, fc, pin, use_geom_pin, fl,
+                     blockIdx.x);
+}
+
+// Several independent compact-derivative passes in one launch (blockIdx.y =
+// pass): the axes of a gradient, or the terms of a divergence, whose chains
+// then run side by side instead of one launch after another.  Plain
+// epilogue (out = D); k_div_combine sums divergence terms afterwards.
+struct LineFewJobs {
+  const double* in[4];
+  double* out[4];
+  int axis[4];
+  TriDev T[4];
+  int count;
+};
+static __global__ void __launch_bounds__(LF_T)
+    k_line_few_multi(LineFewJobs jobs, Geom g, int scheme, int fl, const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const int j = blockIdx.y;  // select chains, not indexing: the struct stays in param space
+  const int axis = pick(jobs.axis, j);
+  const int n = pick(g.n, axis);
+  const Epi plain{0, nullptr, nullptr, 0.0};
+  FilterCoef fc;  // unused by JOB 0
+  const TriDev T = pick(jobs.T, j);
+  line_few_body<0>(pick(jobs.in, j), pick(jobs.out, j), g, axis, n, pick(g.s, axis),
+                   pick(g.per, axis), 0.0, scheme, T, plain, fc, nullptr, 0, fl, blockIdx.x);
 }
 
 __host__ __forceinline__ size_t line_few_smem(int n, int fl) {

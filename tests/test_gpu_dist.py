@@ -394,6 +394,12 @@ def _proc(rank, world, port, q):
         g2, cfg2, p2 = _cylinder("hj_curvature", "exact", 3)
         rep2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2, comm=comm)
         out["generic"] = (rep2.phi, rep2.residual_history)
+        # again in the same process: kernels are loaded now, so nothing hides
+        # a setup upload that has not landed before the first collective
+        # (the metric-term flags once raced with their all-reduce here)
+        for i in range(3):
+            rep2 = W.solve_steady(g2, W.BoundarySpec(CYL), cfg2, phi0=p2, comm=comm)
+            out[f"generic{i}"] = (rep2.phi, rep2.residual_history)
         q.put((rank, out))
         comm.close()
     finally:
@@ -428,6 +434,7 @@ def test_two_processes_torchcomm_gloo():
         assert np.allclose(hist, ref.residual_history, rtol=1e-9, atol=1e-15)
         assert same(res[r]["p2p"][0], res[r]["fused"][0])
         assert same(res[r]["p2p"][1], res[r]["fused"][1])
-        phi, hist = res[r]["generic"]
-        assert same(hist, ref2.residual_history)
-        assert same(phi, ref2.phi)
+        for key in ("generic", "generic0", "generic1", "generic2"):
+            phi, hist = res[r][key]
+            assert same(hist, ref2.residual_history), key
+            assert same(phi, ref2.phi), key
