@@ -22,6 +22,7 @@
 #include "wd_dist_filter0.cuh"
 #include "wd_deriv_scan.cuh"
 #include "wd_stage_explicit.cuh"
+#include "wd_filter_long.cuh"
 
 using namespace wd;
 
@@ -449,6 +450,7 @@ struct wd_ctx {
   TriDev comp[3], filt[3];
   ScanDev scan[3];
   ScanDev cscan[3];  // fast compact derivatives (wd_deriv_scan.cuh), per axis
+  ScanDev lscan[3];  // fast filter, 2-D lines of 513..2048 rows (wd_filter_long.cuh)
   double* factor_dev = nullptr;
   FilterCoef fcoef;
   // per-node metric sums (curvilinear) or scalars (uniform)
@@ -910,6 +912,23 @@ void enqueue_filter_bc(wd_ctx* c, double* x, double* out, const Status* st,
       cur = nxt;
       continue;
     }
+    // the same for the few long lines of a 2-D grid (wd_filter_long.cuh)
+    if (st && c->sd.arith == 1 && g.mask == nullptr && g.nd == 2 && c->lscan[a].tab &&
+        !getenv("WD_NO_GEN_SCANF")) {
+      LongScanArgs la;
+      la.in = cur;
+      la.out = nxt;
+      la.L = L;
+      la.rstride = g.s[a];
+      la.lstride = g.s[1 - a];
+      la.per = g.per[a];
+      la.T = c->lscan[a];
+      la.fc = c->fcoef;
+      la.st = st;
+      launch_filter_long(la, c->stream);
+      cur = nxt;
+      continue;
+    }
     if (line_solve_ok(g.n[a])) {
       launch_line_solve<1>(cur, nxt, nxt, g, a, g.per[a], 0.0, 0, c->filt[a], epi_plain(),
                            c->fcoef, nullptr, 1, st, c->stream);
@@ -1236,7 +1255,8 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   std::vector<double> packed, all;
   size_t off_comp[3] = {0, 0, 0}, off_filt[3] = {0, 0, 0}, off_scan[3] = {0, 0, 0};
   size_t off_cscan[3] = {0, 0, 0};
-  int scan_m[3] = {0, 0, 0}, cscan_m[3] = {0, 0, 0};
+  int scan_m[3] = {0, 0, 0}, cscan_m[3] = {0, 0, 0}, lscan_m[3] = {0, 0, 0};
+  size_t off_lscan[3] = {0, 0, 0};
   HostFactor cfast[3];
   for (int a = 0; a < g.nd; ++a) {
     if (sd->scheme == WD_C4 || sd->scheme == WD_C6) {
@@ -1271,6 +1291,13 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
         all.insert(all.end(), packed.begin(), packed.end());
       } else {
         scan_m[a] = 0;
+        if (sd->arith == 1 && g.nd == 2 && g.n[a] > FS_NMAX &&
+            scan_pack(c->hfilt[a], packed, lscan_m[a], FL_S)) {
+          off_lscan[a] = all.size();
+          all.insert(all.end(), packed.begin(), packed.end());
+        } else {
+          lscan_m[a] = 0;
+        }
       }
     }
   }
@@ -1295,6 +1322,12 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
         c->scan[a].m = scan_m[a];
         c->scan[a].tab = c->factor_dev + off_scan[a];
         c->scan[a].denom = c->hfilt[a].cyclic ? c->hfilt[a].denom : 1.0;
+      }
+      if (lscan_m[a]) {
+        c->lscan[a].n = c->hfilt[a].n;
+        c->lscan[a].m = lscan_m[a];
+        c->lscan[a].tab = c->factor_dev + off_lscan[a];
+        c->lscan[a].denom = c->hfilt[a].cyclic ? c->hfilt[a].denom : 1.0;
       }
     }
   }
@@ -1438,6 +1471,15 @@ int wd_steps(wd_ctx* c, int k) {
     if (rc) return rc;
   }
   const int parity = (int)(c->enq & 1);
+  if (getenv("WD_NO_GRAPH")) {  // plain launches (debugging, per-kernel profiling)
+    for (int s = 0; s < k; ++s) {
+      const bool even = ((parity + s) & 1) == 0;
+      enqueue_step(c, even ? c->phi : c->phiY, even ? c->phiY : c->phi);
+    }
+    CK(cudaGetLastError());
+    c->enq += k;
+    return WD_OK;
+  }
   auto key = std::make_pair(k, parity);
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {

@@ -120,6 +120,42 @@ def test_c3_bump_1025x513_e6_exact(kind):
     _check_exact(rep, div, z)
 
 
+@pytest.mark.parametrize("kind", ["hj", "eikonal"])
+def test_c3_bump_1025x513_e6_fast(kind):
+    """Fast arithmetic on config 3: lines of 1025 / 513 rows take the
+    long-line scan filter (wd_filter_long.cuh).  Against the exact mode (bit
+    identical to the oracle, above) over the golden's steps (300 / 1,033): the
+    residual history to 1e-9 relative + 1e-13 absolute (the change per step
+    falls to 1e-8, where round-off of phi ~ 0.06 shows), the field to
+    1e-10 * max|phi| (north_star)."""
+    z = goldens.load(f"base_c3_bump_{kind}_E6")
+    g = W.build_sinusoidal_bump(1025, 513, scheme="E6")
+    ex, _ = _solve(g, PLATE, z)
+    fa, _ = _solve(g, PLATE, z, arith="fast")
+    assert fa is not None and fa.iters == ex.iters
+    np.testing.assert_allclose(fa.residual_history, ex.residual_history, rtol=1e-9, atol=1e-13)
+    assert np.max(np.abs(fa.phi - ex.phi)) <= 1e-10 * float(np.max(np.abs(ex.phi)))
+
+
+@pytest.mark.parametrize("dims", [(1024, 65), (700, 67), (2048, 33)])
+def test_long_periodic_lines_fast_filter(dims):
+    """The long-line scan filter on cyclic lines (a strip periodic in x with
+    513..2048 rows per line; partial line tiles and partial segments; all
+    three register-window instantiations) on rough data."""
+    g = W.build_cartesian(*dims, Lx=dims[0] / 100.0, Ly=1.0, periodic=(True, False))
+    rng = np.random.default_rng(dims[0])
+    phi0 = 1e-3 * rng.random(dims)
+    reps = []
+    for arith in ("exact", "fast"):
+        cfg = W.SolveConfig(formulation=W.FormulationConfig(kind="hj"), scheme="E6",
+                            filter_config=W.FilterConfig(0.49), tol=1e-15, max_iters=40,
+                            arith=arith)
+        reps.append(W.solve_steady(g, W.BoundarySpec(RING), cfg, phi0=phi0))
+    ex, fa = reps
+    np.testing.assert_allclose(fa.residual_history, ex.residual_history, rtol=1e-9, atol=1e-15)
+    assert np.max(np.abs(fa.phi - ex.phi)) <= 1e-12 * max(1.0, float(np.max(np.abs(ex.phi))))
+
+
 # --------------------------------------------------------------- config 5
 @pytest.mark.parametrize("kind", ["hj_curvature", "poisson"])
 def test_c5_cylinder_128x64x32_c6_50_steps_exact(kind):
