@@ -459,6 +459,8 @@ struct wd_ctx {
   // workspace
   double* ws = nullptr;
   double* ws_generic = nullptr;  // lazily allocated (ensure_generic)
+  double* mk_dev = nullptr;      // compact metric terms (k-invariant grids, fast arithmetic)
+  Metric Mk;                     // view of mk_dev (m == nullptr: none)
   double *p, *k, *acc, *dt, *lap, *tmp, *tmp2, *gam, *phiY;
   double *advf = nullptr, *gmf = nullptr;  // generic: advection, |grad phi|
   double* uabsf = nullptr;                 // generic: sum |U_hat| for the time step
@@ -499,6 +501,10 @@ Epi epi_metric(const wd_ctx* c, int l, int m, bool first, double* acc) {
   if (c->M.m) {
     e.cfield = c->M.m + (long long)(l * c->g.nd + m) * c->g.N;
     e.cscal = 0.0;
+    if (c->Mk.m) {
+      e.ccomp = c->Mk.m + (long long)(l * c->g.nd + m) * c->Mk.N;
+      e.cdiv = c->Mk.kdiv;
+    }
   } else {
     e.cfield = nullptr;
     e.cscal = l == m ? c->M.c[l] : 0.0;
@@ -733,7 +739,7 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   for (int t = 0; t < c->g.nd * c->g.nd; ++t)
     if (c->M.m == nullptr || c->mterm[t]) nzm |= 1u << t;
   if (c->g.nd == 3)
-    k_assemble<3><<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv,
+    k_assemble<3><<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->Mk.m ? c->Mk : c->M, Uv, Uhv,
                                                                         c->g.N, 3, nzm, x, st);
   else
     k_assemble<2><<<nblocks(c->g.N, kThreads), kThreads, 0, c->stream>>>(dv, c->M, Uv, Uhv,
@@ -1006,6 +1012,32 @@ int ensure_generic(wd_ctx* c) {
     if (e != cudaSuccess) return fail(WD_ERR_CUDA, std::string("metric scan: ") + cudaGetErrorString(e));
     for (int t = 0; t < nt; ++t) c->mterm[t] = hf[t] != 0;
   }
+  // fast arithmetic, 3-D: metric terms constant along the last axis are kept
+  // once per (i, j) for the scan derivatives and the assemble kernel
+  if (c->M.m && c->sd.arith == 1 && c->g.nd == 3 && c->g.n[2] > 1 && N <= 0xffffffffLL &&
+      !c->mk_dev && !getenv("WD_NO_KMETRIC")) {
+    const int nt = 9, n2 = c->g.n[2];
+    int* fl = nullptr;
+    int hv = 1;
+    if (cudaMalloc(&fl, sizeof(int)) == cudaSuccess) {
+      cudaMemsetAsync(fl, 0, sizeof(int), c->stream);
+      k_metric_kvar<<<148 * 4, kThreads, 0, c->stream>>>(c->M.m, N, n2, nt, fl);
+      cudaMemcpyAsync(&hv, fl, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+      if (cudaStreamSynchronize(c->stream) != cudaSuccess) hv = 1;
+      cudaFree(fl);
+    }
+    cudaGetLastError();
+    const long long Nk = N / n2;
+    if (hv == 0 && cudaMalloc(&c->mk_dev, (size_t)nt * Nk * sizeof(double)) == cudaSuccess) {
+      k_metric_kgather<<<nblocks(nt * Nk, kThreads), kThreads, 0, c->stream>>>(c->M.m, c->mk_dev,
+                                                                              N, n2, nt);
+      c->Mk = c->M;
+      c->Mk.m = c->mk_dev;
+      c->Mk.N = Nk;
+      c->Mk.kdiv = n2;
+    }
+    cudaGetLastError();
+  }
   double* w = c->ws_generic;
   auto take = [&]() {
     double* r = w;
@@ -1245,6 +1277,7 @@ int wd_create(const wd_grid_desc* gd, const wd_solver_desc* sd, void* stream, wd
   c->M.m = gd->uniform ? nullptr : gd->metrics_dev;
   c->M.N = g.N;
   c->M.nd = g.nd;
+  c->M.kdiv = 0;
   for (int a = 0; a < 3; ++a) c->M.c[a] = gd->uniform ? gd->inv_spacing[a] : 0.0;
   (void)stream;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1431,6 +1464,7 @@ int wd_destroy(wd_ctx* c) {
   fused_release(c->fused);
   for (auto& kv : c->dfilt) cudaFree(kv.second.second);
   cudaFree(c->factor_dev);
+  cudaFree(c->mk_dev);
   cudaFree(c->sums_dev);
   ws_free(c->ws, (size_t)7 * c->g.N * sizeof(double));
   ws_free(c->ws_generic, (size_t)27 * c->g.N * sizeof(double));

@@ -63,8 +63,9 @@ struct Geom {
 struct Metric {
   const double* m;        // nullptr when uniform
   double c[kMaxDim];      // uniform: d xi_l / d x_l
-  long long N;
+  long long N;            // nodes per term (kdiv > 1: per compact term)
   int nd;
+  int kdiv;               // > 1: terms stored once per line of the last axis (index idx / kdiv)
   __device__ __forceinline__ double get(int l, int mm, long long idx) const {
     if (m == nullptr) return l == mm ? pick(c, l) : 0.0;
     return m[(long long)(l * nd + mm) * N + idx];

@@ -227,6 +227,9 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
     // their HBM latencies overlap instead of serialising on the store loop
     const Epi& e = a.epi;
     const bool need_acc = e.mode == 2, need_c = e.mode != 0 && e.cfield != nullptr;
+    // coefficient stored once per line of the last axis (Epi::ccomp): on the
+    // strided axes the tile's 16 lines share one value per row
+    const bool kc = e.cdiv > 1;
     auto fin = [&](double x, double av, double cv) {
       if (e.mode == 0) return x;
       const double t = cv * x;
@@ -236,7 +239,8 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
       if (l < nl) {
         const long long b = base + l + (long long)r0 * sa;
         const double* pa = e.acc + b;
-        const double* pc = e.cfield + b;
+        const long long csa = kc ? sa / e.cdiv : sa;
+        const double* pc = kc ? e.ccomp + b / e.cdiv : e.cfield + b;
         double* po = a.out + b;
 #pragma unroll
         for (int rb = 0; rb < UM; rb += 8) {
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
           for (int u = 0; u < 8; ++u) {
             const bool ok = MM > 0 || rb + u < cnt;
             av[u] = ok && need_acc ? pa[u * sa] : 0.0;
-            cv[u] = ok && need_c ? pc[u * sa] : e.cscal;
+            cv[u] = ok && need_c ? pc[u * csa] : e.cscal;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
             }
           }
           pa += 8 * sa;
-          pc += 8 * sa;
+          pc += 8 * csa;
           po += 8 * sa;
         }
       }
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
       // rows per thread and line (exact for full segments), lines per batch
       constexpr int KR = MM > 0 ? (NS * MM + TT - 1) / TT : NS * FS_M / TT;
       constexpr int LB = 8 / KR;
+      const long long cline = kc ? base / n : 0;  // first line of the tile
       for (int l0 = 0; l0 < nl; l0 += LB) {
         double av[LB][KR], cv[LB][KR];
 #pragma unroll
@@ -288,7 +293,8 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
             const bool ok = l0 + u < nl && r < n;
             const long long idx = base + (l0 + u) * lstride + r;
             av[u][k] = ok && need_acc ? e.acc[idx] : 0.0;
-            cv[u][k] = ok && need_c ? e.cfield[idx] : e.cscal;
+            // stride-1 lines are lines of the last axis: one value per line
+            cv[u][k] = ok && need_c ? (kc ? e.ccomp[cline + l0 + u] : e.cfield[idx]) : e.cscal;
           }
 #pragma unroll
         for (int u = 0; u < LB; ++u)

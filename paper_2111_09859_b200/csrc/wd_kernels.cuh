@@ -35,6 +35,11 @@ struct Epi {
   const double* acc;     // may alias out
   const double* cfield;  // per-node coefficient or nullptr
   double cscal;
+  // the same coefficient stored once per line of the last axis (metric terms
+  // of an extruded grid; index idx / cdiv), for the kernels that know of it
+  // (wd_deriv_scan.cuh); cdiv <= 1: none
+  const double* ccomp = nullptr;
+  int cdiv = 0;
   __device__ __forceinline__ double apply(double D, long long idx) const {
     if (mode == 0) return D;
     double c = cfield ? cfield[idx] : cscal;
@@ -284,6 +289,8 @@ struct AsmExtra {
 template <int ND>
 __device__ __forceinline__ double mget(const Metric& M, int l, int m, long long idx) {
   if (M.m == nullptr) return l == m ? pick(M.c, l) : 0.0;
+  if (M.kdiv > 1)  // compact terms (N < 2^32 whenever they are built)
+    return M.m[(long long)(l * ND + m) * M.N + (unsigned)idx / (unsigned)M.kdiv];
   return M.m[(long long)(l * ND + m) * M.N + idx];
 }
 
@@ -814,6 +821,38 @@ static __global__ void k_metric_nonzero(const double* __restrict__ m, long long 
        idx += (long long)gridDim.x * blockDim.x)
     nz |= !(f[idx] == 0.0);
   if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flags + blockIdx.y, 1);
+}
+
+// Metric terms that do not vary along the last axis (an O-grid extruded along
+// z: BASELINE config 5) need one value per (i, j).  Computed metrics agree
+// along such an axis only to round-off (z_k = k dz differenced: a few ulp;
+// cross terms that are analytically zero come out as 1e-13 noise), so the
+// test is |M - M_first| <= 1e-12 x the node's largest term; flag = 1 if any
+// node fails it.  The gather keeps each line's first node.  Only the
+// fast-arithmetic kernels read the compact copy (L2-resident: 4 MB per term
+// instead of 1 GB at 1024 x 512 x 256); exact arithmetic never does.
+constexpr double kKMetricTol = 1e-12;
+static __global__ void k_metric_kvar(const double* __restrict__ m, long long N, int n2, int nt,
+                                     int* flag) {
+  bool var = false;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long first = idx - idx % n2;
+    double sc = 0.0;
+    for (int t = 0; t < nt; ++t) sc = fmax(sc, fabs(m[t * N + first]));
+    for (int t = 0; t < nt; ++t)
+      var |= !(fabs(m[t * N + idx] - m[t * N + first]) <= kKMetricTol * sc);
+  }
+  if (__syncthreads_or(var) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+static __global__ void k_metric_kgather(const double* __restrict__ m, double* out, long long N,
+                                        int n2, int nt) {
+  const long long Nk = N / n2;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Nk * nt;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long t = q / Nk, j = q - t * Nk;
+    out[q] = m[t * N + j * n2];
+  }
 }
 
 // 2-D / 3-D metric inversion (grid.py:196-216).  fwd[m*d+l] = dx_m/dxi_l.
