@@ -6,6 +6,8 @@
 #include "wd_stage_fast.cuh"
 #include "wd_stage_fast4.cuh"
 
+#include <cstdlib>
+
 // interior tiles of stage s run k_f3_fast4 (two j rows per thread) when bit
 // s-1 of WD_S4 is set.  A/B (same box, 512^3): stages 3 / 4 faster with
 // fast4 (0.94 -> 0.84 / 1.04 -> 1.02 ms), stages 1 / 2 slower (1.00 -> 1.05,
@@ -142,6 +144,10 @@ void launch_fast3(int stage, F3Args a, int ntiles, const int* tiles, int chunks,
 // i-chunks for the fast3 grid: few partial waves over 2 CTAs / SM, long
 // enough chunks that the 2R-plane window prologue stays cheap
 int fast3_chunks(int ntiles, int ni) {
+  if (const char* f = getenv("WD_F3_CHUNKS")) {  // A/B of the cost model below
+    const int c = atoi(f);
+    if (c >= 1 && c <= ni) return c;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
