@@ -359,6 +359,114 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
   }
 }
 
+// k_assemble for two consecutive nodes per thread (N even): 16-byte loads and
+// stores, twice the bytes in flight per thread -- one node per thread with
+// ~150 (U only) to 400 (curvature extras) instructions left the kernel bound
+// by load latency at half occupancy (2.5-3.6 TB/s) -- and the set of
+// non-zero metric terms as a template parameter (NZ != 0: the bit tests and
+// the first-term selects of the sums fold away; NZ == 0: run-time nzm).
+// Every expression is k_assemble's, per node, so the results are identical.
+template <int ND, unsigned NZ>
+static __global__ void __launch_bounds__(256) k_assemble2(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh,
+                                                          long long N, unsigned nzm, AsmExtra x,
+                                                          const Status* st) {
+  if (st && st->state != WD_STATE_RUNNING) return;
+  const unsigned nz = NZ ? NZ : nzm;
+  const long long half = N >> 1;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < half;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long idx = 2 * q;
+    double d[ND][2], mm[ND * ND][2];
+#pragma unroll
+    for (int l = 0; l < ND; ++l) {
+      const double2 v = *reinterpret_cast<const double2*>(dphi.p[l] + idx);
+      d[l][0] = v.x;
+      d[l][1] = v.y;
+    }
+    // compact terms: idx and idx + 1 lie on one line of the last axis (kdiv even)
+    const long long mi = M.kdiv > 1 ? (long long)((unsigned)idx / (unsigned)M.kdiv) : idx;
+#pragma unroll
+    for (int t = 0; t < ND * ND; ++t) {
+      mm[t][0] = mm[t][1] = 0.0;
+      if ((nz >> t) & 1u) {
+        if (M.m == nullptr) {
+          mm[t][0] = mm[t][1] = (t / ND == t % ND) ? pick(M.c, t / ND) : 0.0;
+        } else if (M.kdiv > 1) {
+          mm[t][0] = mm[t][1] = M.m[(long long)t * M.N + mi];
+        } else {
+          const double2 v = *reinterpret_cast<const double2*>(M.m + (long long)t * M.N + idx);
+          mm[t][0] = v.x;
+          mm[t][1] = v.y;
+        }
+      }
+    }
+    double u[ND][2], uh[ND][2], adv[2] = {0.0, 0.0}, ua[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0};
+    double nr[ND][2];
+    const bool second = Uh.p[0] != nullptr || x.adv || x.uabs;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+#pragma unroll
+      for (int m = 0; m < ND; ++m) {
+        double sacc = 0.0;
+        bool any = false;
+#pragma unroll
+        for (int l = 0; l < ND; ++l)
+          if ((nz >> (l * ND + m)) & 1u) {
+            const double t = mm[l * ND + m][e] * d[l][e];
+            sacc = any ? sacc + t : t;
+            any = true;
+          }
+        u[m][e] = sacc;
+      }
+      if (second) {
+#pragma unroll
+        for (int l = 0; l < ND; ++l) {
+          double sacc = 0.0;
+          bool any = false;
+#pragma unroll
+          for (int m = 0; m < ND; ++m)
+            if ((nz >> (l * ND + m)) & 1u) {
+              const double t = mm[l * ND + m][e] * u[m][e];
+              sacc = any ? sacc + t : t;
+              any = true;
+            }
+          uh[l][e] = sacc;
+          if (x.adv) {
+            const double t = sacc * d[l][e];
+            adv[e] = l == 0 ? t : adv[e] + t;
+          }
+          ua[e] = l == 0 ? fabs(sacc) : ua[e] + fabs(sacc);
+        }
+      }
+      if (x.gm) {
+        double sq = 0.0;
+#pragma unroll
+        for (int m = 0; m < ND; ++m) sq = m == 0 ? u[0][e] * u[0][e] : sq + u[m][e] * u[m][e];
+        gm[e] = sqrt(sq);
+        if (x.nrm.p[0])
+#pragma unroll
+          for (int m = 0; m < ND; ++m) nr[m][e] = u[m][e] / (gm[e] + x.eps0);
+      }
+    }
+    auto put = [&](double* f, const double v[2]) {
+      *reinterpret_cast<double2*>(f + idx) = make_double2(v[0], v[1]);
+    };
+#pragma unroll
+    for (int m = 0; m < ND; ++m) put(U.p[m], u[m]);
+    if (second && Uh.p[0] != nullptr)
+#pragma unroll
+      for (int l = 0; l < ND; ++l) put(Uh.p[l], uh[l]);
+    if (x.adv) put(x.adv, adv);
+    if (x.uabs) put(x.uabs, ua);
+    if (x.gm) {
+      put(x.gm, gm);
+      if (x.nrm.p[0])
+#pragma unroll
+        for (int m = 0; m < ND; ++m) put(x.nrm.p[m], nr[m]);
+    }
+  }
+}
+
 // Curvature normal n_m = U_m / (|U| + eps0) (formulations.py:212-214).
 static __global__ void k_normal(Vec3 U, MVec3 nrm, long long N, int nd, double eps0,
                          const Status* st) {

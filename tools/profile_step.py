@@ -3,7 +3,7 @@
 for `ncu --profile-from-start off` (launch lists and full captures of exactly
 the profiled steps).
 
-  python tools/profile_step.py [--case c4|c1|c2|c3|c5] [--arith fast|exact]
+  python tools/profile_step.py [--case c4|c1|c2|c3|c5|c5p] [--arith fast|exact]
                                [--n 512] [--steps 1]
 """
 import argparse
@@ -28,6 +28,11 @@ def case(name, n):
     if name == "c3":
         return (W.build_sinusoidal_bump(1025, 513, scheme="E6"), plate, "E6",
                 W.FormulationConfig(kind="hj"), W.FilterConfig(0.49))
+    if name == "c5p":
+        faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield",
+                 "kmin": "periodic", "kmax": "periodic"}
+        return (W.build_cylinder(1024, 512, 256, scheme="C6"), faces, "C6",
+                W.FormulationConfig(kind="poisson"), W.FilterConfig(0.48))
     if name == "c5":
         faces = {"imin": "periodic", "imax": "periodic", "jmin": "wall", "jmax": "farfield",
                  "kmin": "periodic", "kmax": "periodic"}
