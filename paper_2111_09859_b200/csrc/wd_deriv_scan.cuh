@@ -73,7 +73,11 @@ __global__ void __launch_bounds__(TT, TT == 256 ? 2 : 1) k_deriv_scan(DScanArgs 
   constexpr int NS = TT / NL;
   constexpr bool TG = NL == 8;            // tables from global (L1)
   constexpr int UM = MM > 0 ? MM : FS_M;  // unrolled rows per segment
-  const int n = a.T.n, m = MM > 0 ? MM : a.T.m;
+  // full-segment tiles: n = NS * MM is a compile-time constant (dscan_pick),
+  // which folds the tile / table offsets and the row bounds
+  // (not the 512-thread n = 1024 tiles: at their 128-register cap the extra
+  // constant propagation spills and measured 774 -> 808 us per pass)
+  const int n = (MM > 0 && TT == 256) ? (TT / NL) * MM : a.T.n, m = MM > 0 ? MM : a.T.m;
   constexpr bool per = PER;
   const double* tb = TG ? a.T.tab : ds_smem;
   const double2* T1 = reinterpret_cast<const double2*>(tb);  // (fm, h)

@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(FS_T, WD_SCAN_MINB)
   extern __shared__ __align__(128) double fs_smem[];
   constexpr bool kTma = TMA && !AX2 && MM > 0;
   __shared__ __align__(8) unsigned long long tbar[2];
-  const int n = a.T.n, m = a.T.m, per = a.per;
+  // full-segment tiles: n = FS_S * MM at compile time (scan dispatch, wd_fused.cu)
+  const int n = MM > 0 ? FS_S * MM : a.T.n, m = MM > 0 ? MM : a.T.m, per = a.per;
   // tables: T1 (fm, h), T2 (P, g), T4 (Q, z) as double2; T3 rinv
   const double* tb = WD_SCAN_TG ? a.T.tab : fs_smem;
   const double2* T1 = reinterpret_cast<const double2*>(tb);
