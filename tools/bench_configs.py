@@ -48,7 +48,7 @@ def words(nd, filt, uniform):
     return 21 + (2 * nd if filt else 0) + 1 + (0 if uniform else 4 * nd * nd)
 
 
-def measure(name, spec, K, Wm, arith, peak):
+def measure(name, spec, K, Wm, arith, peak, prepass=True):
     import torch
     from paper_2111_09859_b200 import _context, _native as nat
     grid, faces, scheme, fc, filt, label = spec
@@ -60,7 +60,7 @@ def measure(name, spec, K, Wm, arith, peak):
     # latency-bound small grids: one untimed pass of the same K-step graph
     # first, so the timed pass sees settled clocks (a C2 exact step measured
     # 0.78 / 0.97 / 1.21 ms depending on what ran before it with 3 warm-up steps)
-    pre = K if N < 2_000_000 else 0
+    pre = K if (N < 2_000_000 and prepass) else 0
     hist = torch.zeros(K + pre + Wm + 8, dtype=torch.float64, device="cuda")
     nat.check(ctx.lib.wd_bind(ctx.ptr, phi.data_ptr(), hist.data_ptr()))
     stream = ctx.stream()
@@ -160,6 +160,12 @@ def main():
             if arith == "fast" and name == "c4exact":
                 continue
             r = measure(name, spec, K, args.warmup, arith, peak)
+            if r["state"] != 0:
+                # the run stopped inside the untimed pre-pass (HJ-LAD on C3
+                # diverges from phi = 0 after ~1,500 steps, as in the
+                # reference): time the first K steps instead
+                r = measure(name, spec, K, args.warmup, arith, peak, prepass=False)
+                r["note"] = "no pre-pass: the iteration leaves RUNNING within 2K steps"
             print(json.dumps(r), flush=True)
             rows.append(r)
     if "oracle" in args.cases.split(","):
