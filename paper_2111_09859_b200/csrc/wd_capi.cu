@@ -741,7 +741,7 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   // the full metric fields even when a compact copy exists (c->Mk): measured
   // at 1024 x 512 x 256, this kernel runs 2.68 ms with the 16-byte loads of the
   // full terms and 3.81 ms with the broadcast loads of the compact ones
-  const Metric& Mu = c->M;
+  const Metric& Mu = (c->Mk.m && getenv("WD_ASM_COMPACT")) ? c->Mk : c->M;
   const long long N = c->g.N;
   // two nodes per thread when the pairs are 16-byte aligned and, for compact
   // terms, never straddle two lines of the last axis
