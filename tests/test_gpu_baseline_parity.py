@@ -196,3 +196,37 @@ def test_c5_cylinder_64x32x16_c6_converged_exact(kind):
     rep, div = _solve(g, CYL, z)
     _check_exact(rep, div, z)
     assert np.array_equal(rep.phi, z["phi"])
+
+
+# ------------------------------------------------- kernel variants, A/B
+@pytest.mark.parametrize("kind", ["hj_curvature", "poisson", "hj_lad"])
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_two_node_assemble_kernel_is_bit_identical(kind, arith, monkeypatch):
+    """k_assemble2 (two nodes per thread, compile-time non-zero-term pattern)
+    evaluates k_assemble's expressions: the same solve with WD_NO_ASM2=1 must
+    agree bit for bit in either arithmetic (the extruded-grid pattern on the
+    cylinder, the full pattern on a sheared grid)."""
+    from paper_2111_09859_b200 import _context
+    for build in ("cyl", "full"):
+        reps = []
+        for off in (False, True):
+            if off:
+                monkeypatch.setenv("WD_NO_ASM2", "1")
+            else:
+                monkeypatch.delenv("WD_NO_ASM2", raising=False)
+            _context.drop_cached()
+            g = W.build_cylinder(32, 16, 12, scheme="C6")
+            if build == "full":  # shear z with x: every metric term becomes non-zero
+                c = np.array(g.coords, copy=True)
+                c[2] = c[2] + 0.05 * c[0] + 0.03 * c[1]
+                g = W.compute_metrics(W.CurvilinearGrid(coords=c, periodic=g.periodic,
+                                                        periods=g.periods), "C6")
+            cfg = W.SolveConfig(formulation=W.FormulationConfig(kind=kind), scheme="C6",
+                                filter_config=W.FilterConfig(0.48), tol=1e-15, max_iters=4,
+                                arith=arith)
+            d = np.sqrt(g.coords[0] ** 2 + g.coords[1] ** 2) - 0.5
+            reps.append(W.solve_steady(g, W.BoundarySpec(CYL), cfg, phi0=0.5 * d))
+        monkeypatch.delenv("WD_NO_ASM2", raising=False)
+        a, b = reps
+        assert np.array_equal(a.residual_history, b.residual_history), build
+        assert np.array_equal(a.phi, b.phi), build
