@@ -741,7 +741,11 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   // the full metric fields even when a compact copy exists (c->Mk): measured
   // at 1024 x 512 x 256, this kernel runs 2.68 ms with the 16-byte loads of the
   // full terms and 3.81 ms with the broadcast loads of the compact ones
-  const Metric& Mu = (c->Mk.m && getenv("WD_ASM_COMPACT")) ? c->Mk : c->M;
+  // ... except the U-only instantiation (Poisson): at three times the
+  // resident warps it gains from the five reads it drops, 1.70 -> 1.33 ms
+  const bool uonly = Uhv.p[0] == nullptr && !x.adv && !x.uabs && !x.gm &&
+                     !getenv("WD_NO_ASM_UONLY");
+  const Metric& Mu = (c->Mk.m && (uonly || getenv("WD_ASM_COMPACT"))) ? c->Mk : c->M;
   const long long N = c->g.N;
   // two nodes per thread when the pairs are 16-byte aligned and, for compact
   // terms, never straddle two lines of the last axis
@@ -751,6 +755,15 @@ void launch_assemble(wd_ctx* c, double* const d[3], double* const U[3], double* 
   if (N % 2 == 0 && (al & 15) == 0 && (Mu.kdiv <= 1 || Mu.kdiv % 2 == 0) &&
       !getenv("WD_NO_ASM2")) {
     const int nb = nblocks(N / 2, 256);
+    if (uonly && c->g.nd == 3) {
+      if (nzm == 0x1FFu)
+        k_assemble2<3, 0x1FFu, true><<<nb, 256, 0, c->stream>>>(dv, Mu, Uv, Uhv, N, nzm, x, st);
+      else if (nzm == 0x11Bu)
+        k_assemble2<3, 0x11Bu, true><<<nb, 256, 0, c->stream>>>(dv, Mu, Uv, Uhv, N, nzm, x, st);
+      else
+        k_assemble2<3, 0u, true><<<nb, 256, 0, c->stream>>>(dv, Mu, Uv, Uhv, N, nzm, x, st);
+      return;
+    }
     if (c->g.nd == 3) {
       if (nzm == 0x1FFu)
         k_assemble2<3, 0x1FFu><<<nb, 256, 0, c->stream>>>(dv, Mu, Uv, Uhv, N, nzm, x, st);

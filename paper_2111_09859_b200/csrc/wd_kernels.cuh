@@ -366,7 +366,10 @@ static __global__ void k_assemble(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh, long l
 // non-zero metric terms as a template parameter (NZ != 0: the bit tests and
 // the first-term selects of the sums fold away; NZ == 0: run-time nzm).
 // Every expression is k_assemble's, per node, so the results are identical.
-template <int ND, unsigned NZ>
+// UONLY: only U is wanted (Poisson, the UW Laplacian's E2 gradient): the
+// instantiation carries none of the optional outputs' registers (40 instead
+// of ~100: three times the resident warps).
+template <int ND, unsigned NZ, bool UONLY = false>
 static __global__ void __launch_bounds__(256) k_assemble2(Vec3 dphi, Metric M, MVec3 U, MVec3 Uh,
                                                           long long N, unsigned nzm, AsmExtra x,
                                                           const Status* st) {
@@ -402,7 +405,7 @@ static __global__ void __launch_bounds__(256) k_assemble2(Vec3 dphi, Metric M, M
     }
     double u[ND][2], uh[ND][2], adv[2] = {0.0, 0.0}, ua[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0};
     double nr[ND][2];
-    const bool second = Uh.p[0] != nullptr || x.adv || x.uabs;
+    const bool second = !UONLY && (Uh.p[0] != nullptr || x.adv || x.uabs);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
 #pragma unroll
@@ -438,7 +441,7 @@ static __global__ void __launch_bounds__(256) k_assemble2(Vec3 dphi, Metric M, M
           ua[e] = l == 0 ? fabs(sacc) : ua[e] + fabs(sacc);
         }
       }
-      if (x.gm) {
+      if (!UONLY && x.gm) {
         double sq = 0.0;
 #pragma unroll
         for (int m = 0; m < ND; ++m) sq = m == 0 ? u[0][e] * u[0][e] : sq + u[m][e] * u[m][e];
@@ -453,6 +456,7 @@ static __global__ void __launch_bounds__(256) k_assemble2(Vec3 dphi, Metric M, M
     };
 #pragma unroll
     for (int m = 0; m < ND; ++m) put(U.p[m], u[m]);
+    if (UONLY) continue;
     if (second && Uh.p[0] != nullptr)
 #pragma unroll
       for (int l = 0; l < ND; ++l) put(Uh.p[l], uh[l]);
