@@ -811,15 +811,37 @@ static __global__ void k_bc_change(const double* __restrict__ in, double* out,
   if (st->state != WD_STATE_RUNNING) return;
   double md = 0.0, ma = 0.0;
   int bad = 0;
+  // four nodes a grid stride apart per iteration, their loads issued before
+  // any store (one node per iteration: 1.12 ms for 3 words at 1024 x 512 x 256)
+  constexpr int U = 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < g.N;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int c[kMaxDim];
-    node_coords(g, idx, c);
-    const double v = is_pinned(g, idx, c) ? 0.0 : in[bc_source(g, idx, c)];
-    out[idx] = v;
-    if (!isfinite(v)) bad = 1;
-    ma = fmax(ma, fabs(v));
-    if (g.mask == nullptr || g.mask[idx] == 0) md = fmax(md, fabs(v - old[idx]));
+       idx += U * stride) {
+    double v[U], o[U];
+    bool cmp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = idx + u * stride;
+      v[u] = o[u] = 0.0;
+      cmp[u] = false;
+      if (i < g.N) {
+        int c[kMaxDim];
+        node_coords(g, i, c);
+        v[u] = is_pinned(g, i, c) ? 0.0 : in[bc_source(g, i, c)];
+        cmp[u] = g.mask == nullptr || g.mask[i] == 0;
+        if (cmp[u]) o[u] = old[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = idx + u * stride;
+      if (i < g.N) {
+        out[i] = v[u];
+        if (!isfinite(v[u])) bad = 1;
+        ma = fmax(ma, fabs(v[u]));
+        if (cmp[u]) md = fmax(md, fabs(v[u] - o[u]));
+      }
+    }
   }
   md = warp_max(md);
   ma = warp_max(ma);
